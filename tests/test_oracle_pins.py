@@ -1,0 +1,450 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (not against itself).
+
+Each test names the passage it pins.  P = /root/reference/PAPER.md line, S = SPEC.md line
+(the reference is not read at run time; the worked values live in tests/golden/).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import phantoms as P
+from oracle import alm, brute
+from oracle import energy as E
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+RNG = np.random.default_rng(1234)
+
+
+def _S_of(inp):
+    """Capacity per node id as the oracle sees it (fp32 inputs widened to fp64)."""
+    S = np.zeros((inp.graph.num_nodes,) + inp.shape)
+    for v in range(1, inp.graph.num_nodes):
+        S[v] = inp.s_fields()[v]
+    return S
+
+
+def _vol1d(a):
+    return np.asarray(a, dtype=np.float64).reshape(1, 1, -1)
+
+
+# ---------------------------------------------------------------- P1 operators
+@pytest.mark.parametrize("ex", GOLD["grad_1d"])
+def test_grad_examples(ex):
+    g = O.grad(_vol1d(ex["f"]), 0, 2)
+    assert np.array_equal(g.ravel(), np.asarray(ex["grad"], float))
+
+
+@pytest.mark.parametrize("ex", GOLD["div_1d"])
+def test_div_examples(ex):
+    q = np.zeros((2, 1, 1, len(ex["q"])))
+    q[0, 0, 0] = ex["q"]
+    assert np.array_equal(O.div(q, 2).ravel(), np.asarray(ex["div"], float))
+
+
+@pytest.mark.parametrize("ex", GOLD["project_l2"])
+def test_project_examples(ex):
+    q = np.asarray(ex["q"], float).reshape(2, 1, 1, 1)
+    out = O.project(q, np.full((1, 1, 1), ex["S"], float), 2, O.CAP_L2)
+    np.testing.assert_allclose(out.ravel(), ex["out"], rtol=0, atol=1e-15)
+
+
+def test_project_box_and_idempotence():
+    q = RNG.normal(size=(3, 4, 5, 6))
+    S = np.abs(RNG.normal(size=(4, 5, 6)))
+    S[0, 0, 0] = 0.0
+    for cap in (O.CAP_L2, O.CAP_LINF):
+        p1 = O.project(q, S, 3, cap)
+        p2 = O.project(p1, S, 3, cap)
+        np.testing.assert_allclose(p2, p1, rtol=4e-16, atol=0)   # idempotent up to one rounding
+        nrm = np.sqrt((p1 ** 2).sum(0)) if cap == O.CAP_L2 else np.abs(p1).max(0)
+        assert np.all(nrm <= S * (1 + 1e-15) + 1e-300)      # feasible
+    box = O.project(q, S, 3, O.CAP_LINF)
+    assert np.array_equal(box, np.clip(q, -S, S))
+
+
+@pytest.mark.parametrize("shape,ndim", [((1, 7, 9), 2), ((5, 6, 7), 3), ((1, 1, 4), 2), ((3, 1, 2), 3)])
+def test_adjointness(shape, ndim):
+    """<nabla u, q> = -<u, div q> when q^k(last) = 0 (reading R4 fixes S:62)."""
+    u = RNG.normal(size=shape)
+    q = RNG.normal(size=(ndim,) + shape)
+    for k, ax in zip(range(ndim), (2, 1, 0)):
+        sl = [slice(None)] * 3
+        sl[ax] = -1
+        q[k][tuple(sl)] = 0.0
+    lhs = sum(float(np.sum(O.grad(u, k, ndim) * q[k])) for k in range(ndim))
+    rhs = -float(np.sum(u * O.div(q, ndim)))
+    assert abs(lhs - rhs) <= 1e-10 * (1 + abs(lhs))
+    # the numpy copies in energy.py obey the same identities
+    lhs2 = float(np.sum(E.grad(u, ndim) * q))
+    assert abs(lhs2 - lhs) <= 1e-12 * (1 + abs(lhs))
+    assert np.allclose(E.div(q, ndim), O.div(q, ndim), rtol=0, atol=1e-14)
+
+
+def test_grad_constant_zero():
+    assert np.all(O.grad(np.full((3, 4, 5), 2.5), 2, 3) == 0)
+
+
+# ---------------------------------------------------------------- P2 single voxel
+def _single_voxel(d_over_c, c=0.25, shift=O.SHIFT_MIN, dag=False):
+    K = len(d_over_c)
+    D = (np.asarray(d_over_c, float) * c).reshape(K, 1, 1, 1)
+    S = np.zeros((K, 1, 1, 1))
+    u, q = O.init_state(K, K, (1, 1, 1), 2)
+    if dag:
+        g = P.potts_graph(K)
+        O.dag_iterate(g.num_nodes, g.parent, g.child, g.weight, D, np.concatenate([np.zeros((1, 1, 1, 1)), S]),
+                      u, q, 2, c, 0.1, 1, shift)
+    else:
+        O.potts_iterate(D, S, u, q, 2, c, 0.1, 1, shift)
+    return u.ravel()
+
+
+@pytest.mark.parametrize("dag", [False, True])
+@pytest.mark.parametrize("shift", [O.SHIFT_MIN, O.SHIFT_NONE])
+def test_single_voxel_label_update(dag, shift):
+    """Eq. 7: (0.5, 0.5), d = (0, c ln 2) -> (2/3, 1/3)  (golden: S:222)."""
+    ex = GOLD["single_voxel_update"]
+    u = _single_voxel(ex["d_over_c_times"], dag=dag, shift=shift)
+    np.testing.assert_allclose(u, ex["u1"], rtol=1e-15, atol=0)
+
+
+# ---------------------------------------------------------------- P3/P12 closed forms
+@pytest.mark.parametrize("shift", [O.SHIFT_MIN, O.SHIFT_NONE])
+def test_zero_smoothness_closed_form(shift):
+    """S = 0 => q stays 0 and u^t_L = exp(-t D_L/c)/sum_L' exp(-t D_L'/c) (Eq. 7 iterated)."""
+    c, K = 0.25, 4
+    D = RNG.uniform(0, 1, size=(K, 3, 4, 5))
+    S = np.zeros_like(D)
+    u, q = O.init_state(K, K, D.shape[1:], 3)
+    for t in range(1, 31):
+        O.potts_iterate(D, S, u, q, 3, c, 0.1, 1, shift)
+        z = -t * D / c
+        ref = np.exp(z - z.max(0)) / np.exp(z - z.max(0)).sum(0)
+        np.testing.assert_allclose(u, ref, rtol=1e-12, atol=1e-300)
+        assert np.all(q == 0)
+
+
+def test_softmin_concentration():
+    """c -> 0 concentrates u on argmin_L d_L: max u > 0.99 at c = 0.1 with gap >= 1."""
+    K = 5
+    D = RNG.uniform(0, 1, size=(K, 2, 3, 4))
+    best = np.argmin(D, axis=0)
+    D = D + 1.0
+    np.put_along_axis(D, best[None], np.take_along_axis(D, best[None], 0) - 1.0 - 0.0, axis=0)
+    for c in (1.0, 0.5, 0.25, 0.1):
+        u, q = O.init_state(K, K, D.shape[1:], 3)
+        O.potts_iterate(D, np.zeros_like(D), u, q, 3, c, 0.1, 1)
+        ref = np.exp(-D / c) / np.exp(-D / c).sum(0)
+        np.testing.assert_allclose(u, ref, rtol=1e-12)
+    assert np.all(u.max(0) > 0.99) and np.array_equal(np.argmax(u, 0), best)
+
+
+@pytest.mark.parametrize("kind", ["potts", "hmf", "dag"])
+def test_uniform_data_gives_constant_solution(kind):
+    """Spatially uniform D_L(x) = delta_L: u~ uniform in x => nabla u~ = 0 => q stays 0 and u(x) is
+    constant in x and equal to the S = 0 softmax (BJ north_star)."""
+    g = {"potts": P.potts_graph(4), "hmf": P.hmf_graph(), "dag": P.dag_graph()}[kind]
+    NL = len(g.leaves())
+    delta = RNG.uniform(0, 1, size=NL)
+    shape = (4, 5, 6)
+    D = np.ascontiguousarray(np.broadcast_to(delta[:, None, None, None], (NL,) + shape))
+    S = RNG.uniform(0.01, 0.2, size=(g.num_nodes,) + shape)
+    u, q = O.init_state(NL, g.num_nodes - 1, shape, 3)
+    c = 0.25
+    T = 12
+    if kind == "potts":
+        O.potts_iterate(D, np.ascontiguousarray(S[1:]), u, q, 3, c, 0.1, T)
+    else:
+        O.dag_iterate(g.num_nodes, g.parent, g.child, g.weight, D, S, u, q, 3, c, 0.1, T)
+    assert np.all(q == 0)
+    assert np.all(u == u[:, :1, :1, :1])           # bitwise constant in x
+    z = -T * delta / c
+    np.testing.assert_allclose(u[:, 0, 0, 0], np.exp(z - z.max()) / np.exp(z - z.max()).sum(), rtol=1e-12)
+
+
+def test_symmetric_data_keeps_uniform():
+    """D identical across labels => uniform u stays uniform."""
+    K = 3
+    D = np.repeat(RNG.uniform(0, 1, size=(1, 5, 6, 7)), K, axis=0)
+    S = np.full_like(D, 0.1)
+    u, q = O.init_state(K, K, D.shape[1:], 3)
+    O.potts_iterate(D, S, u, q, 3, 0.25, 0.1, 20)
+    np.testing.assert_allclose(u, 1.0 / K, rtol=1e-14)
+
+
+# ---------------------------------------------------------------- P10 DAG machinery
+def _dag_one_step_leaf_ratio(nn, edges, divs, D_leaves, c=0.25):
+    """Run one Alg. 2 iteration on a 2-voxel 1D grid whose voxel 0 has div q_v = divs[v];
+    returns u at voxel 0 (S = 0 so the flow step does not matter)."""
+    par = [e[0] for e in edges]; chi = [e[1] for e in edges]; w = [e[2] for e in edges]
+    leaves = [v for v in range(1, nn) if v not in par]
+    q = np.zeros((nn - 1, 2, 1, 1, 2))
+    for v, dv in divs.items():
+        q[v - 1, 0, 0, 0, 0] = dv      # div at voxel 0 = q(0) - 0 = dv
+    D = np.zeros((len(leaves), 1, 1, 2))
+    for slot, v in enumerate(leaves):
+        D[slot, 0, 0, :] = D_leaves.get(v, 0.0)
+    u = np.full(D.shape, 1.0 / len(leaves))
+    O.dag_iterate(nn, par, chi, w, D, np.zeros((nn, 1, 1, 2)), u, q, 2, c, 0.1, 1)
+    return leaves, u[:, 0, 0, 0]
+
+
+def test_chain_excess_example():
+    """d recursion, golden S:287: chain S->A->B gives d_A = 0.1, d_B = 1.3.
+    Observed through the softmax against a sibling end label E under S (d_E = D_E = 0)."""
+    ex = GOLD["chain_excess"]
+    c = 0.25
+    leaves, u = _dag_one_step_leaf_ratio(4, [(0, 1, 1.0), (1, 2, 1.0), (0, 3, 1.0)],
+                                         {1: ex["div_A"], 2: ex["div_B"]}, {2: ex["D_B"], 3: 0.0}, c)
+    assert leaves == [2, 3]
+    assert math.isclose(u[0] / u[1], math.exp(-(ex["d_B"] - 0.0) / c), rel_tol=1e-12)
+
+
+def test_diamond_excess_example():
+    """golden S:289: diamond with w = 0.5, div q_A = div q_B = 1, D_C = 0 gives d_C = 1.0."""
+    ex = GOLD["diamond_excess"]
+    c = 0.25
+    leaves, u = _dag_one_step_leaf_ratio(5, [(0, 1, 1.0), (0, 2, 1.0), (1, 3, 0.5), (2, 3, 0.5), (0, 4, 1.0)],
+                                         {1: ex["div_A"], 2: ex["div_B"], 3: ex["div_C"]}, {3: ex["D_C"], 4: 0.0}, c)
+    assert leaves == [3, 4]
+    assert math.isclose(u[0] / u[1], math.exp(-ex["d_C"] / c), rel_tol=1e-12)
+
+
+@pytest.mark.parametrize("gname", ["hmf", "dag"])
+def test_bottom_up_mass_and_flow_step(gname):
+    """First iteration from q = 0 with huge capacities: q_v = -c tau nabla M_v where
+    M_v = sum_B W_(v,B) u_B exp(-(D_B - m)/c) (Eq. 16, W of P:199-209, listing P:291-301)."""
+    g = P.hmf_graph() if gname == "hmf" else P.dag_graph()
+    NL = len(g.leaves())
+    shape = (3, 4, 5)
+    D = RNG.uniform(0, 1, size=(NL,) + shape)
+    S = np.full((g.num_nodes,) + shape, 1e6)
+    c, tau = 0.25, 0.1
+    u, q = O.init_state(NL, g.num_nodes - 1, shape, 3)
+    O.dag_iterate(g.num_nodes, g.parent, g.child, g.weight, D, S, u, q, 3, c, tau, 1)
+    m = D.min(0)
+    mass = (1.0 / NL) * np.exp(-(D - m) / c)
+    W = brute.path_weights(g.num_nodes, g.parent, g.child, g.weight)
+    for v in range(1, g.num_nodes):
+        M = np.tensordot(W[v], mass, axes=1)
+        ref = -c * tau * E.grad(M, 3)
+        np.testing.assert_allclose(q[v - 1], ref, rtol=1e-12, atol=1e-15)
+
+
+def test_star_dag_equals_potts_bitwise():
+    """The star DAG reduces Alg. 2 to Alg. 1: identical iterates, bit for bit."""
+    inp = P.generate(P.config("C1").resized(19, 13, 1))
+    for shift in (O.SHIFT_MIN, O.SHIFT_NONE):
+        D = inp.D.astype(np.float64)
+        S = _S_of(inp)
+        u1, q1 = O.init_state(3, 3, inp.shape, 2)
+        u2, q2 = O.init_state(3, 3, inp.shape, 2)
+        O.potts_iterate(D, np.ascontiguousarray(S[1:]), u1, q1, 2, 0.25, 0.1, 50, shift)
+        g = P.potts_graph(3)
+        O.dag_iterate(4, g.parent, g.child, g.weight, D, S, u2, q2, 2, 0.25, 0.1, 50, shift)
+        assert np.array_equal(u1, u2) and np.array_equal(q1, q2)
+
+
+@pytest.mark.parametrize("ex", GOLD["path_weight"])
+def test_path_weights(ex):
+    """W_(A,B), golden S:157-158."""
+    if "chain" in ex["graph"]:
+        W = brute.path_weights(4, [0, 1, 0], [1, 2, 3], [0.7, 0.5, 1.0])
+        assert math.isclose(W[0, 0], ex["W_SB"], rel_tol=1e-15)
+    else:
+        W = brute.path_weights(5, [0, 0, 1, 2, 0], [1, 2, 3, 3, 4], [0.5, 0.5, 0.5, 0.5, 1.0])
+        assert math.isclose(W[0, 0], ex["W_SC"], rel_tol=1e-15)
+
+
+def test_config_graphs_have_unit_source_weight():
+    """Reading R9: sum_{L} u_L = 1 <=> u_S = 1 needs W_(S,L) = 1 for every end label."""
+    for g in (P.hmf_graph(), P.dag_graph(), P.potts_graph(5)):
+        W = brute.path_weights(g.num_nodes, g.parent, g.child, g.weight)
+        np.testing.assert_allclose(W[0], 1.0, rtol=1e-15)
+
+
+def test_topological_order():
+    """O with lowest-id tie-break."""
+    assert O.topo_order(3, [0, 0], [1, 2], [1, 1]) == [0, 1, 2]
+    o = O.topo_order(4, [0, 0, 1, 2], [1, 2, 3, 3], [1, 1, .5, .5])
+    assert o[-1] == 3 and o[0] == 0
+    assert O.topo_order(3, [0, 1, 2], [1, 2, 1], [1, 1, 1]) is None       # cycle
+    o = O.topo_order(10, P.dag_graph().parent, P.dag_graph().child, P.dag_graph().weight)
+    assert o == [0, 1, 2, 3, 4, 5, 6, 7, 8, 9]
+
+
+# ---------------------------------------------------------------- P5/P6 invariants over iterations
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s"])
+def test_feasibility_and_weak_duality_every_iteration(name):
+    """After every iteration: sum_L u_L = 1, u >= 0 (P:342 'constrains intermediate segmentations to be
+    feasible'), |q_v| <= S_v, q^k(last) = 0, and E(u) - F(q) >= 0 (weak duality from P:86-106)."""
+    base = {"C1": P.config("C1"), "C2s": P.config("C2").resized(12, 10, 9), "C3s": P.config("C3").resized(10, 9, 8),
+            "C4s": P.config("C4").resized(9, 10, 8)}[name]
+    inp = P.generate(base)
+    g = inp.graph
+    nd = base.ndim
+    D = inp.D.astype(np.float64)
+    S = np.zeros((g.num_nodes,) + inp.shape)
+    for v in range(1, g.num_nodes):
+        S[v] = inp.s_fields()[v]
+    u, q = O.init_state(D.shape[0], g.num_nodes - 1, inp.shape, nd)
+    gaps = []
+    for t in range(60):
+        O.run_inputs(inp, 1, state=(u, q))
+        assert np.all(u >= 0)
+        np.testing.assert_allclose(u.sum(0), 1.0, rtol=0, atol=1e-12)
+        nrm = np.sqrt((q ** 2).sum(1))
+        assert np.all(nrm <= S[1:] * (1 + 1e-12) + 1e-300)
+        for k, ax in zip(range(nd), (2, 1, 0)):
+            sl = [slice(None)] * 3
+            sl[ax] = -1
+            assert np.all(q[:, k][(slice(None),) + tuple(sl)] == 0)
+        e = E.primal(u, D, S, g.num_nodes, g.parent, g.child, g.weight, nd, "l2")
+        f = E.dual(q, D, g.num_nodes, g.parent, g.child, g.weight, nd)
+        assert e - f >= -1e-9 * abs(e)
+        gaps.append(e - f)
+    assert gaps[-1] < 0.5 * gaps[0]
+
+
+# ---------------------------------------------------------------- convergence of the fixed point
+def test_gap_converges_to_zero_shift_min():
+    """With the SHIFT_MIN reading (R1) the iteration reaches the saddle point of Eq. 3 / Eq. 4: gap -> 0."""
+    inp = P.generate(P.config("C1").resized(24, 24, 1))
+    g = inp.graph
+    D = inp.D.astype(np.float64)
+    S = _S_of(inp)
+    u, q = O.run_inputs(inp, 4000)
+    e = E.primal(u, D, S, 4, g.parent, g.child, g.weight, 2)
+    f = E.dual(q, D, 4, g.parent, g.child, g.weight, 2)
+    assert 0 <= e - f < 1e-7 * e
+
+
+def test_literal_listing_fixed_point_is_not_optimal():
+    """Evidence for reading R1: without the shift (literal P:147) a(x) != 1 at the fixed point and the
+    gap stalls well above zero, while SHIFT_MIN converges on the same instance."""
+    inp = P.generate(P.config("C1").resized(24, 24, 1))
+    g = inp.graph
+    D = inp.D.astype(np.float64)
+    S = _S_of(inp)
+    gaps = {}
+    for shift in (O.SHIFT_MIN, O.SHIFT_NONE):
+        u, q = O.run_inputs(inp, 4000, shift=shift)
+        gaps[shift] = (E.primal(u, D, S, 4, g.parent, g.child, g.weight, 2)
+                       - E.dual(q, D, 4, g.parent, g.child, g.weight, 2))
+    assert gaps[O.SHIFT_MIN] < 1e-6 and gaps[O.SHIFT_NONE] > 1e-3
+
+
+# ---------------------------------------------------------------- P7/P8 exhaustive search
+@pytest.mark.parametrize("seed", range(8))
+def test_two_label_exact_against_brute_force(seed):
+    """2-label 4x4 grids with l-inf capacities (dual of anisotropic l1 TV): the thresholded converged
+    labeling attains the exhaustive-search optimum over all 2^16 labelings (BJ north_star)."""
+    r = np.random.default_rng(100 + seed)
+    D = r.uniform(0, 1, size=(2, 1, 4, 4))
+    Sf = r.uniform(0.05, 0.4, size=(1, 4, 4)) if seed % 2 else np.full((1, 4, 4), r.uniform(0.05, 0.4))
+    S3 = np.stack([np.zeros_like(Sf), Sf, Sf])
+    u, q = O.init_state(2, 2, (1, 4, 4), 2)
+    O.potts_iterate(D, np.ascontiguousarray(S3[1:]), u, q, 2, 0.25, 0.1, 20000, O.SHIFT_MIN, O.CAP_LINF)
+    Eopt, _ = brute.brute_force(D, S3, 3, [0, 0], [1, 2], [1.0, 1.0], 2, cap="linf")
+    b = O.argmax(u)
+    onehot = np.stack([(b == 0), (b == 1)]).astype(np.float64)
+    Eb = E.primal(onehot, D, S3, 3, [0, 0], [1, 2], [1, 1], 2, "linf")
+    Erel = E.primal(u, D, S3, 3, [0, 0], [1, 2], [1, 1], 2, "linf")
+    F = E.dual(q, D, 3, [0, 0], [1, 2], [1, 1], 2)
+    assert abs(Eb - Eopt) <= 1e-9 * abs(Eopt)
+    # weak duality F <= discrete optimum; tightness of the 2-label relaxation: optimum <= relaxed E;
+    # and the pair has converged (certified gap)
+    assert F <= Eopt + 1e-12 and Eopt <= Erel + 1e-12 and Erel - F <= 1e-7 * Eopt
+
+
+def test_relaxation_lower_bounds_discrete_optimum():
+    """Converged relaxed energy <= brute-force discrete optimum on 2x2, 3 labels (81 labelings)."""
+    r = np.random.default_rng(7)
+    for _ in range(5):
+        D = r.uniform(0, 1, size=(3, 1, 2, 2))
+        S4 = np.concatenate([np.zeros((1, 1, 2, 2)), np.full((3, 1, 2, 2), r.uniform(0.05, 0.5))])
+        u, q = O.init_state(3, 3, (1, 2, 2), 2)
+        O.potts_iterate(D, np.ascontiguousarray(S4[1:]), u, q, 2, 0.25, 0.1, 40000)
+        Eopt, _ = brute.brute_force(D, S4, 4, [0, 0, 0], [1, 2, 3], [1, 1, 1], 2, cap="l2")
+        Erel = E.primal(u, D, S4, 4, [0, 0, 0], [1, 2, 3], [1, 1, 1], 2, "l2")
+        F = E.dual(q, D, 4, [0, 0, 0], [1, 2, 3], [1, 1, 1], 2)
+        assert Erel - F <= 1e-10 * Eopt            # converged (certified by the dual)
+        assert Erel <= Eopt + 1e-10 * Eopt
+
+
+# ---------------------------------------------------------------- P9 independent explicit-flow solver
+def test_alm_potts_agrees_with_pseudo_flow():
+    """The explicit-flow ALM of Eq. 3 and the pseudo-flow iteration reach the same optimum (E, F, u, argmax)."""
+    inp = P.generate(P.config("C1").resized(14, 12, 1))
+    g = inp.graph
+    D = inp.D.astype(np.float64)
+    S = _S_of(inp)
+    u, q = O.run_inputs(inp, 8000)
+    Epf = E.primal(u, D, S, 4, g.parent, g.child, g.weight, 2)
+    Fpf = E.dual(q, D, 4, g.parent, g.child, g.weight, 2)
+    ua, qa, pS = alm.potts_alm(D, S[1:], 2, 3000)
+    Ealm = E.primal(np.clip(ua, 0, None) / np.clip(ua, 0, None).sum(0), D, S, 4, g.parent, g.child, g.weight, 2)
+    assert abs(Epf - Fpf) <= 1e-7 * Epf
+    assert abs(float(pS.sum()) - Fpf) <= 1e-6 * Epf
+    assert abs(Ealm - Epf) <= 1e-6 * Epf
+    assert np.max(np.abs(ua - u)) < 1e-4
+    assert np.mean(O.argmax(ua) == O.argmax(u)) >= 0.999
+
+
+@pytest.mark.parametrize("gname", ["dag", "hmf"])
+def test_alm_dag_agrees_with_pseudo_flow(gname):
+    """The explicit-flow ALM of Eq. 11 and Alg. 2 reach the same saddle point (C4 / C3 graphs)."""
+    cfg = P.config("C4" if gname == "dag" else "C3")
+    cfg = P.Config(cfg.name + "-2d", 2, 12, 12, 1, cfg.kind, 6, 4, 0.15, "sq", "per_node_uniform", 0.0, 0, seed=cfg.seed)
+    inp = P.generate(cfg)
+    g = inp.graph
+    D = inp.D.astype(np.float64)
+    S = _S_of(inp)
+    c = 0.25 if gname == "dag" else 1.0
+    u, q = O.run_inputs(inp, 30000, c=c)
+    Epf = E.primal(u, D, S, g.num_nodes, g.parent, g.child, g.weight, 2)
+    Fpf = E.dual(q, D, g.num_nodes, g.parent, g.child, g.weight, 2)
+    ua, qa, p = alm.dag_alm(D, S, g.num_nodes, g.parent, g.child, g.weight, 2, 16000)
+    assert abs(Epf - Fpf) <= 1e-9 * Epf
+    assert abs(float(p[0].sum()) - Epf) <= 1e-9 * Epf      # int p_S (Eq. 10 objective) = E = F
+    assert np.max(np.abs(ua - u)) < 1e-6
+    assert np.array_equal(O.argmax(ua), O.argmax(u))
+
+
+# ---------------------------------------------------------------- energy functions themselves
+def test_energy_examples():
+    """D = 0 and constant labeling -> 0; two voxels with one-hot labels differing, S = s -> 2s;
+    S = 0 and argmin one-hot -> sum_x min_L D_L."""
+    nn, par, chi, w = E.potts_graph_arrays(2)
+    u = np.zeros((2, 1, 1, 2)); u[0] = 1
+    S = np.zeros((3, 1, 1, 2))
+    assert E.primal(u, np.zeros_like(u), S, nn, par, chi, w, 2) == 0.0
+    u = np.zeros((2, 1, 1, 2)); u[0, 0, 0, 0] = 1; u[1, 0, 0, 1] = 1
+    S = np.full((3, 1, 1, 2), 0.3)
+    assert math.isclose(E.primal(u, np.zeros_like(u), S, nn, par, chi, w, 2), 0.6, rel_tol=1e-15)
+    D = RNG.uniform(size=(3, 2, 3, 4))
+    b = np.argmin(D, 0)
+    oh = np.stack([(b == l) for l in range(3)]).astype(float)
+    nn, par, chi, w = E.potts_graph_arrays(3)
+    assert math.isclose(E.primal(oh, D, np.zeros((4, 2, 3, 4)), nn, par, chi, w, 3), float(D.min(0).sum()))
+
+
+def test_weak_duality_random_feasible_pairs():
+    """E(u) >= F(q) for ANY simplex-feasible u and capacity-feasible q with q^k(last) = 0."""
+    g = P.dag_graph()
+    for cap in ("l2", "linf"):
+        for _ in range(5):
+            shape = (3, 4, 5)
+            D = RNG.uniform(size=(6,) + shape)
+            S = RNG.uniform(0, 0.5, size=(10,) + shape)
+            u = RNG.uniform(size=(6,) + shape); u /= u.sum(0)
+            q = RNG.normal(size=(9, 3) + shape)
+            q = np.stack([O.project(q[v], S[v + 1], 3, O.CAP_L2 if cap == "l2" else O.CAP_LINF) for v in range(9)])
+            q[:, 0, :, :, -1] = 0; q[:, 1, :, -1, :] = 0; q[:, 2, -1] = 0
+            e = E.primal(u, D, S, 10, g.parent, g.child, g.weight, 3, cap)
+            f = E.dual(q, D, 10, g.parent, g.child, g.weight, 3)
+            assert e >= f - 1e-12
