@@ -1,0 +1,189 @@
+/*
+ * pf.h -- C-ABI of the B200 pseudo-flow continuous max-flow solver (arXiv 1501.07844).
+ *
+ * The library (paper_1501_07844_b200/libpf.so) runs the per-iteration hot path of
+ * the paper's Algorithm 1 (Potts) and Algorithm 2
+ * (HMF / DAGMF) on one sm_100a GPU per solver, entirely in its own CUDA
+ * kernels.  No torch types cross this boundary; PyTorch (above it) only provides
+ * device selection, streams and process groups.
+ *
+ * Problem statement (BASELINE.json north_star):
+ *   create(volume dims, label graph, data terms D_L, smoothness S_L), iterate(n),
+ *   get_labeling.
+ *
+ * Conventions
+ *   - Every call returns pf_status; PF_OK == 0.  On error a message is available
+ *     from pf_last_error() (thread-local, valid until the next call on the thread).
+ *     After PF_ERR_CUDA or PF_ERR_NUMERIC the solver is poisoned: every later call
+ *     except pf_destroy returns PF_ERR_STATE.
+ *   - Boundary layout of every volume: x fastest, then y, then z (V = nx*ny*nz_local
+ *     values).  End labels (leaves) are numbered in increasing node-id order; that
+ *     number is the label id written by pf_get_labeling.
+ *   - Pointers may be host or device memory (detected per call with
+ *     cudaPointerGetAttributes).  Inputs are copied during the call and the caller
+ *     keeps ownership; outputs go into caller-allocated buffers.
+ *   - One solver per device; a solver is not thread-safe.  Work is issued on the
+ *     solver's stream (default: a stream created by pf_create; see pf_set_stream);
+ *     calls that return data to the host synchronize that stream.
+ *
+ * Spatial discretization (readings R4, R5):
+ *   nabla = forward differences, 0 at the last index of each axis;
+ *   div   = -nabla^T (backward differences, q^k(-1) = 0);
+ *   |q(x)| <= S(x) is the Euclidean ball (PF_CAP_L2, isotropic TV) or the box
+ *   (PF_CAP_LINF, anisotropic l1 TV).
+ */
+#ifndef PF_H_
+#define PF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pf_solver pf_solver; /* opaque; owns all of its device memory */
+
+typedef enum {
+    PF_OK = 0,
+    PF_ERR_INVALID = 1, /* bad dims, config, pointers, slab range */
+    PF_ERR_GRAPH = 2,   /* label graph violates the DAGMF assumptions (all violations listed) */
+    PF_ERR_OOM = 3,     /* device allocation failed */
+    PF_ERR_CUDA = 4,    /* CUDA runtime error (message carries cudaGetErrorString) */
+    PF_ERR_UNSUPPORTED = 5, /* graph shape outside the compiled kernel set */
+    PF_ERR_NUMERIC = 6, /* a(x) <= 0 or not finite detected at a check (message names the voxel) */
+    PF_ERR_STATE = 7    /* solver poisoned by an earlier error */
+} pf_status;
+
+typedef enum { PF_CAP_L2 = 0, PF_CAP_LINF = 1 } pf_capacity;
+
+/* Exponent shift of the label update (reading R1).  PF_SHIFT_MIN
+ * subtracts m(x) = min over end labels of d_L(x) before exp (log-sum-exp form);
+ * PF_SHIFT_NONE is the literal listing P:147 / P:290. */
+typedef enum { PF_SHIFT_MIN = 0, PF_SHIFT_NONE = 1 } pf_shift;
+
+typedef struct {
+    int32_t ndim;           /* 2 or 3 */
+    int64_t nx, ny, nz;     /* GLOBAL extents, each >= 1; nz == 1 when ndim == 2 */
+} pf_dims;
+
+/* Label graph.  Node 0 is the source S.  Edge e is
+ * parent[e] -> child[e] with weight w_(parent,child) = weight[e] > 0.  End labels
+ * L = {L : L.C empty}.  Requirements (PF_ERR_GRAPH otherwise):
+ * acyclic, S has no parents, every node reachable from S, >= 2 end labels,
+ * weights > 0, and W_(S,L) = 1 for every end label (reading R9: needed for
+ * sum_L u_L = 1 <=> u_S = 1).  A Potts model is the star S -> L_k. */
+typedef struct {
+    int32_t num_nodes;
+    int32_t num_edges;
+    const int32_t *parent;
+    const int32_t *child;
+    const float *weight;
+} pf_graph;
+
+typedef enum {
+    PF_S_SCALAR_PER_NODE = 0, /* scalars[v] for v = 1..num_nodes-1 (scalars[0] ignored) */
+    PF_S_SHARED_FIELD = 1,    /* fields[0]: one local volume shared by every node (Eq. 1 writes S(x)) */
+    PF_S_FIELD_PER_NODE = 2   /* fields[v-1]: one local volume per non-source node v (S_L(x)) */
+} pf_s_kind;
+
+typedef struct {
+    pf_s_kind kind;
+    const float *scalars;
+    const float *const *fields;
+} pf_smoothness;
+
+typedef struct {
+    float c;             /* proximal weight c > 0 (Eq. 6) */
+    float tau;           /* flow step tau > 0 (Eq. 8) */
+    int32_t cap;         /* pf_capacity */
+    int32_t shift;       /* pf_shift */
+    int32_t check_every; /* residual max|u_new - u_old| every k iterations; 0 = never */
+} pf_config;
+
+/* z-slab of a volume split along z across ranks / devices.
+ * The solver owns global planes [z_begin, z_end).  Inputs D_L cover
+ * [z_begin, min(z_end + 1, nz)): the owned slab plus the static halo plane above
+ * it (absent at the top of the volume).  Smoothness fields cover the owned slab. */
+typedef struct {
+    int64_t z_begin, z_end;
+} pf_slab;
+
+/* Create a solver for the (slab of the) volume and initialise the state:
+ * u_L = 1/|L|, q = 0 (reading R8).
+ *   D    : array of |L| pointers, one volume per end label in node-id order.
+ *   slab : NULL for the whole volume. */
+pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *const *D, const pf_smoothness *S,
+                    const pf_config *cfg, const pf_slab *slab, pf_solver **out);
+
+/* Re-initialise u and q (row a0) keeping D and S resident. */
+pf_status pf_reset(pf_solver *s);
+
+/* Run n iterations of the while-loop body of Alg. 1 / Alg. 2, one fused kernel
+ * launch per iteration.  If residual != NULL it receives max over owned voxels
+ * and end labels of |u_new - u_old| at the last iteration of this call that was a
+ * check iteration (global count % check_every == 0), or -1 if none was.  A
+ * residual != NULL synchronizes the stream.  Multi-slab: the halo planes must be
+ * exchanged between calls (pf_halo_regions / pf_exchange_local); n must then be 1. */
+pf_status pf_iterate(pf_solver *s, int32_t n, float *residual);
+
+/* Current labeling of the owned slab: u (may be NULL) as [|L|][V_local] and the
+ * thresholded labeling argmax (may be NULL) as uint8 [V_local], ties to the lowest
+ * label id ("thresholded"). */
+pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax);
+
+/* Spatial flows of the owned slab as [num_nodes-1][ndim][V_local], node-id order. */
+pf_status pf_get_flows(pf_solver *s, float *q);
+
+/* Energies over the owned slab, accumulated in fp64: primal E(u) (Eq. 1 P:53-59 /
+ * Eq. 9, intermediate labels u_v = sum_B W_(v,B) u_B) and pseudo-flow dual
+ * F(q) = sum_x min_L d_L(x) (Eq. 4 P:82-85 / Eq. 13).  Multi-slab: the
+ * halos must be current; the caller sums over ranks. */
+pf_status pf_get_energy(pf_solver *s, double *primal, double *dual);
+
+/* Iterations run since create / reset. */
+pf_status pf_iterations(const pf_solver *s, int64_t *done);
+
+/* Issue all work on `stream` (a cudaStream_t, may be NULL for the legacy default stream). */
+pf_status pf_set_stream(pf_solver *s, void *stream);
+
+/* Halo planes of the CURRENT state.  After an iteration,
+ * the solver's neighbour below (rank-1) needs this solver's first-plane u and q,
+ * the neighbour above (rank+1) needs this solver's last-plane q^z.  Each region is
+ * a contiguous device range: send regions are read, recv regions are written by
+ * the exchange.  Entries of a missing neighbour are NULL / 0. */
+typedef struct {
+    void *send_down_u, *recv_up_u;   /* |L| planes: own plane 0 -> below; halo plane above <- above */
+    void *send_down_q, *recv_up_q;   /* ndim*(num_nodes-1) planes */
+    void *send_up_qz, *recv_down_qz; /* (num_nodes-1) planes: own last plane q^z -> above; halo below <- below */
+    int64_t bytes_u, bytes_q, bytes_qz;
+} pf_halo;
+
+pf_status pf_halo_regions(pf_solver *s, pf_halo *h);
+
+/* Single-process exchange between consecutive slabs solvers[0..n-1] (ascending z),
+ * possibly on different devices (peer copies).  Issued on each receiver's stream
+ * after the senders' pending work. */
+pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n);
+
+/* Static description of the kernel configuration (for reports). */
+typedef struct {
+    int32_t tile_x, tile_y, z_chunk, threads_per_cta, ctas, regs_per_thread, smem_bytes, ctas_per_sm;
+    int64_t algorithmic_bytes_per_iteration;
+    int64_t device_bytes;                    /* resident footprint of this solver */
+    int64_t kernel_launches;                 /* this solver's own kernels launched so far */
+} pf_kernel_info;
+
+pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info);
+
+void pf_destroy(pf_solver *s);
+
+const char *pf_last_error(void);
+
+/* Library version string. */
+const char *pf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PF_H_ */

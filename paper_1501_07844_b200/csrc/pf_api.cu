@@ -1,0 +1,726 @@
+// pf_api.cu -- the C-ABI of include/pf.h: graph compilation (row a10), device state
+// and layouts, the per-iteration launch loop (rows a0-a8), labeling (a9), halo
+// regions for z-slab decomposition (row e).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pf.h"
+#include "pf_aux.cuh"
+#include "pf_kernels.cuh"
+
+using namespace pf;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pf_status fail(pf_status st, const char *fmt, ...) {
+    char buf[2048];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// --------------------------------------------------------------------------
+// Label-graph compilation (reading R9)
+// --------------------------------------------------------------------------
+struct Compiled {
+    int num_nodes = 0, NI = 0, NL = 0, NV = 0;
+    std::vector<int> pos_of_node;  // node id -> position, S -> -1
+    std::vector<int> node_of_pos;
+    GraphConst g;
+    std::vector<std::vector<float>> W;  // W[pos][leaf slot] path weights
+};
+
+pf_status compile_graph(const pf_graph *gr, Compiled *out) {
+    if (!gr || gr->num_nodes < 3 || gr->num_edges < 2 || !gr->parent || !gr->child || !gr->weight)
+        return fail(PF_ERR_GRAPH, "graph: need >= 3 nodes (S + 2 end labels), >= 2 edges and non-NULL arrays");
+    const int n = gr->num_nodes, ne = gr->num_edges;
+    std::string errs;
+    auto add = [&](const std::string &s) { errs += (errs.empty() ? "" : "; ") + s; };
+    std::vector<std::vector<std::pair<int, float>>> kids(n), pars(n);
+    bool idx_ok = true;
+    for (int e = 0; e < ne; ++e) {
+        const int p = gr->parent[e], c = gr->child[e];
+        const float w = gr->weight[e];
+        if (p < 0 || p >= n || c < 0 || c >= n) {
+            add("edge " + std::to_string(e) + " has a node id out of range");
+            idx_ok = false;
+            continue;
+        }
+        if (!(w > 0.f) || !std::isfinite(w)) add("edge " + std::to_string(e) + " weight must be > 0");
+        if (p == c) add("self-loop at node " + std::to_string(p));
+        kids[p].push_back({c, w});
+        pars[c].push_back({p, w});
+    }
+    if (!idx_ok) return fail(PF_ERR_GRAPH, "graph: %s", errs.c_str());
+    if (!pars[0].empty()) add("source S (node 0) has parents");
+    // Kahn with lowest-id tie-break
+    std::vector<int> indeg(n, 0), order;
+    for (int v = 0; v < n; ++v) indeg[v] = (int)pars[v].size();
+    std::vector<bool> placed(n, false);
+    for (int k = 0; k < n; ++k) {
+        int pick = -1;
+        for (int v = 0; v < n; ++v)
+            if (!placed[v] && indeg[v] == 0) { pick = v; break; }
+        if (pick < 0) break;
+        placed[pick] = true;
+        order.push_back(pick);
+        for (auto &c : kids[pick]) indeg[c.first]--;
+    }
+    if ((int)order.size() != n) add("graph has a cycle");
+    // reachability from S
+    std::vector<bool> reach(n, false);
+    std::vector<int> stack{0};
+    reach[0] = true;
+    while (!stack.empty()) {
+        int v = stack.back();
+        stack.pop_back();
+        for (auto &c : kids[v])
+            if (!reach[c.first]) { reach[c.first] = true; stack.push_back(c.first); }
+    }
+    for (int v = 1; v < n; ++v)
+        if (!reach[v]) add("node " + std::to_string(v) + " unreachable from S");
+    std::vector<int> leaves, internals;
+    for (int v = 1; v < n; ++v) (kids[v].empty() ? leaves : internals).push_back(v);
+    if (leaves.size() < 2) add("fewer than 2 end labels");
+    if (!errs.empty()) return fail(PF_ERR_GRAPH, "graph: %s", errs.c_str());
+    // W_(v, B) by memoised recursion in reverse topological order
+    const int NL = (int)leaves.size();
+    std::vector<std::vector<double>> Wd(n, std::vector<double>(NL, 0.0));
+    for (int k = n - 1; k >= 0; --k) {
+        const int v = order[k];
+        if (kids[v].empty() && v != 0) {
+            Wd[v][std::find(leaves.begin(), leaves.end(), v) - leaves.begin()] = 1.0;
+        } else {
+            for (auto &c : kids[v])
+                for (int l = 0; l < NL; ++l) Wd[v][l] += (double)c.second * Wd[c.first][l];
+        }
+    }
+    for (int l = 0; l < NL; ++l)
+        if (std::fabs(Wd[0][l] - 1.0) > 1e-6)
+            add("W_(S," + std::to_string(leaves[l]) + ") = " + std::to_string(Wd[0][l]) +
+                " != 1 (sum of end labels must equal u_S = 1, reading R9)");
+    if (!errs.empty()) return fail(PF_ERR_GRAPH, "graph: %s", errs.c_str());
+    const int NI = (int)internals.size();
+    if (NI > kMaxInternal || NI + NL > kMaxNodes)
+        return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes exceeds the compiled kernel set "
+                                        "(<= %d internal, <= %d non-source nodes)", NI, NL, kMaxInternal, kMaxNodes);
+    out->num_nodes = n;
+    out->NI = NI;
+    out->NL = NL;
+    out->NV = NI + NL;
+    out->pos_of_node.assign(n, -1);
+    out->node_of_pos.clear();
+    for (int k = 0; k < n; ++k) {  // internal nodes in topological order
+        const int v = order[k];
+        if (v != 0 && !kids[v].empty()) {
+            out->pos_of_node[v] = (int)out->node_of_pos.size();
+            out->node_of_pos.push_back(v);
+        }
+    }
+    for (int v : leaves) {  // end labels in node-id order
+        out->pos_of_node[v] = (int)out->node_of_pos.size();
+        out->node_of_pos.push_back(v);
+    }
+    memset(&out->g, 0, sizeof(out->g));
+    for (int v = 1; v < n; ++v) {
+        if (kids[v].empty()) continue;
+        const int i = out->pos_of_node[v];
+        for (auto &c : kids[v]) out->g.w[i][out->pos_of_node[c.first]] += c.second;
+    }
+    out->W.assign(out->NV, std::vector<float>(NL, 0.f));
+    for (int p = 0; p < out->NV; ++p)
+        for (int l = 0; l < NL; ++l) out->W[p][l] = (float)Wd[out->node_of_pos[p]][l];
+    return PF_OK;
+}
+
+}  // namespace
+
+struct pf_solver {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool poisoned = false;
+    int ndim = 3;
+    int64_t nx = 0, ny = 0, nz = 0;
+    int64_t z0 = 0, z1 = 0, nzl = 0;
+    int64_t P = 0;
+    Compiled gc;
+    pf_config cfg{};
+    int s_kind = 0;
+    // allocations (base pointers) and plane-0 pointers
+    float *u_alloc[2] = {nullptr, nullptr}, *q_alloc[2] = {nullptr, nullptr};
+    float *D_alloc = nullptr, *S_alloc = nullptr;
+    float *u[2] = {nullptr, nullptr}, *q[2] = {nullptr, nullptr};
+    int cur = 0;
+    int64_t iters = 0;
+    unsigned int *d_resid = nullptr;
+    unsigned long long *d_err = nullptr;
+    unsigned int *d_flag = nullptr;
+    double *d_energy = nullptr;  // partials + result
+    IterKernelInfo kinfo{};
+    int zchunk = 0;
+    dim3 grid;
+    int ctas_per_sm = 0;
+    int regs = 0;
+    int64_t device_bytes = 0;
+    bool last_resid_valid = false;
+    int64_t launches = 0;
+};
+
+namespace {
+
+pf_status cuda_fail(pf_solver *s, cudaError_t e, const char *what) {
+    if (s) s->poisoned = true;
+    return fail(PF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                     \
+    do {                                                   \
+        cudaError_t e__ = (expr);                          \
+        if (e__ != cudaSuccess) return cuda_fail(s, e__, what); \
+    } while (0)
+
+int64_t ups(const pf_solver *s) { return (int64_t)s->gc.NL * s->P; }
+int64_t qps(const pf_solver *s) { return (int64_t)s->ndim * s->gc.NV * s->P; }
+
+void free_all(pf_solver *s) {
+    for (int i = 0; i < 2; ++i) {
+        if (s->u_alloc[i]) cudaFree(s->u_alloc[i]);
+        if (s->q_alloc[i]) cudaFree(s->q_alloc[i]);
+        s->u_alloc[i] = s->q_alloc[i] = nullptr;
+    }
+    if (s->D_alloc) cudaFree(s->D_alloc);
+    if (s->S_alloc) cudaFree(s->S_alloc);
+    if (s->d_resid) cudaFree(s->d_resid);
+    if (s->d_err) cudaFree(s->d_err);
+    if (s->d_flag) cudaFree(s->d_flag);
+    if (s->d_energy) cudaFree(s->d_energy);
+    s->D_alloc = s->S_alloc = nullptr;
+}
+
+pf_status alloc(pf_solver *s, void **p, size_t bytes, const char *what) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(PF_ERR_OOM, "cudaMalloc(%zu bytes) for %s failed: %s", bytes, what, cudaGetErrorString(e));
+    }
+    s->device_bytes += (int64_t)bytes;
+    return PF_OK;
+}
+
+pf_status init_state(pf_solver *s) {
+    const int64_t nu = (s->nzl + 2) * ups(s), nq = (s->nzl + 2) * qps(s);
+    for (int i = 0; i < 2; ++i) {
+        CK(launch_fill(s->u_alloc[i], nu, 1.0f / (float)s->gc.NL, s->stream), "init u");
+        s->launches++;
+        CK(cudaMemsetAsync(s->q_alloc[i], 0, nq * sizeof(float), s->stream), "init q");
+    }
+    CK(cudaMemsetAsync(s->d_err, 0xff, sizeof(unsigned long long), s->stream), "init err");
+    s->cur = 0;
+    s->iters = 0;
+    return PF_OK;
+}
+
+void choose_chunking(pf_solver *s) {
+    const int gx = (int)((s->nx + kTX - 1) / kTX), gy = (int)((s->ny + s->kinfo.tile_y - 1) / s->kinfo.tile_y);
+    const int64_t tiles = (int64_t)gx * gy;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+    const int nzl = (int)s->nzl;
+    // minimise (CTAs per SM, rounded up) x (planes per CTA incl. the look-ahead plane)
+    int best_n = 1;
+    double best_cost = 1e300;
+    const int max_n = std::max(1, nzl / 4);
+    for (int n = 1; n <= max_n; ++n) {
+        const int ch = (nzl + n - 1) / n;
+        const int nn = (nzl + ch - 1) / ch;
+        const double per_sm = std::ceil((double)(tiles * nn) / sms);
+        const double cost = per_sm * (ch + 1);
+        if (cost < best_cost - 1e-9) { best_cost = cost; best_n = nn; }
+    }
+    s->zchunk = (nzl + best_n - 1) / best_n;
+    s->grid = dim3(gx, gy, (nzl + s->zchunk - 1) / s->zchunk);
+}
+
+pf_status check_usable(const pf_solver *s) {
+    if (!s) return fail(PF_ERR_INVALID, "NULL solver");
+    if (s->poisoned) return fail(PF_ERR_STATE, "solver poisoned by an earlier error");
+    return PF_OK;
+}
+
+pf_status check_numeric(pf_solver *s) {
+    unsigned long long v = ~0ull;
+    CK(cudaMemcpyAsync(&v, s->d_err, sizeof(v), cudaMemcpyDeviceToHost, s->stream), "read error word");
+    CK(cudaStreamSynchronize(s->stream), "sync");
+    if (v != ~0ull) {
+        s->poisoned = true;
+        const unsigned long long P = (unsigned long long)s->P;
+        return fail(PF_ERR_NUMERIC, "numerical collapse: a(x) <= 0 or not finite at voxel (x=%llu, y=%llu, z=%llu)",
+                    (v % P) % (unsigned long long)s->nx, (v % P) / (unsigned long long)s->nx, v / P);
+    }
+    return PF_OK;
+}
+
+// copy one volume [z][y][x] (nzc planes) into / out of a strided internal layout
+cudaError_t copy_planes(float *dst, int64_t dst_pitch_floats, const float *src, int64_t src_pitch_floats,
+                        int64_t plane_floats, int64_t nplanes, cudaStream_t st) {
+    if (nplanes <= 0) return cudaSuccess;
+    return cudaMemcpy2DAsync(dst, dst_pitch_floats * sizeof(float), src, src_pitch_floats * sizeof(float),
+                             plane_floats * sizeof(float), nplanes, cudaMemcpyDefault, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *pf_last_error(void) { return g_last_error.c_str(); }
+
+const char *pf_version(void) { return "pf 0.1 (sm_100a)"; }
+
+pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *const *D, const pf_smoothness *S,
+                    const pf_config *cfg, const pf_slab *slab, pf_solver **out) {
+    if (!out) return fail(PF_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    if (!dims || !graph || !D || !S || !cfg) return fail(PF_ERR_INVALID, "NULL argument");
+    if ((dims->ndim != 2 && dims->ndim != 3) || dims->nx < 1 || dims->ny < 1 || dims->nz < 1 ||
+        (dims->ndim == 2 && dims->nz != 1))
+        return fail(PF_ERR_INVALID, "dims: ndim must be 2 or 3, extents >= 1, nz == 1 for ndim == 2");
+    if (dims->nx * dims->ny >= (int64_t)1 << 31)
+        return fail(PF_ERR_INVALID, "dims: an x-y plane must have < 2^31 voxels");
+    if (!(cfg->c > 0.f) || !(cfg->tau > 0.f) || !std::isfinite(cfg->c) || !std::isfinite(cfg->tau))
+        return fail(PF_ERR_INVALID, "config: c and tau must be finite and > 0");
+    if ((cfg->cap != PF_CAP_L2 && cfg->cap != PF_CAP_LINF) || (cfg->shift != PF_SHIFT_MIN && cfg->shift != PF_SHIFT_NONE) ||
+        cfg->check_every < 0)
+        return fail(PF_ERR_INVALID, "config: bad cap / shift / check_every");
+    int64_t z0 = 0, z1 = dims->nz;
+    if (slab) {
+        z0 = slab->z_begin;
+        z1 = slab->z_end;
+        if (z0 < 0 || z1 > dims->nz || z1 <= z0) return fail(PF_ERR_INVALID, "slab: need 0 <= z_begin < z_end <= nz");
+    }
+    Compiled gc;
+    pf_status st = compile_graph(graph, &gc);
+    if (st != PF_OK) return st;
+    if (S->kind != PF_S_SCALAR_PER_NODE && S->kind != PF_S_SHARED_FIELD && S->kind != PF_S_FIELD_PER_NODE)
+        return fail(PF_ERR_INVALID, "smoothness: bad kind");
+    if (S->kind == PF_S_SCALAR_PER_NODE) {
+        if (!S->scalars) return fail(PF_ERR_INVALID, "smoothness: scalars is NULL");
+        for (int v = 1; v < gc.num_nodes; ++v)
+            if (!(S->scalars[v] >= 0.f) || !std::isfinite(S->scalars[v]))
+                return fail(PF_ERR_INVALID, "smoothness: S_%d = %g must be finite and >= 0", v, (double)S->scalars[v]);
+    } else if (!S->fields) {
+        return fail(PF_ERR_INVALID, "smoothness: fields is NULL");
+    }
+    for (int l = 0; l < gc.NL; ++l)
+        if (!D[l]) return fail(PF_ERR_INVALID, "D[%d] is NULL", l);
+
+    pf_solver *s = new pf_solver();
+    cudaGetDevice(&s->device);
+    s->ndim = dims->ndim;
+    s->nx = dims->nx;
+    s->ny = dims->ny;
+    s->nz = dims->nz;
+    s->z0 = z0;
+    s->z1 = z1;
+    s->nzl = z1 - z0;
+    s->P = dims->nx * dims->ny;
+    s->gc = gc;
+    s->cfg = *cfg;
+    s->s_kind = S->kind;
+    if (!iter_kernel_lookup(gc.NI, gc.NL, &s->kinfo)) {
+        delete s;
+        return fail(PF_ERR_UNSUPPORTED, "no compiled kernel for %d internal / %d end nodes", gc.NI, gc.NL);
+    }
+    cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete s;
+        return fail(PF_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
+    s->own_stream = true;
+    const int NL = gc.NL, NV = gc.NV;
+    const int64_t P = s->P, nzl = s->nzl;
+    auto bail = [&](pf_status st2) {
+        std::string msg = g_last_error;
+        free_all(s);
+        if (s->own_stream) cudaStreamDestroy(s->stream);
+        delete s;
+        g_last_error = msg;
+        return st2;
+    };
+    // state: planes -1 .. nzl (halo below / above)
+    for (int i = 0; i < 2; ++i) {
+        if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u")) != PF_OK)
+            return bail(st);
+        if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * s->ndim * NV * P) * sizeof(float), "q")) != PF_OK)
+            return bail(st);
+        s->u[i] = s->u_alloc[i] + NL * P;
+        s->q[i] = s->q_alloc[i] + (int64_t)s->ndim * NV * P;
+    }
+    const int64_t nzD = std::min(z1 + 1, dims->nz) - z0;  // owned + static halo plane above
+    if ((st = alloc(s, (void **)&s->D_alloc, (size_t)((nzl + 1) * NL * P) * sizeof(float), "D")) != PF_OK)
+        return bail(st);
+    const int64_t nS = S->kind == PF_S_SHARED_FIELD ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? NV : 0);
+    if (nS > 0 && (st = alloc(s, (void **)&s->S_alloc, (size_t)(nzl * nS * P) * sizeof(float), "S")) != PF_OK)
+        return bail(st);
+    if ((st = alloc(s, (void **)&s->d_resid, 64, "resid")) != PF_OK) return bail(st);
+    if ((st = alloc(s, (void **)&s->d_err, 64, "err")) != PF_OK) return bail(st);
+    if ((st = alloc(s, (void **)&s->d_flag, 64, "flag")) != PF_OK) return bail(st);
+    if ((st = alloc(s, (void **)&s->d_energy, (size_t)(2 * kEnergyBlocks + 2) * sizeof(double), "energy")) != PF_OK)
+        return bail(st);
+    // inputs -> internal layouts (boundary [z][y][x] per label -> [z][l][y][x])
+    for (int l = 0; l < NL; ++l) {
+        e = copy_planes(s->D_alloc + l * P, NL * P, D[l], P, P, nzD, s->stream);
+        if (e != cudaSuccess) { cuda_fail(s, e, "upload D"); return bail(PF_ERR_CUDA); }
+    }
+    if (nzD < nzl + 1) {
+        e = cudaMemsetAsync(s->D_alloc + nzD * NL * P, 0, (size_t)((nzl + 1 - nzD) * NL * P) * sizeof(float), s->stream);
+        if (e != cudaSuccess) { cuda_fail(s, e, "zero D halo"); return bail(PF_ERR_CUDA); }
+    }
+    if (S->kind == PF_S_SHARED_FIELD) {
+        if (!S->fields[0]) return bail(fail(PF_ERR_INVALID, "smoothness: fields[0] is NULL"));
+        e = copy_planes(s->S_alloc, P, S->fields[0], P, P, nzl, s->stream);
+        if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
+    } else if (S->kind == PF_S_FIELD_PER_NODE) {
+        for (int p = 0; p < NV; ++p) {
+            const int v = gc.node_of_pos[p];
+            if (!S->fields[v - 1]) return bail(fail(PF_ERR_INVALID, "smoothness: fields[%d] is NULL", v - 1));
+            e = copy_planes(s->S_alloc + p * P, NV * P, S->fields[v - 1], P, P, nzl, s->stream);
+            if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
+        }
+    } else {
+        for (int p = 0; p < NV; ++p) s->gc.g.s[p] = S->scalars[gc.node_of_pos[p]];
+    }
+    if (nS > 0) {
+        cudaMemsetAsync(s->d_flag, 0, 4, s->stream);
+        launch_check_nonneg(s->S_alloc, nzl * nS * P, s->d_flag, s->stream);
+        s->launches++;
+        unsigned int flag = 0;
+        cudaMemcpyAsync(&flag, s->d_flag, 4, cudaMemcpyDeviceToHost, s->stream);
+        e = cudaStreamSynchronize(s->stream);
+        if (e != cudaSuccess) { cuda_fail(s, e, "validate S"); return bail(PF_ERR_CUDA); }
+        if (flag) return bail(fail(PF_ERR_INVALID, "smoothness: S must be >= 0 and finite everywhere"));
+    }
+    if ((st = init_state(s)) != PF_OK) return bail(st);
+    // kernel configuration
+    e = cudaFuncSetAttribute(s->kinfo.func, cudaFuncAttributeMaxDynamicSharedMemorySize, s->kinfo.smem_bytes);
+    if (e != cudaSuccess) { cuda_fail(s, e, "cudaFuncSetAttribute"); return bail(PF_ERR_CUDA); }
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, s->kinfo.func) == cudaSuccess) s->regs = fa.numRegs;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->ctas_per_sm, s->kinfo.func, s->kinfo.threads,
+                                                  s->kinfo.smem_bytes);
+    choose_chunking(s);
+    e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) { cuda_fail(s, e, "create"); return bail(PF_ERR_CUDA); }
+    *out = s;
+    return PF_OK;
+}
+
+pf_status pf_reset(pf_solver *s) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    DeviceGuard dg(s->device);
+    return init_state(s);
+}
+
+pf_status pf_set_stream(pf_solver *s, void *stream) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    DeviceGuard dg(s->device);
+    if (s->own_stream) {
+        cudaStreamSynchronize(s->stream);
+        cudaStreamDestroy(s->stream);
+        s->own_stream = false;
+    }
+    s->stream = (cudaStream_t)stream;
+    return PF_OK;
+}
+
+pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (n < 0) return fail(PF_ERR_INVALID, "n must be >= 0");
+    DeviceGuard dg(s->device);
+    IterArgs a;
+    memset(&a, 0, sizeof(a));
+    a.D = s->D_alloc;
+    a.S = s->S_alloc;
+    a.nx = (int)s->nx;
+    a.ny = (int)s->ny;
+    a.nzl = (int)s->nzl;
+    a.zg0 = (int)s->z0;
+    a.nzg = (int)s->nz;
+    a.zchunk = s->zchunk;
+    a.ndim = s->ndim;
+    a.s_kind = s->s_kind;
+    a.cap = s->cfg.cap;
+    a.shift = s->cfg.shift;
+    a.inv_c = 1.0f / s->cfg.c;
+    a.ctau = s->cfg.c * s->cfg.tau;
+    a.resid_bits = s->d_resid;
+    a.err_voxel = s->d_err;
+    a.g = s->gc.g;
+    bool any_check = false;
+    for (int t = 0; t < n; ++t) {
+        const int64_t it = s->iters + 1;
+        a.check = (s->cfg.check_every > 0 && it % s->cfg.check_every == 0) ? 1 : 0;
+        if (a.check) {
+            CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
+            any_check = true;
+        }
+        a.u_in = s->u[s->cur];
+        a.q_in = s->q[s->cur];
+        a.u_out = s->u[1 - s->cur];
+        a.q_out = s->q[1 - s->cur];
+        void *args[] = {(void *)&a};
+        CK(cudaLaunchKernel(s->kinfo.func, s->grid, dim3(s->kinfo.threads), args, s->kinfo.smem_bytes, s->stream),
+           "launch pf_iter_kernel");
+        s->launches++;
+        s->cur = 1 - s->cur;
+        s->iters = it;
+    }
+    if (any_check) s->last_resid_valid = true;
+    if (residual) {
+        *residual = -1.f;
+        if ((st = check_numeric(s)) != PF_OK) return st;
+        if (any_check) {
+            unsigned int bits = 0;
+            CK(cudaMemcpyAsync(&bits, s->d_resid, sizeof(bits), cudaMemcpyDeviceToHost, s->stream), "read residual");
+            CK(cudaStreamSynchronize(s->stream), "sync");
+            float r;
+            memcpy(&r, &bits, 4);
+            *residual = r;
+        }
+    }
+    return PF_OK;
+}
+
+pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    DeviceGuard dg(s->device);
+    const int NL = s->gc.NL;
+    const int64_t P = s->P, nzl = s->nzl;
+    if (u) {
+        for (int l = 0; l < NL; ++l)
+            CK(copy_planes(u + l * nzl * P, P, s->u[s->cur] + l * P, NL * P, P, nzl, s->stream), "download u");
+    }
+    if (argmax) {
+        const bool dev = is_device_ptr(argmax);
+        uint8_t *dst = argmax;
+        if (!dev) CK(cudaMalloc((void **)&dst, (size_t)(nzl * P)), "argmax scratch");
+        CK(launch_argmax(s->u[s->cur], dst, NL, P, nzl, s->stream), "argmax kernel");
+        s->launches++;
+        if (!dev) {
+            CK(cudaMemcpyAsync(argmax, dst, (size_t)(nzl * P), cudaMemcpyDeviceToHost, s->stream), "download argmax");
+            CK(cudaStreamSynchronize(s->stream), "sync");
+            cudaFree(dst);
+        }
+    }
+    return check_numeric(s);
+}
+
+pf_status pf_get_flows(pf_solver *s, float *q) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (!q) return fail(PF_ERR_INVALID, "q is NULL");
+    DeviceGuard dg(s->device);
+    const int NV = s->gc.NV, nd = s->ndim;
+    const int64_t P = s->P, nzl = s->nzl;
+    for (int p = 0; p < NV; ++p) {
+        const int v = s->gc.node_of_pos[p];
+        for (int k = 0; k < nd; ++k) {
+            float *dst = q + ((int64_t)(v - 1) * nd + k) * nzl * P;
+            CK(copy_planes(dst, P, s->q[s->cur] + ((int64_t)k * NV + p) * P, (int64_t)nd * NV * P, P, nzl, s->stream),
+               "download q");
+        }
+    }
+    return check_numeric(s);
+}
+
+pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    DeviceGuard dg(s->device);
+    EnergyArgs a;
+    memset(&a, 0, sizeof(a));
+    a.u = s->u[s->cur];
+    a.q = s->q[s->cur];
+    a.D = s->D_alloc;
+    a.S = s->S_alloc;
+    a.nx = (int)s->nx;
+    a.ny = (int)s->ny;
+    a.nzl = (int)s->nzl;
+    a.zg0 = (int)s->z0;
+    a.nzg = (int)s->nz;
+    a.ndim = s->ndim;
+    a.NI = s->gc.NI;
+    a.NL = s->gc.NL;
+    a.NV = s->gc.NV;
+    a.s_kind = s->s_kind;
+    a.cap = s->cfg.cap;
+    a.g = s->gc.g;
+    CK(launch_energy(a, s->d_energy + 2, kEnergyBlocks, s->d_energy, s->stream), "energy kernel");
+    s->launches += 2;
+    double h[2];
+    CK(cudaMemcpyAsync(h, s->d_energy, sizeof(h), cudaMemcpyDeviceToHost, s->stream), "download energy");
+    CK(cudaStreamSynchronize(s->stream), "sync");
+    if (primal) *primal = h[0];
+    if (dual) *dual = h[1];
+    return check_numeric(s);
+}
+
+pf_status pf_iterations(const pf_solver *s, int64_t *done) {
+    if (!s || !done) return fail(PF_ERR_INVALID, "NULL argument");
+    *done = s->iters;
+    return PF_OK;
+}
+
+pf_status pf_halo_regions(pf_solver *s, pf_halo *h) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (!h) return fail(PF_ERR_INVALID, "h is NULL");
+    memset(h, 0, sizeof(*h));
+    const int NV = s->gc.NV;
+    const int64_t P = s->P, nzl = s->nzl;
+    float *u = s->u[s->cur], *q = s->q[s->cur];
+    h->bytes_u = ups(s) * (int64_t)sizeof(float);
+    h->bytes_q = qps(s) * (int64_t)sizeof(float);
+    h->bytes_qz = s->ndim == 3 ? (int64_t)NV * P * (int64_t)sizeof(float) : 0;
+    if (s->z0 > 0) {  // neighbour below exists
+        h->send_down_u = u;
+        h->send_down_q = q;
+        if (s->ndim == 3) h->recv_down_qz = q - qps(s) + 2 * NV * P;
+    }
+    if (s->z1 < s->nz) {  // neighbour above exists
+        h->recv_up_u = u + nzl * ups(s);
+        h->recv_up_q = q + nzl * qps(s);
+        if (s->ndim == 3) h->send_up_qz = q + (nzl - 1) * qps(s) + 2 * NV * P;
+    }
+    return PF_OK;
+}
+
+pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n) {
+    if (!solvers || n < 1) return fail(PF_ERR_INVALID, "need >= 1 solver");
+    for (int i = 0; i < n; ++i) {
+        pf_status st = check_usable(solvers[i]);
+        if (st != PF_OK) return st;
+    }
+    for (int i = 0; i + 1 < n; ++i) {
+        pf_solver *lo = solvers[i], *hi = solvers[i + 1];
+        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->gc.NV != hi->gc.NV)
+            return fail(PF_ERR_INVALID, "exchange: solvers %d and %d are not consecutive slabs of one volume", i, i + 1);
+    }
+    // order: every receiver waits for every sender's pending work, copies on the receiver's stream,
+    // then every sender waits for the copies that read its current state.
+    std::vector<cudaEvent_t> ev(n);
+    for (int i = 0; i < n; ++i) {
+        pf_solver *s = solvers[i];
+        DeviceGuard dg(s->device);
+        CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event");
+        CK(cudaEventRecord(ev[i], s->stream), "record");
+    }
+    for (int i = 0; i < n; ++i) {
+        pf_solver *s = solvers[i];
+        DeviceGuard dg(s->device);
+        if (i > 0) CK(cudaStreamWaitEvent(s->stream, ev[i - 1], 0), "wait");
+        if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, ev[i + 1], 0), "wait");
+    }
+    for (int i = 0; i + 1 < n; ++i) {
+        pf_solver *lo = solvers[i], *hi = solvers[i + 1];
+        pf_halo hl, hh;
+        pf_halo_regions(lo, &hl);
+        pf_halo_regions(hi, &hh);
+        pf_solver *s = lo;
+        {
+            DeviceGuard dg(lo->device);
+            CK(cudaMemcpyAsync(hl.recv_up_u, hh.send_down_u, hl.bytes_u, cudaMemcpyDefault, lo->stream), "halo u");
+            CK(cudaMemcpyAsync(hl.recv_up_q, hh.send_down_q, hl.bytes_q, cudaMemcpyDefault, lo->stream), "halo q");
+        }
+        s = hi;
+        if (hh.bytes_qz) {
+            DeviceGuard dg(hi->device);
+            CK(cudaMemcpyAsync(hh.recv_down_qz, hl.send_up_qz, hh.bytes_qz, cudaMemcpyDefault, hi->stream), "halo qz");
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        pf_solver *s = solvers[i];
+        DeviceGuard dg(s->device);
+        CK(cudaEventRecord(ev[i], s->stream), "record");
+    }
+    for (int i = 0; i < n; ++i) {
+        pf_solver *s = solvers[i];
+        DeviceGuard dg(s->device);
+        if (i > 0) CK(cudaStreamWaitEvent(s->stream, ev[i - 1], 0), "wait");
+        if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, ev[i + 1], 0), "wait");
+    }
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+    return PF_OK;
+}
+
+pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
+    if (!s || !info) return fail(PF_ERR_INVALID, "NULL argument");
+    info->tile_x = kTX;
+    info->tile_y = s->kinfo.tile_y;
+    info->z_chunk = s->zchunk;
+    info->threads_per_cta = s->kinfo.threads;
+    info->ctas = (int)(s->grid.x * s->grid.y * s->grid.z);
+    info->regs_per_thread = s->regs;
+    info->smem_bytes = s->kinfo.smem_bytes;
+    info->ctas_per_sm = s->ctas_per_sm;
+    // algorithmic bytes per iteration: per end label u r/w + D r + q r/w,
+    // per internal node q r/w, plus the capacity fields
+    const int64_t V = s->P * s->nzl;
+    const int64_t per_leaf = 4 + 4 + 4 + 8 * s->ndim, per_int = 8 * s->ndim;
+    int64_t b = V * (per_leaf * s->gc.NL + per_int * s->gc.NI);
+    if (s->s_kind == PF_S_SHARED_FIELD) b += 4 * V;
+    if (s->s_kind == PF_S_FIELD_PER_NODE) b += 4 * V * s->gc.NV;
+    info->algorithmic_bytes_per_iteration = b;
+    info->device_bytes = s->device_bytes;
+    info->kernel_launches = s->launches;
+    return PF_OK;
+}
+
+void pf_destroy(pf_solver *s) {
+    if (!s) return;
+    DeviceGuard dg(s->device);
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    free_all(s);
+    if (s->own_stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// pf_aux.cu -- auxiliary sm_100a kernels: state init (row a0), thresholded labeling
+// (row a9), primal / dual energies (row a8 diagnostics), capacity validation.
+#include <cfloat>
+#include <cstdint>
+
+#include "pf_aux.cuh"
+
+namespace pf {
+
+__global__ void fill_kernel(float *p, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// argmax over end labels, lowest label id wins ties ("thresholded").
+__global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__ out, int NL, int64_t P,
+                              int64_t nz) {
+    const int64_t V = P * nz;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / P, pix = i - z * P;
+        const float *b = u + z * NL * P + pix;
+        float best = b[0];
+        int arg = 0;
+        for (int l = 1; l < NL; ++l) {
+            const float v = b[l * P];
+            if (v > best) { best = v; arg = l; }
+        }
+        out[i] = (uint8_t)arg;
+    }
+}
+
+__global__ void min_kernel(const float *__restrict__ p, int64_t n, unsigned int *out_bits_neg) {
+    // records whether any value is negative or NaN (out = 1)
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = p[i];
+        if (!(v >= 0.f) || !(v <= FLT_MAX)) bad = true;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(out_bits_neg, 1u);
+}
+
+// ---------------------------------------------------------------------------
+// Energies.  One thread per owned voxel; fp64 per-block partials reduced in a
+// fixed order by energy_finish_kernel (deterministic).
+// ---------------------------------------------------------------------------
+struct NodeVals {
+    float v[kMaxNodes];
+};
+
+__device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, int64_t P, float *out) {
+    // u_v for every position: end labels read, internal by bottom-up sums (Eq. 9)
+    const int NV = a.NV, NI = a.NI;
+    for (int l = 0; l < a.NL; ++l) out[NI + l] = ub[l * P];
+    for (int i = NI - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int j = i + 1; j < NV; ++j) acc += (double)a.g.w[i][j] * out[j];
+        out[i] = (float)acc;
+    }
+}
+
+__global__ void energy_kernel(const EnergyArgs a, double *partial) {
+    const int64_t P = (int64_t)a.nx * a.ny;
+    const int64_t V = P * a.nzl;
+    const int NV = a.NV, NI = a.NI, NL = a.NL;
+    const int64_t ups = (int64_t)NL * P, qps = (int64_t)a.ndim * NV * P;
+    double e_acc = 0.0, f_acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / P, pix = i - z * P;
+        const int x = (int)(pix % a.nx), y = (int)(pix / a.nx);
+        const int64_t zg = a.zg0 + z;
+        // ---- primal: sum_L D_L u_L + sum_v S_v |nabla u_v|
+        float uc[kMaxNodes], un[kMaxNodes];
+        labels_at(a, a.u + z * ups + pix, P, uc);
+        for (int l = 0; l < NL; ++l) e_acc += (double)a.D[z * ups + l * P + pix] * (double)uc[NI + l];
+        double g2[kMaxNodes], g1[kMaxNodes];
+        for (int v = 0; v < NV; ++v) { g2[v] = 0.0; g1[v] = 0.0; }
+        if (x < a.nx - 1) {
+            labels_at(a, a.u + z * ups + pix + 1, P, un);
+            for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
+        }
+        if (y < a.ny - 1) {
+            labels_at(a, a.u + z * ups + pix + a.nx, P, un);
+            for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
+        }
+        if (a.ndim == 3 && zg < a.nzg - 1) {
+            labels_at(a, a.u + (z + 1) * ups + pix, P, un);
+            for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
+        }
+        for (int v = 0; v < NV; ++v) {
+            float sv;
+            if (a.s_kind == 0) sv = a.g.s[v];
+            else if (a.s_kind == 1) sv = a.S[z * P + pix];
+            else sv = a.S[(z * NV + v) * P + pix];
+            e_acc += (double)sv * (a.cap == 0 ? sqrt(g2[v]) : g1[v]);
+        }
+        // ---- dual: min over end labels of d_L
+        double d[kMaxNodes];
+        const float *qb = a.q + z * qps + pix;
+        for (int v = 0; v < NV; ++v) {
+            double dv = (double)qb[v * P] - (x > 0 ? (double)qb[v * P - 1] : 0.0);
+            dv += (double)qb[(NV + v) * P] - (y > 0 ? (double)qb[(NV + v) * P - a.nx] : 0.0);
+            if (a.ndim == 3)
+                dv += (double)qb[(2 * NV + v) * P] - (zg > 0 ? (double)qb[(2 * NV + v) * P - qps] : 0.0);
+            d[v] = dv;
+        }
+        for (int l = 0; l < NL; ++l) d[NI + l] += (double)a.D[z * ups + l * P + pix];
+        for (int ii = 0; ii < NI; ++ii)
+            for (int j = ii + 1; j < NV; ++j) d[j] += (double)a.g.w[ii][j] * d[ii];
+        double mn = d[NI];
+        for (int l = 1; l < NL; ++l) mn = fmin(mn, d[NI + l]);
+        f_acc += mn;
+    }
+    __shared__ double se[256], sf[256];
+    se[threadIdx.x] = e_acc;
+    sf[threadIdx.x] = f_acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) { se[threadIdx.x] += se[threadIdx.x + s]; sf[threadIdx.x] += sf[threadIdx.x + s]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { partial[2 * blockIdx.x] = se[0]; partial[2 * blockIdx.x + 1] = sf[0]; }
+}
+
+__global__ void energy_finish_kernel(const double *partial, int n, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double e = 0.0, f = 0.0;
+        for (int i = 0; i < n; ++i) { e += partial[2 * i]; f += partial[2 * i + 1]; }
+        out[0] = e;
+        out[1] = f;
+    }
+}
+
+cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st) {
+    fill_kernel<<<1184, 256, 0, st>>>(p, n, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int64_t P, int64_t nz, cudaStream_t st) {
+    argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, P, nz);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_nonneg(const float *p, int64_t n, unsigned int *flag, cudaStream_t st) {
+    min_kernel<<<592, 256, 0, st>>>(p, n, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energy(const EnergyArgs &a, double *partial, int nblocks, double *out, cudaStream_t st) {
+    energy_kernel<<<nblocks, 256, 0, st>>>(a, partial);
+    energy_finish_kernel<<<1, 32, 0, st>>>(partial, nblocks, out);
+    return cudaGetLastError();
+}
+
+}  // namespace pf

@@ -1,0 +1,28 @@
+// pf_aux.cuh -- auxiliary kernels (init, labeling, energies, validation).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pf_kernels.cuh"
+
+namespace pf {
+
+struct EnergyArgs {
+    const float *u;   // current u, plane 0 (the plane above the slab must be current for the primal)
+    const float *q;   // current q, plane 0 (the plane below must be current for the dual)
+    const float *D;
+    const float *S;
+    int nx, ny, nzl, zg0, nzg, ndim;
+    int NI, NL, NV;
+    int s_kind, cap;
+    GraphConst g;
+};
+
+constexpr int kEnergyBlocks = 592;
+
+cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st);
+cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int64_t P, int64_t nz, cudaStream_t st);
+cudaError_t launch_check_nonneg(const float *p, int64_t n, unsigned int *flag, cudaStream_t st);
+cudaError_t launch_energy(const EnergyArgs &a, double *partial, int nblocks, double *out, cudaStream_t st);
+
+}  // namespace pf

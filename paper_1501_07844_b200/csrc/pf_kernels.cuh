@@ -1,0 +1,280 @@
+// pf_kernels.cuh -- sm_100a kernels of the pseudo-flow iteration (arXiv 1501.07844).
+//
+// One launch of pf_iter_kernel performs one pass of the while-loop body of
+// Algorithm 1 or Algorithm 2 over the whole
+// (slab of the) volume, fused into a single HBM pass:
+//
+//   a1  div q_v(x)          backward differences of the OLD flows
+//   a2  d_v = div q_v (+D_L), top-down pushes in O
+//   a3  u~_L = u_L exp(-(d_L - m)/c), a = sum u~, u' = u~/a          (R1)
+//   a4  M_L = u~_L, bottom-up pushes in O^-1
+//   a5  q^ = q_v - c tau nabla M_v                                  (Eq. 8, Eq. 16)
+//   a6  q' = Proj_{|q| <= S_v}(q^)                                   (R5, R14)
+//   a7  u', q' written to the other half of the ping-pong pair
+//   a8  optional residual max|u' - u| (fused, one atomic per warp)
+//
+// Work decomposition ("2.5-D z-march"): a CTA owns a 32 x TY tile of (x, y)
+// columns and walks a chunk of z planes.  For every plane p it computes the
+// unnormalised masses M(p) of its tile plus a +1 halo in x and y (two extra
+// warps) into a 3-deep shared-memory ring, writes u'(p), then finishes the flow
+// step of plane p-1, which needs M(p-1) at x, x+e_x, x+e_y and M(p) at x.  Each
+// voxel's state is read from HBM once per iteration; the +1 halo columns/rows are
+// re-read from L2.  Node positions: 0..NI-1 internal nodes in topological order,
+// NI..NV-1 end labels in node-id order (a topological order, since end labels
+// have no children).
+//
+// Layouts (internal, per z-plane contiguous so a plane of every label is one
+// chunk for the halo exchange):  u, D: [z][l][y][x];  q: [z][k][v][y][x];
+// S field: [z][y][x] (shared) or [z][v][y][x] (per node).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pf {
+
+constexpr int kMaxNodes = 16;     // non-source nodes handled by the compiled kernels
+constexpr int kMaxInternal = 4;   // internal (non-end) nodes
+constexpr int kTX = 32;
+
+struct GraphConst {
+    float w[kMaxInternal][kMaxNodes];  // w[i][j]: weight of edge (position i -> position j); 0 = no edge; S excluded
+    float s[kMaxNodes];                // capacity scalar per position (PF_S_SCALAR_PER_NODE)
+};
+
+struct IterArgs {
+    const float *u_in;
+    float *u_out;
+    const float *q_in;
+    float *q_out;
+    const float *D;
+    const float *S;   // null when capacities are scalars
+    int nx, ny, nzl;  // local extents
+    int zg0, nzg;     // global z of local plane 0, global nz
+    int zchunk;
+    int ndim;
+    int s_kind;       // 0 scalar per node, 1 shared field, 2 field per node
+    int cap;          // 0 l2, 1 box
+    int shift;        // 0 min, 1 none
+    int check;        // compute the residual this launch
+    float inv_c;
+    float ctau;
+    unsigned int *resid_bits;          // max |u' - u| as float bits (non-negative)
+    unsigned long long *err_voxel;     // min global linear voxel index with a(x) <= 0 / non-finite
+    GraphConst g;
+};
+
+__device__ __forceinline__ float ldg(const float *p) { return __ldg(p); }
+
+template <int NI, int NL, int TY>
+struct IterSmem {
+    static constexpr int NV = NI + NL;
+    static constexpr int kPlane = NV * (TY + 1) * (kTX + 1);
+    static constexpr int kBytes = 3 * kPlane * (int)sizeof(float);
+};
+
+template <int NI, int NL, int TY>
+__global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a) {
+    constexpr int NV = NI + NL;
+    constexpr int RS = kTX + 1;              // smem row stride
+    constexpr int PS = (TY + 1) * RS;        // smem per-node plane stride
+    constexpr int RING = NV * PS;            // smem per ring slot
+    extern __shared__ float Ms[];            // [3][NV][TY+1][33]
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool is_main = warp < TY;
+    int lx, ly;
+    if (is_main) {
+        lx = lane; ly = warp;
+    } else {
+        const int h = (warp - TY) * 32 + lane;
+        if (h < kTX) { lx = h; ly = TY; }
+        else if (h < kTX + TY) { lx = kTX; ly = h - kTX; }
+        else { lx = -1; ly = 0; }
+    }
+    const int x = blockIdx.x * kTX + lx, y = blockIdx.y * TY + ly;
+    const bool active = (lx >= 0) && (x < a.nx) && (y < a.ny);
+    const int64_t P = (int64_t)a.nx * a.ny;
+    const int pix = active ? y * a.nx + x : 0;
+    const int zc0 = blockIdx.z * a.zchunk;
+    const int zc1 = min(zc0 + a.zchunk, a.nzl);
+    const bool has_above = (a.zg0 + zc1) < a.nzg;
+    const int64_t ups = (int64_t)NL * P;
+    const int64_t qps = (int64_t)a.ndim * NV * P;
+    const bool is3 = a.ndim == 3;
+    const int sme = ly * RS + (lx < 0 ? 0 : lx);
+
+    float qzp[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) qzp[v] = 0.f;
+    if (active && is3 && (a.zg0 + zc0) > 0) {
+        const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + 2 * NV * P + pix;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) qzp[v] = ldg(qb + v * P);
+    }
+
+    float resid = 0.f;
+    for (int p = zc0; p <= zc1; ++p) {
+        if (p == zc1 && !has_above) break;  // block-uniform
+        float *Mp = Ms + (p % 3) * RING;
+        // ---------------- stage A: masses of plane p (tile + halo)
+        if (active) {
+            const float *qb = a.q_in + (int64_t)p * qps + pix;
+            float d[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float qx = ldg(qb + v * P);
+                const float qxm = (x > 0) ? ldg(qb + v * P - 1) : 0.f;
+                const float qy = ldg(qb + (NV + v) * P);
+                const float qym = (y > 0) ? ldg(qb + (NV + v) * P - a.nx) : 0.f;
+                float dv = (qx - qxm) + (qy - qym);
+                if (is3) {
+                    const float qz = ldg(qb + (2 * NV + v) * P);
+                    dv += qz - qzp[v];
+                    qzp[v] = qz;
+                }
+                d[v] = dv;
+            }
+            const float *Db = a.D + (int64_t)p * ups + pix;
+#pragma unroll
+            for (int l = 0; l < NL; ++l) d[NI + l] = ldg(Db + l * P) + d[NI + l];
+            // top-down pushes along O \ {S}
+#pragma unroll
+            for (int i = 0; i < NI; ++i)
+#pragma unroll
+                for (int j = i + 1; j < NV; ++j) d[j] = fmaf(a.g.w[i][j], d[i], d[j]);
+            float m = 0.f;
+            if (a.shift == 0) {
+                m = d[NI];
+#pragma unroll
+                for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
+            }
+            const float *ub = a.u_in + (int64_t)p * ups + pix;
+            float ut[NL], uold[NL];
+            float sum = 0.f;
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+                uold[l] = ldg(ub + l * P);
+                ut[l] = uold[l] * expf((m - d[NI + l]) * a.inv_c);
+                sum += ut[l];
+            }
+            if (is_main && p < zc1) {
+                if (!(sum > 0.f) || !(sum <= 3.402823466e38f)) {
+                    const unsigned long long vox =
+                        (unsigned long long)(a.zg0 + p) * (unsigned long long)P + (unsigned long long)pix;
+                    atomicMin(a.err_voxel, vox);
+                }
+                const float inv = 1.f / sum;
+                float *uo = a.u_out + (int64_t)p * ups + pix;
+#pragma unroll
+                for (int l = 0; l < NL; ++l) {
+                    const float nu = ut[l] * inv;
+                    uo[l * P] = nu;
+                    resid = fmaxf(resid, fabsf(nu - uold[l]));
+                }
+            }
+            // bottom-up masses along O^-1 \ {S}
+            float M[NV];
+#pragma unroll
+            for (int l = 0; l < NL; ++l) M[NI + l] = ut[l];
+#pragma unroll
+            for (int i = NI - 1; i >= 0; --i) {
+                float acc = 0.f;
+#pragma unroll
+                for (int j = i + 1; j < NV; ++j) acc = fmaf(a.g.w[i][j], M[j], acc);
+                M[i] = acc;
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) Mp[v * PS + sme] = M[v];
+        }
+        __syncthreads();
+        // ---------------- stage B: flow step + projection of plane p-1
+        if (is_main && active && p > zc0) {
+            const int z = p - 1;
+            const float *Mz = Ms + (z % 3) * RING;
+            const int zg = a.zg0 + z;
+            const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = is3 && (zg < a.nzg - 1);
+            const float *qb = a.q_in + (int64_t)z * qps + pix;
+            float *qo = a.q_out + (int64_t)z * qps + pix;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float mc = Mz[v * PS + sme];
+                const float gx = gxv ? Mz[v * PS + sme + 1] - mc : 0.f;
+                const float gy = gyv ? Mz[v * PS + sme + RS] - mc : 0.f;
+                const float gz = gzv ? Mp[v * PS + sme] - mc : 0.f;
+                float hx = fmaf(-a.ctau, gx, ldg(qb + v * P));
+                float hy = fmaf(-a.ctau, gy, ldg(qb + (NV + v) * P));
+                float hz = is3 ? fmaf(-a.ctau, gz, ldg(qb + (2 * NV + v) * P)) : 0.f;
+                float sv;
+                if (a.s_kind == 0) sv = a.g.s[v];
+                else if (a.s_kind == 1) sv = ldg(a.S + (int64_t)z * P + pix);
+                else sv = ldg(a.S + ((int64_t)z * NV + v) * P + pix);
+                if (a.cap == 0) {
+                    const float n = sqrtf(fmaf(hx, hx, fmaf(hy, hy, hz * hz)));
+                    if (n > sv) {
+                        const float f = sv / n;
+                        hx *= f; hy *= f; hz *= f;
+                    }
+                } else {
+                    hx = fminf(fmaxf(hx, -sv), sv);
+                    hy = fminf(fmaxf(hy, -sv), sv);
+                    hz = fminf(fmaxf(hz, -sv), sv);
+                }
+                qo[v * P] = hx;
+                qo[(NV + v) * P] = hy;
+                if (is3) qo[(2 * NV + v) * P] = hz;
+            }
+        }
+    }
+    // last plane of the volume: no plane above, nabla_z = 0
+    if (!has_above && is_main && active) {
+        const int z = zc1 - 1;
+        const float *Mz = Ms + (z % 3) * RING;
+        const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1;
+        const float *qb = a.q_in + (int64_t)z * qps + pix;
+        float *qo = a.q_out + (int64_t)z * qps + pix;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float mc = Mz[v * PS + sme];
+            const float gx = gxv ? Mz[v * PS + sme + 1] - mc : 0.f;
+            const float gy = gyv ? Mz[v * PS + sme + RS] - mc : 0.f;
+            float hx = fmaf(-a.ctau, gx, ldg(qb + v * P));
+            float hy = fmaf(-a.ctau, gy, ldg(qb + (NV + v) * P));
+            float hz = is3 ? ldg(qb + (2 * NV + v) * P) : 0.f;
+            float sv;
+            if (a.s_kind == 0) sv = a.g.s[v];
+            else if (a.s_kind == 1) sv = ldg(a.S + (int64_t)z * P + pix);
+            else sv = ldg(a.S + ((int64_t)z * NV + v) * P + pix);
+            if (a.cap == 0) {
+                const float n = sqrtf(fmaf(hx, hx, fmaf(hy, hy, hz * hz)));
+                if (n > sv) {
+                    const float f = sv / n;
+                    hx *= f; hy *= f; hz *= f;
+                }
+            } else {
+                hx = fminf(fmaxf(hx, -sv), sv);
+                hy = fminf(fmaxf(hy, -sv), sv);
+                hz = fminf(fmaxf(hz, -sv), sv);
+            }
+            qo[v * P] = hx;
+            qo[(NV + v) * P] = hy;
+            if (is3) qo[(2 * NV + v) * P] = hz;
+        }
+    }
+    if (a.check) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) resid = fmaxf(resid, __shfl_xor_sync(0xffffffffu, resid, o));
+        if (lane == 0 && resid > 0.f) atomicMax(a.resid_bits, __float_as_uint(resid));
+    }
+}
+
+// Launch table entry (pf_iter_table.cu); returns false if (NI, NL) is not compiled in.
+struct IterKernelInfo {
+    const void *func;
+    int threads;
+    int smem_bytes;
+    int tile_y;
+};
+
+bool iter_kernel_lookup(int NI, int NL, IterKernelInfo *info);
+
+}  // namespace pf

@@ -1,0 +1,95 @@
+"""Multi-GPU z-slab driver: one process per GPU, halo planes exchanged with torch.distributed P2P.
+
+Row e of the hot-path scope: the volume is split into z-slabs of
+ceil(nz/P) planes; after every iteration rank r sends its first-plane u and q to r-1 and its
+last-plane q^z to r+1 (pf_halo_regions names the device ranges).  The exchange rides on the
+process group (NCCL over NVLink on a GPU box, gloo on CPU for the host-side tests) and is
+ordered on the solver's stream, which is set to torch's current stream.
+"""
+from __future__ import annotations
+
+from typing import Dict, Optional
+
+import torch
+import torch.distributed as dist
+
+from .solver import Solver, slab_bounds
+
+
+class _CudaBuf:
+    """__cuda_array_interface__ view of a raw device range (zero-copy into torch)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def device_view(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
+    return torch.as_tensor(_CudaBuf(ptr, nbytes), device=device)
+
+
+def halo_exchange(regions: Dict[str, Optional[torch.Tensor]], rank: int, world: int, group=None):
+    """Exchange one iteration's halo planes.  regions: send_down_u, send_down_q, recv_up_u, recv_up_q,
+    send_up_qz, recv_down_qz (None where the neighbour does not exist).  Per peer pair the messages
+    are posted in the same order on both sides (u, then q downward; q^z upward)."""
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, regions["send_down_u"], rank - 1, group))
+        ops.append(dist.P2POp(dist.isend, regions["send_down_q"], rank - 1, group))
+        if regions.get("recv_down_qz") is not None:
+            ops.append(dist.P2POp(dist.irecv, regions["recv_down_qz"], rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.irecv, regions["recv_up_u"], rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, regions["recv_up_q"], rank + 1, group))
+        if regions.get("send_up_qz") is not None:
+            ops.append(dist.P2POp(dist.isend, regions["send_up_qz"], rank + 1, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+class DistSolver:
+    """The rank's slab solver plus its halo exchange.  `make_solver(slab)` builds the Solver."""
+
+    def __init__(self, make_solver, nz: int, rank: int, world: int, device: torch.device, group=None):
+        self.rank, self.world, self.group = rank, world, group
+        self.device = device
+        self.bounds = slab_bounds(nz, world)
+        assert len(self.bounds) == world, "every rank needs at least one plane"
+        self.slab = self.bounds[rank]
+        self.solver: Solver = make_solver(self.slab)
+        self.solver.set_stream(torch.cuda.current_stream(device).cuda_stream)
+
+    def _regions(self):
+        h = self.solver.halo()
+        dv = self.device
+        return {
+            "send_down_u": device_view(h.send_down_u, h.bytes_u, dv) if h.send_down_u else None,
+            "send_down_q": device_view(h.send_down_q, h.bytes_q, dv) if h.send_down_q else None,
+            "recv_up_u": device_view(h.recv_up_u, h.bytes_u, dv) if h.recv_up_u else None,
+            "recv_up_q": device_view(h.recv_up_q, h.bytes_q, dv) if h.recv_up_q else None,
+            "send_up_qz": device_view(h.send_up_qz, h.bytes_qz, dv) if h.send_up_qz else None,
+            "recv_down_qz": device_view(h.recv_down_qz, h.bytes_qz, dv) if h.recv_down_qz else None,
+        }
+
+    def iterate(self, n: int, residual: bool = False):
+        if self.world == 1:
+            return self.solver.iterate(n, residual)
+        r = None
+        for t in range(n):
+            last = residual and t == n - 1
+            val = self.solver.iterate(1, last)
+            if self.world > 1:
+                halo_exchange(self._regions(), self.rank, self.world, self.group)
+            if last:
+                rt = torch.tensor([val], device=self.device)
+                if self.world > 1:
+                    dist.all_reduce(rt, op=dist.ReduceOp.MAX, group=self.group)
+                r = float(rt.item())
+        return r
+
+    def reset(self):
+        self.solver.reset()
+
+    def close(self):
+        self.solver.close()

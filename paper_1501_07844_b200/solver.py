@@ -1,0 +1,143 @@
+"""Convenience wrappers over the C-ABI (marshalling only; all compute is in libpf.so)."""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD,
+               pf_create, pf_destroy, pf_exchange_local, pf_get_energy, pf_get_flows, pf_get_kernel_info,
+               pf_get_labeling, pf_halo_regions, pf_iterate, pf_iterations, pf_reset, pf_set_stream)
+
+
+class Solver:
+    """One pseudo-flow solver (one device, one z-slab or the whole volume).
+
+    graph = (num_nodes, parent, child, weight) with node 0 the source;
+    D = one float32 [z][y][x] volume per end label (numpy or CUDA tensor) covering the
+    slab plus the plane above it; capacities: exactly one of `s_scalars` ([num_nodes]),
+    `s_shared` (one volume) or `s_fields` (one volume per non-source node).
+    """
+
+    def __init__(self, dims: Sequence[int], ndim: int, graph, D: Sequence, *, s_scalars=None, s_shared=None,
+                 s_fields=None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2, shift: int = PF_SHIFT_MIN,
+                 check_every: int = 10, slab: Optional[Sequence[int]] = None):
+        num_nodes, parent, child, weight = graph
+        self.dims = tuple(int(v) for v in dims)
+        self.ndim = ndim
+        self.num_nodes = int(num_nodes)
+        self.NL = len(D)
+        self.slab = (0, self.dims[2]) if slab is None else (int(slab[0]), int(slab[1]))
+        if s_scalars is not None:
+            kind, fields = PF_S_SCALAR_PER_NODE, None
+        elif s_shared is not None:
+            kind, fields = PF_S_SHARED_FIELD, [s_shared]
+        else:
+            kind, fields = PF_S_FIELD_PER_NODE, list(s_fields)
+        self.h = pf_create(self.dims, ndim, num_nodes, parent, child, weight, list(D), kind, s_scalars, fields, c, tau, cap,
+                           shift, check_every, slab)
+
+    # ---------------------------------------------------------------- C-ABI calls
+    @property
+    def nz_local(self) -> int:
+        return self.slab[1] - self.slab[0]
+
+    @property
+    def shape(self):
+        return (self.nz_local, self.dims[1], self.dims[0])
+
+    def reset(self):
+        pf_reset(self.h)
+
+    def iterate(self, n: int, residual: bool = False):
+        return pf_iterate(self.h, n, residual)
+
+    def set_stream(self, stream_ptr: int):
+        pf_set_stream(self.h, stream_ptr)
+
+    def labeling(self, u_out=None, argmax_out=None):
+        """Return (u [NL][z][y][x] float32, argmax [z][y][x] uint8) as numpy unless outputs are given."""
+        ret_u = u_out is None
+        ret_a = argmax_out is None
+        if u_out is None:
+            u_out = np.empty((self.NL,) + self.shape, dtype=np.float32)
+        if argmax_out is None:
+            argmax_out = np.empty(self.shape, dtype=np.uint8)
+        pf_get_labeling(self.h, u_out, argmax_out)
+        return u_out, argmax_out
+
+    def flows(self):
+        q = np.empty((self.num_nodes - 1, self.ndim) + self.shape, dtype=np.float32)
+        pf_get_flows(self.h, q)
+        return q
+
+    def energy(self):
+        return pf_get_energy(self.h)
+
+    def iterations(self) -> int:
+        return pf_iterations(self.h)
+
+    def halo(self):
+        return pf_halo_regions(self.h)
+
+    def kernel_info(self) -> dict:
+        return pf_get_kernel_info(self.h)
+
+    def close(self):
+        if self.h:
+            pf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def slab_bounds(nz: int, parts: int) -> List[tuple]:
+    """z-slabs of ceil(nz/parts) planes; the last may be shorter."""
+    h = -(-nz // parts)
+    out = []
+    for r in range(parts):
+        z0, z1 = r * h, min(nz, (r + 1) * h)
+        if z0 < z1:
+            out.append((z0, z1))
+    return out
+
+
+class SlabSet:
+    """A volume split into consecutive z-slab solvers driven from one process (one or several
+    devices); halos are exchanged by pf_exchange_local after every iteration."""
+
+    def __init__(self, solvers: Sequence[Solver]):
+        self.solvers = list(solvers)
+        self.handles = [s.h for s in self.solvers]
+
+    def iterate(self, n: int, residual: bool = False):
+        r = None
+        for t in range(n):
+            last = residual and t == n - 1
+            vals = [s.iterate(1, last) for s in self.solvers]
+            pf_exchange_local(self.handles)
+            if last:
+                r = max(vals)
+        return r
+
+    def exchange(self):
+        pf_exchange_local(self.handles)
+
+    def labeling(self):
+        us, ams = zip(*[s.labeling() for s in self.solvers])
+        return np.concatenate(us, axis=1), np.concatenate(ams, axis=0)
+
+    def flows(self):
+        return np.concatenate([s.flows() for s in self.solvers], axis=2)
+
+    def energy(self):
+        es = [s.energy() for s in self.solvers]
+        return sum(e for e, _ in es), sum(f for _, f in es)
+
+    def close(self):
+        for s in self.solvers:
+            s.close()

@@ -1,0 +1,69 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+* after a few iterations: sampled voxels against the oracle run on windows around them (the
+  window method is itself checked on CPU in test_window_method.py);
+* after the configured iteration count: properties that hold at any size (simplex, capacity
+  feasibility, q^k(last) = 0, weak duality of the device energies).
+Samples include volume corners and faces, CTA-tile edges (x = 31|32, y = 7|8) and z-chunk edges.
+"""
+import numpy as np
+import pytest
+
+import phantoms as P
+from helpers import solver_from_inputs, window_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _sample_points(cfg, zchunk):
+    nx, ny, nz = cfg.nx, cfg.ny, cfg.nz
+    pts = [(0, 0, 0), (nx - 1, ny - 1, nz - 1), (nx - 1, 0, nz // 2), (0, ny - 1, 0), (nx // 2, ny // 2, nz // 2),
+           (31, 7, zchunk - 1), (32, 8, zchunk), (63, 15, 2 * zchunk - 1) if 2 * zchunk < nz else (63, 15, nz - 2),
+           (nx - 33, ny - 9, nz - 1), (100 % nx, 201 % ny, 77 % nz)]
+    return pts
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_fullsize_sampled_parity(name):
+    cfg = P.config(name)
+    inp = P.generate(cfg)
+    s = solver_from_inputs(inp)
+    n = 6
+    s.iterate(n)
+    u, _ = s.labeling()
+    q = s.flows()
+    zchunk = s.kernel_info()["z_chunk"]
+    s.close()
+    worst = 0.0
+    for pt in _sample_points(cfg, zchunk):
+        reg, ur, qr = window_oracle(cfg, pt, n, r=2)
+        sl = tuple(slice(a, b) for a, b in reg)
+        ug = u[(slice(None),) + sl].astype(np.float64)
+        qg = q[(slice(None), slice(None)) + sl].astype(np.float64)
+        worst = max(worst, float(np.max(np.abs(ug - ur))), float(np.max(np.abs(qg - qr))))
+        assert np.array_equal(np.argmax(ug, 0), np.argmax(ur, 0))
+    assert worst <= 1e-4, worst
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_fullsize_properties_after_configured_iterations(name):
+    cfg = P.config(name)
+    inp = P.generate(cfg)
+    s = solver_from_inputs(inp)
+    r = s.iterate(cfg.iters, residual=True)
+    assert 0 <= r < 1
+    e, f = s.energy()
+    assert e >= f - 1e-7 * abs(e)
+    u, am = s.labeling()
+    assert np.all(u >= 0)
+    assert float(np.max(np.abs(u.sum(0, dtype=np.float64) - 1.0))) < 1e-5
+    assert np.array_equal(am, np.argmax(u, 0).astype(np.uint8))
+    del u
+    q = s.flows()
+    s.close()
+    # q^k at the last index along k stays 0 (reading R4)
+    assert np.all(q[:, 0, :, :, -1] == 0) and np.all(q[:, 1, :, -1, :] == 0) and np.all(q[:, 2, -1] == 0)
+    nrm = np.sqrt(np.sum(q.astype(np.float64) ** 2, axis=1))
+    fields = inp.s_fields()
+    for v in range(1, inp.graph.num_nodes):
+        assert np.all(nrm[v - 1] <= fields[v].astype(np.float64) * (1 + 1e-6) + 1e-30)

@@ -1,0 +1,203 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): u and q within max-abs 1e-4 after the configured iteration
+count, thresholded labeling agreeing on >= 99.99% of voxels.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import phantoms as P
+from helpers import compare, solver_from_inputs, with_field_per_node
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_both(inp, n, shift=O.SHIFT_MIN, cap=None, **kw):
+    s = solver_from_inputs(inp, shift=shift, cap=cap, **kw)
+    s.iterate(n)
+    u, _ = s.labeling()
+    q = s.flows()
+    s.close()
+    ur, qr = O.run_inputs(inp, n, shift=shift, cap=cap)
+    return u, q, ur, qr
+
+
+@pytest.mark.parametrize("shift", [O.SHIFT_MIN, O.SHIFT_NONE])
+def test_c1_every_iteration(shift):
+    """configs[0] (C1, 2D Potts 64x64, K=3, 200 iterations): parity at EVERY iteration."""
+    inp = P.generate(P.config("C1"))
+    s = solver_from_inputs(inp, shift=shift)
+    ur, qr = O.init_state(3, 3, inp.shape, 2)
+    for t in range(1, 201):
+        s.iterate(1)
+        O.run_inputs(inp, 1, shift=shift, state=(ur, qr))
+        if t % 20 == 0 or t < 5:
+            u, am = s.labeling()
+            q = s.flows()
+            compare(u, q, ur, qr)
+            assert np.array_equal(am, O.argmax(u))
+    s.close()
+
+
+@pytest.mark.parametrize("name,dims,n,shift", [
+    ("C2", (64, 64, 64), 300, O.SHIFT_MIN),
+    ("C2", (67, 45, 37), 300, O.SHIFT_NONE),     # ragged tiles in x, y and z-chunks
+    ("C3", (48, 40, 36), 300, O.SHIFT_MIN),
+    ("C3", (33, 17, 9), 300, O.SHIFT_NONE),
+    ("C4", (40, 40, 40), 300, O.SHIFT_MIN),
+    ("C4", (35, 70, 21), 120, O.SHIFT_NONE),
+    ("C5", (40, 36, 24), 200, O.SHIFT_MIN),      # K = 16
+])
+def test_configs_scaled(name, dims, n, shift):
+    inp = P.generate(P.config(name).resized(*dims))
+    u, q, ur, qr = _run_both(inp, n, shift)
+    compare(u, q, ur, qr)
+
+
+@pytest.mark.parametrize("case", ["linf_potts", "linf_dag", "field_per_node", "k2", "line_x", "line_y", "single_voxel",
+                                  "one_plane_3d", "two_planes", "2d_ragged", "2d_dag"])
+def test_edge_cases(case):
+    cap = None
+    if case == "linf_potts":
+        inp, cap = P.generate(P.config("C2").resized(21, 19, 17)), O.CAP_LINF
+    elif case == "linf_dag":
+        inp, cap = P.generate(P.config("C4").resized(19, 22, 13)), O.CAP_LINF
+    elif case == "field_per_node":
+        inp = with_field_per_node(P.generate(P.config("C3").resized(23, 29, 11)))
+    elif case == "k2":
+        c = P.config("C2").resized(30, 20, 10)
+        inp = P.generate(P.Config("k2", 3, 30, 20, 10, "potts", 2, 6, 0.15, "sq", "edge", 0.05, 100, seed=77))
+    elif case == "line_x":
+        inp = P.generate(P.config("C2").resized(70, 1, 1))
+    elif case == "line_y":
+        inp = P.generate(P.config("C2").resized(1, 50, 3))
+    elif case == "single_voxel":
+        inp = P.generate(P.config("C2").resized(1, 1, 1))
+    elif case == "one_plane_3d":
+        inp = P.generate(P.config("C4").resized(40, 9, 1))
+    elif case == "two_planes":
+        inp = P.generate(P.config("C2").resized(35, 33, 2))
+    elif case == "2d_ragged":
+        inp = P.generate(P.config("C1").resized(97, 41, 1))
+    else:
+        cfg = P.config("C4")
+        inp = P.generate(P.Config("dag2d", 2, 45, 38, 1, "dag", 6, 4, 0.15, "sq", "per_node_uniform", 0.0, 0,
+                                  seed=cfg.seed))
+    u, q, ur, qr = _run_both(inp, 150, cap=cap)
+    compare(u, q, ur, qr)
+
+
+def test_uniform_data_constant_solution_bitwise():
+    """Spatially uniform D: u(x) is the same for every voxel (bitwise) and q stays exactly 0 (pin P4)."""
+    cfg = P.config("C4").resized(40, 33, 20)
+    inp = P.generate(cfg)
+    r = np.random.default_rng(3)
+    inp.D[:] = r.uniform(0, 1, size=(6, 1, 1, 1)).astype(np.float32)
+    s = solver_from_inputs(inp)
+    s.iterate(50)
+    u, _ = s.labeling()
+    q = s.flows()
+    assert np.all(q == 0)
+    assert np.all(u == u[:, :1, :1, :1])
+    ur, qr = O.run_inputs(inp, 50)
+    compare(u, q, ur, qr, tol=1e-6)
+
+
+def test_device_inputs_equal_host_inputs():
+    inp = P.generate(P.config("C2").resized(40, 36, 20))
+    a = solver_from_inputs(inp)
+    b = solver_from_inputs(inp, device_inputs=True)
+    a.iterate(30)
+    b.iterate(30)
+    assert np.array_equal(a.labeling()[0], b.labeling()[0]) and np.array_equal(a.flows(), b.flows())
+
+
+def test_deterministic_and_reset():
+    inp = P.generate(P.config("C3").resized(50, 40, 30))
+    s = solver_from_inputs(inp)
+    s.iterate(40)
+    u1, a1 = s.labeling()
+    q1 = s.flows()
+    s.reset()
+    assert s.iterations() == 0
+    s.iterate(40)
+    u2, a2 = s.labeling()
+    assert np.array_equal(u1, u2) and np.array_equal(a1, a2) and np.array_equal(q1, s.flows())
+
+
+def test_split_calls_equal_one_call():
+    """iterate(a) + iterate(b) == iterate(a + b), bitwise (ping-pong bookkeeping)."""
+    inp = P.generate(P.config("C2").resized(33, 30, 27))
+    s1, s2 = solver_from_inputs(inp), solver_from_inputs(inp)
+    s1.iterate(37)
+    s2.iterate(10); s2.iterate(1); s2.iterate(26)
+    assert np.array_equal(s1.labeling()[0], s2.labeling()[0]) and np.array_equal(s1.flows(), s2.flows())
+
+
+def test_residual_matches_state_difference():
+    inp = P.generate(P.config("C2").resized(40, 30, 20))
+    s = solver_from_inputs(inp, check_every=5)
+    s.iterate(9)
+    u9, _ = s.labeling()
+    r = s.iterate(1, residual=True)      # iteration 10 is a check iteration
+    u10, _ = s.labeling()
+    assert r == float(np.max(np.abs(u10 - u9)))
+    assert s.iterate(3, residual=True) == -1.0   # 11..13: no check
+
+
+def test_energies_match_oracle_and_weak_duality():
+    """Device energies (fp64 accumulation) of the GPU state vs the oracle energies of the oracle state."""
+    from oracle import energy as E
+    for name, dims in (("C2", (30, 28, 26)), ("C4", (26, 24, 22)), ("C1", (64, 64, 1))):
+        inp = P.generate(P.config(name).resized(*dims))
+        g = inp.graph
+        s = solver_from_inputs(inp)
+        for n in (0, 1, 20, 100):
+            s.iterate(n)
+            e, f = s.energy()
+            assert e >= f - 1e-9 * abs(e)
+        tot = s.iterations()
+        ur, qr = O.run_inputs(inp, tot)
+        S = np.zeros((g.num_nodes,) + inp.shape)
+        for v in range(1, g.num_nodes):
+            S[v] = inp.s_fields()[v]
+        eo = E.primal(ur, inp.D.astype(np.float64), S, g.num_nodes, g.parent, g.child, g.weight, inp.cfg.ndim)
+        fo = E.dual(qr, inp.D.astype(np.float64), g.num_nodes, g.parent, g.child, g.weight, inp.cfg.ndim)
+        e, f = s.energy()
+        assert abs(e - eo) <= 1e-4 * abs(eo) and abs(f - fo) <= 1e-4 * abs(eo)
+
+
+def test_numeric_error_reported_with_voxel():
+    import paper_1501_07844_b200 as pf
+    inp = P.generate(P.config("C2").resized(20, 20, 20))
+    inp.D[:, 7, 5, 3] = np.nan       # a(x) not finite at voxel (3, 5, 7)
+    s = solver_from_inputs(inp)
+    with pytest.raises(pf.PFError) as ei:
+        s.iterate(1, residual=True)
+    assert ei.value.status == pf.PF_ERR_NUMERIC and "x=3, y=5, z=7" in str(ei.value)
+    with pytest.raises(pf.PFError) as ei:
+        s.iterate(1)
+    assert ei.value.status == pf.PF_ERR_STATE
+
+
+def test_graph_and_input_validation():
+    import paper_1501_07844_b200 as pf
+    D = [np.zeros((2, 3, 4), np.float32)] * 3
+    base = dict(dims=(4, 3, 2), ndim=3)
+    with pytest.raises(pf.PFError) as ei:   # cycle + weight <= 0
+        pf.Solver(base["dims"], 3, (4, [0, 1, 2, 3, 1], [1, 2, 3, 1, 3], [1, 1, 1, 1, -1]), D, s_scalars=[0, .1, .1, .1])
+    assert ei.value.status == pf.PF_ERR_GRAPH and "cycle" in str(ei.value) and "weight" in str(ei.value)
+    with pytest.raises(pf.PFError) as ei:   # W_(S,L) != 1
+        pf.Solver(base["dims"], 3, (4, [0, 0, 0], [1, 2, 3], [1, 1, 0.5]), D, s_scalars=[0, .1, .1, .1])
+    assert ei.value.status == pf.PF_ERR_GRAPH and "W_(S,3)" in str(ei.value)
+    with pytest.raises(pf.PFError) as ei:   # negative capacity
+        pf.Solver(base["dims"], 3, (4, [0, 0, 0], [1, 2, 3], [1, 1, 1]), D, s_scalars=[0, .1, -.1, .1])
+    assert ei.value.status == pf.PF_ERR_INVALID
+    with pytest.raises(pf.PFError) as ei:   # negative capacity field
+        f = np.full((2, 3, 4), 0.1, np.float32); f[1, 2, 3] = -1
+        pf.Solver(base["dims"], 3, (4, [0, 0, 0], [1, 2, 3], [1, 1, 1]), D, s_shared=f)
+    assert ei.value.status == pf.PF_ERR_INVALID
+    with pytest.raises(pf.PFError) as ei:
+        pf.Solver(base["dims"], 3, (4, [0, 0, 0], [1, 2, 3], [1, 1, 1]), D, s_scalars=[0, .1, .1, .1], c=0.0)
+    assert ei.value.status == pf.PF_ERR_INVALID

@@ -1,0 +1,32 @@
+"""z-slab decomposition on one GPU (row e): P consecutive slab solvers exchanging halo planes with
+pf_exchange_local reproduce the single-domain solver BIT FOR BIT (every voxel's arithmetic is a
+pure function of its neighbourhood)."""
+import numpy as np
+import pytest
+
+import paper_1501_07844_b200 as pf
+import phantoms as P
+from helpers import solver_from_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,dims,parts", [("C2", (48, 40, 36), 2), ("C2", (48, 40, 37), 3), ("C4", (40, 33, 29), 4),
+                                             ("C3", (33, 30, 24), 8), ("C5", (36, 33, 20), 5)])
+def test_slabs_bitwise_equal_single_domain(name, dims, parts):
+    cfg = P.config(name).resized(*dims)
+    inp = P.generate(cfg)
+    ref = solver_from_inputs(inp)
+    ref.iterate(25)
+    u_ref, a_ref = ref.labeling()
+    q_ref = ref.flows()
+    e_ref = ref.energy()
+    slabs = pf.SlabSet([solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, parts)])
+    slabs.iterate(25)
+    u, a = slabs.labeling()
+    q = slabs.flows()
+    assert np.array_equal(u, u_ref) and np.array_equal(a, a_ref) and np.array_equal(q, q_ref)
+    e = slabs.energy()
+    assert abs(e[0] - e_ref[0]) <= 1e-9 * abs(e_ref[0]) and abs(e[1] - e_ref[1]) <= 1e-9 * abs(e_ref[0])
+    slabs.close()
+    ref.close()
