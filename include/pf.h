@@ -171,6 +171,8 @@ typedef struct {
     int64_t algorithmic_bytes_per_iteration; /* DESIGN.md "Roofline" */
     int64_t device_bytes;                    /* resident footprint of this solver */
     int64_t kernel_launches;                 /* this solver's own kernels launched so far */
+    int32_t staged;                          /* 1: TMA-staged persistent kernel, 0: global-load kernel */
+    int32_t work_items;                      /* (tile, z-chunk) items per iteration */
 } pf_kernel_info;
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info);

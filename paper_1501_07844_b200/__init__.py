@@ -72,7 +72,7 @@ class pf_kernel_info(ctypes.Structure):
                 ("threads_per_cta", ctypes.c_int32), ("ctas", ctypes.c_int32), ("regs_per_thread", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("algorithmic_bytes_per_iteration", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64)]
+                ("kernel_launches", ctypes.c_int64), ("staged", ctypes.c_int32), ("work_items", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p

@@ -11,9 +11,12 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "pf.h"
 #include "pf_aux.cuh"
 #include "pf_kernels.cuh"
+#include "pf_staged.cuh"
 
 using namespace pf;
 
@@ -177,7 +180,8 @@ struct pf_solver {
     int ndim = 3;
     int64_t nx = 0, ny = 0, nz = 0;
     int64_t z0 = 0, z1 = 0, nzl = 0;
-    int64_t P = 0;
+    int64_t P = 0;       // channel-plane stride = pitch * ny
+    int64_t pitch = 0;   // row pitch (elements), multiple of 4 for TMA
     Compiled gc;
     pf_config cfg{};
     int s_kind = 0;
@@ -199,6 +203,13 @@ struct pf_solver {
     int64_t device_bytes = 0;
     bool last_resid_valid = false;
     int64_t launches = 0;
+    // TMA-staged persistent kernel (default) -- see pf_staged.cuh
+    bool staged = false;
+    StagedKernelInfo sinfo{};
+    CUtensorMap tm_q[2], tm_u[2], tm_D, tm_S;
+    int s_ch = 0;
+    int tiles_x = 0, tiles = 0, items = 0, sgrid = 0;
+    unsigned int tx_bytes = 0;
 };
 
 namespace {
@@ -255,25 +266,75 @@ pf_status init_state(pf_solver *s) {
     return PF_OK;
 }
 
-void choose_chunking(pf_solver *s) {
-    const int gx = (int)((s->nx + kTX - 1) / kTX), gy = (int)((s->ny + s->kinfo.tile_y - 1) / s->kinfo.tile_y);
-    const int64_t tiles = (int64_t)gx * gy;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
-    const int nzl = (int)s->nzl;
-    // minimise (CTAs per SM, rounded up) x (planes per CTA incl. the look-ahead plane)
+// z-chunk length minimising (work items per CTA slot, rounded up) x (planes per item incl. the
+// look-ahead plane); `slots` = CTAs resident at once (persistent grid) or SMs (one-shot grid).
+int best_chunks(int64_t tiles, int nzl, int64_t slots) {
     int best_n = 1;
     double best_cost = 1e300;
     const int max_n = std::max(1, nzl / 4);
     for (int n = 1; n <= max_n; ++n) {
         const int ch = (nzl + n - 1) / n;
         const int nn = (nzl + ch - 1) / ch;
-        const double per_sm = std::ceil((double)(tiles * nn) / sms);
-        const double cost = per_sm * (ch + 1);
+        const double cost = std::ceil((double)(tiles * nn) / slots) * (ch + 1);
         if (cost < best_cost - 1e-9) { best_cost = cost; best_n = nn; }
     }
-    s->zchunk = (nzl + best_n - 1) / best_n;
-    s->grid = dim3(gx, gy, (nzl + s->zchunk - 1) / s->zchunk);
+    return best_n;
+}
+
+void choose_chunking(pf_solver *s) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+    const int nzl = (int)s->nzl;
+    const int ty = s->staged ? s->sinfo.tile_y : s->kinfo.tile_y;
+    const int gx = (int)((s->nx + kTX - 1) / kTX), gy = (int)((s->ny + ty - 1) / ty);
+    const int64_t tiles = (int64_t)gx * gy;
+    if (s->staged) {
+        const int occ = std::max(1, s->ctas_per_sm);
+        const int64_t slots = (int64_t)sms * occ;
+        const int n = best_chunks(tiles, nzl, slots);
+        s->zchunk = (nzl + n - 1) / n;
+        const int nch = (nzl + s->zchunk - 1) / s->zchunk;
+        s->tiles_x = gx;
+        s->tiles = (int)tiles;
+        s->items = (int)(tiles * nch);
+        s->sgrid = (int)std::min<int64_t>(slots, s->items);
+        s->grid = dim3(s->sgrid, 1, 1);
+    } else {
+        const int n = best_chunks(tiles, nzl, sms);
+        s->zchunk = (nzl + n - 1) / n;
+        s->grid = dim3(gx, gy, (nzl + s->zchunk - 1) / s->zchunk);
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+// 4-D fp32 tensor map over an internal array [plane][channel][y][pitch] (x fastest); elements with
+// x >= nx, y outside [0, ny) or plane outside [0, nplanes) read as 0 (TMA out-of-bounds fill).
+bool encode4d(CUtensorMap *m, const float *base, int64_t nx, int64_t ny, int64_t pitch, int64_t nch, int64_t nplanes,
+              int bx, int by, int bc) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nch, (cuuint64_t)nplanes};
+    cuuint64_t strides[3] = {(cuuint64_t)(pitch * 4), (cuuint64_t)(pitch * ny * 4), (cuuint64_t)(pitch * ny * nch * 4)};
+    cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bc, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 pf_status check_usable(const pf_solver *s) {
@@ -288,19 +349,27 @@ pf_status check_numeric(pf_solver *s) {
     CK(cudaStreamSynchronize(s->stream), "sync");
     if (v != ~0ull) {
         s->poisoned = true;
-        const unsigned long long P = (unsigned long long)s->P;
+        const unsigned long long nx = (unsigned long long)s->nx, ny = (unsigned long long)s->ny;
         return fail(PF_ERR_NUMERIC, "numerical collapse: a(x) <= 0 or not finite at voxel (x=%llu, y=%llu, z=%llu)",
-                    (v % P) % (unsigned long long)s->nx, (v % P) / (unsigned long long)s->nx, v / P);
+                    v % nx, (v / nx) % ny, v / (nx * ny));
     }
     return PF_OK;
 }
 
-// copy one volume [z][y][x] (nzc planes) into / out of a strided internal layout
-cudaError_t copy_planes(float *dst, int64_t dst_pitch_floats, const float *src, int64_t src_pitch_floats,
-                        int64_t plane_floats, int64_t nplanes, cudaStream_t st) {
-    if (nplanes <= 0) return cudaSuccess;
-    return cudaMemcpy2DAsync(dst, dst_pitch_floats * sizeof(float), src, src_pitch_floats * sizeof(float),
-                             plane_floats * sizeof(float), nplanes, cudaMemcpyDefault, st);
+// Copy `nz` planes of one dense volume [z][y][x] (x fastest) into channel `c` of an internal array
+// [plane][channel][y][pitch] with `nch` channels (to_internal), or back out of it.
+cudaError_t copy_volume(bool to_internal, float *internal_c, int64_t nch, float *dense, int64_t nx, int64_t ny,
+                        int64_t pitch, int64_t nz, cudaStream_t st) {
+    if (nz <= 0) return cudaSuccess;
+    cudaMemcpy3DParms p;
+    memset(&p, 0, sizeof(p));
+    cudaPitchedPtr ip = make_cudaPitchedPtr(internal_c, (size_t)pitch * 4, (size_t)nx, (size_t)(ny * nch));
+    cudaPitchedPtr dp = make_cudaPitchedPtr(dense, (size_t)nx * 4, (size_t)nx, (size_t)ny);
+    p.srcPtr = to_internal ? dp : ip;
+    p.dstPtr = to_internal ? ip : dp;
+    p.extent = make_cudaExtent((size_t)nx * 4, (size_t)ny, (size_t)nz);
+    p.kind = cudaMemcpyDefault;
+    return cudaMemcpy3DAsync(&p, st);
 }
 
 }  // namespace
@@ -357,13 +426,19 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     s->z0 = z0;
     s->z1 = z1;
     s->nzl = z1 - z0;
-    s->P = dims->nx * dims->ny;
+    s->pitch = (dims->nx + 3) / 4 * 4;
+    s->P = s->pitch * dims->ny;
     s->gc = gc;
     s->cfg = *cfg;
     s->s_kind = S->kind;
     if (!iter_kernel_lookup(gc.NI, gc.NL, &s->kinfo)) {
         delete s;
         return fail(PF_ERR_UNSUPPORTED, "no compiled kernel for %d internal / %d end nodes", gc.NI, gc.NL);
+    }
+    {
+        const char *env = getenv("PF_ITER_KERNEL");
+        const bool want_global = env && strcmp(env, "global") == 0;
+        s->staged = !want_global && staged_kernel_lookup(gc.NI, gc.NL, &s->sinfo) && encode_fn() != nullptr;
     }
     cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -401,24 +476,27 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     if ((st = alloc(s, (void **)&s->d_flag, 64, "flag")) != PF_OK) return bail(st);
     if ((st = alloc(s, (void **)&s->d_energy, (size_t)(2 * kEnergyBlocks + 2) * sizeof(double), "energy")) != PF_OK)
         return bail(st);
-    // inputs -> internal layouts (boundary [z][y][x] per label -> [z][l][y][x])
+    // inputs -> internal layouts (boundary [z][y][x] per label -> [z][l][y][pitch])
+    e = cudaMemsetAsync(s->D_alloc, 0, (size_t)((nzl + 1) * NL * P) * sizeof(float), s->stream);
+    if (e != cudaSuccess) { cuda_fail(s, e, "zero D"); return bail(PF_ERR_CUDA); }
     for (int l = 0; l < NL; ++l) {
-        e = copy_planes(s->D_alloc + l * P, NL * P, D[l], P, P, nzD, s->stream);
+        e = copy_volume(true, s->D_alloc + l * P, NL, (float *)D[l], s->nx, s->ny, s->pitch, nzD, s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "upload D"); return bail(PF_ERR_CUDA); }
     }
-    if (nzD < nzl + 1) {
-        e = cudaMemsetAsync(s->D_alloc + nzD * NL * P, 0, (size_t)((nzl + 1 - nzD) * NL * P) * sizeof(float), s->stream);
-        if (e != cudaSuccess) { cuda_fail(s, e, "zero D halo"); return bail(PF_ERR_CUDA); }
+    if (nS > 0) {
+        e = cudaMemsetAsync(s->S_alloc, 0, (size_t)(nzl * nS * P) * sizeof(float), s->stream);
+        if (e != cudaSuccess) { cuda_fail(s, e, "zero S"); return bail(PF_ERR_CUDA); }
     }
     if (S->kind == PF_S_SHARED_FIELD) {
         if (!S->fields[0]) return bail(fail(PF_ERR_INVALID, "smoothness: fields[0] is NULL"));
-        e = copy_planes(s->S_alloc, P, S->fields[0], P, P, nzl, s->stream);
+        e = copy_volume(true, s->S_alloc, 1, (float *)S->fields[0], s->nx, s->ny, s->pitch, nzl, s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
     } else if (S->kind == PF_S_FIELD_PER_NODE) {
         for (int p = 0; p < NV; ++p) {
             const int v = gc.node_of_pos[p];
             if (!S->fields[v - 1]) return bail(fail(PF_ERR_INVALID, "smoothness: fields[%d] is NULL", v - 1));
-            e = copy_planes(s->S_alloc + p * P, NV * P, S->fields[v - 1], P, P, nzl, s->stream);
+            e = copy_volume(true, s->S_alloc + p * P, NV, (float *)S->fields[v - 1], s->nx, s->ny, s->pitch, nzl,
+                            s->stream);
             if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
         }
     } else {
@@ -436,12 +514,31 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     }
     if ((st = init_state(s)) != PF_OK) return bail(st);
     // kernel configuration
-    e = cudaFuncSetAttribute(s->kinfo.func, cudaFuncAttributeMaxDynamicSharedMemorySize, s->kinfo.smem_bytes);
-    if (e != cudaSuccess) { cuda_fail(s, e, "cudaFuncSetAttribute"); return bail(PF_ERR_CUDA); }
-    cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, s->kinfo.func) == cudaSuccess) s->regs = fa.numRegs;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->ctas_per_sm, s->kinfo.func, s->kinfo.threads,
-                                                  s->kinfo.smem_bytes);
+    {
+        const void *fn = s->staged ? s->sinfo.func : s->kinfo.func;
+        const int thr = s->staged ? s->sinfo.threads : s->kinfo.threads;
+        const int smb = s->staged ? s->sinfo.smem_bytes : s->kinfo.smem_bytes;
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);
+        if (e != cudaSuccess) { cuda_fail(s, e, "cudaFuncSetAttribute"); return bail(PF_ERR_CUDA); }
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) s->regs = fa.numRegs;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->ctas_per_sm, fn, thr, smb);
+    }
+    if (s->staged) {
+        const int ty = s->sinfo.tile_y;
+        s->s_ch = S->kind == PF_S_SHARED_FIELD ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? NV : 0);
+        bool ok = true;
+        for (int i = 0; i < 2; ++i) {
+            ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)s->ndim * NV, nzl + 2, 40,
+                                ty + 2, s->ndim * NV);
+            ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, NL);
+        }
+        ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
+        if (s->s_ch) ok = ok && encode4d(&s->tm_S, s->S_alloc, s->nx, s->ny, s->pitch, s->s_ch, nzl, 32, ty, s->s_ch);
+        else memset(&s->tm_S, 0, sizeof(s->tm_S));
+        if (!ok) return bail(fail(PF_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
+        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * s->ndim * NV + 2 * 36 * (ty + 1) * NL + 32 * ty * s->s_ch));
+    }
     choose_chunking(s);
     e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) { cuda_fail(s, e, "create"); return bail(PF_ERR_CUDA); }
@@ -480,6 +577,7 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     a.S = s->S_alloc;
     a.nx = (int)s->nx;
     a.ny = (int)s->ny;
+    a.pitch = (int)s->pitch;
     a.nzl = (int)s->nzl;
     a.zg0 = (int)s->z0;
     a.nzg = (int)s->nz;
@@ -493,6 +591,32 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     a.resid_bits = s->d_resid;
     a.err_voxel = s->d_err;
     a.g = s->gc.g;
+    StagedArgs sa;
+    if (s->staged) {
+        memset(&sa, 0, sizeof(sa));
+        sa.tm_D = s->tm_D;
+        sa.tm_S = s->tm_S;
+        sa.nx = a.nx;
+        sa.ny = a.ny;
+        sa.pitch = a.pitch;
+        sa.nzl = a.nzl;
+        sa.zg0 = a.zg0;
+        sa.nzg = a.nzg;
+        sa.zchunk = s->zchunk;
+        sa.tiles_x = s->tiles_x;
+        sa.tiles = s->tiles;
+        sa.items = s->items;
+        sa.ndim = s->ndim;
+        sa.s_ch = s->s_ch;
+        sa.cap = a.cap;
+        sa.shift = a.shift;
+        sa.tx_bytes = s->tx_bytes;
+        sa.inv_c = a.inv_c;
+        sa.ctau = a.ctau;
+        sa.resid_bits = s->d_resid;
+        sa.err_voxel = s->d_err;
+        sa.g = s->gc.g;
+    }
     bool any_check = false;
     for (int t = 0; t < n; ++t) {
         const int64_t it = s->iters + 1;
@@ -501,13 +625,25 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
             CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
             any_check = true;
         }
-        a.u_in = s->u[s->cur];
-        a.q_in = s->q[s->cur];
-        a.u_out = s->u[1 - s->cur];
-        a.q_out = s->q[1 - s->cur];
-        void *args[] = {(void *)&a};
-        CK(cudaLaunchKernel(s->kinfo.func, s->grid, dim3(s->kinfo.threads), args, s->kinfo.smem_bytes, s->stream),
-           "launch pf_iter_kernel");
+        if (s->staged) {
+            sa.tm_q = s->tm_q[s->cur];
+            sa.tm_u = s->tm_u[s->cur];
+            sa.q_in = s->q[s->cur];
+            sa.u_out = s->u[1 - s->cur];
+            sa.q_out = s->q[1 - s->cur];
+            sa.check = a.check;
+            void *args[] = {(void *)&sa};
+            CK(cudaLaunchKernel(s->sinfo.func, s->grid, dim3(s->sinfo.threads), args, s->sinfo.smem_bytes, s->stream),
+               "launch pf_iter_staged");
+        } else {
+            a.u_in = s->u[s->cur];
+            a.q_in = s->q[s->cur];
+            a.u_out = s->u[1 - s->cur];
+            a.q_out = s->q[1 - s->cur];
+            void *args[] = {(void *)&a};
+            CK(cudaLaunchKernel(s->kinfo.func, s->grid, dim3(s->kinfo.threads), args, s->kinfo.smem_bytes, s->stream),
+               "launch pf_iter_kernel");
+        }
         s->launches++;
         s->cur = 1 - s->cur;
         s->iters = it;
@@ -534,18 +670,20 @@ pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {
     DeviceGuard dg(s->device);
     const int NL = s->gc.NL;
     const int64_t P = s->P, nzl = s->nzl;
+    const int64_t V = s->nx * s->ny * nzl;
     if (u) {
         for (int l = 0; l < NL; ++l)
-            CK(copy_planes(u + l * nzl * P, P, s->u[s->cur] + l * P, NL * P, P, nzl, s->stream), "download u");
+            CK(copy_volume(false, s->u[s->cur] + l * P, NL, u + l * V, s->nx, s->ny, s->pitch, nzl, s->stream),
+               "download u");
     }
     if (argmax) {
         const bool dev = is_device_ptr(argmax);
         uint8_t *dst = argmax;
-        if (!dev) CK(cudaMalloc((void **)&dst, (size_t)(nzl * P)), "argmax scratch");
-        CK(launch_argmax(s->u[s->cur], dst, NL, P, nzl, s->stream), "argmax kernel");
+        if (!dev) CK(cudaMalloc((void **)&dst, (size_t)V), "argmax scratch");
+        CK(launch_argmax(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, s->stream), "argmax kernel");
         s->launches++;
         if (!dev) {
-            CK(cudaMemcpyAsync(argmax, dst, (size_t)(nzl * P), cudaMemcpyDeviceToHost, s->stream), "download argmax");
+            CK(cudaMemcpyAsync(argmax, dst, (size_t)V, cudaMemcpyDeviceToHost, s->stream), "download argmax");
             CK(cudaStreamSynchronize(s->stream), "sync");
             cudaFree(dst);
         }
@@ -560,11 +698,13 @@ pf_status pf_get_flows(pf_solver *s, float *q) {
     DeviceGuard dg(s->device);
     const int NV = s->gc.NV, nd = s->ndim;
     const int64_t P = s->P, nzl = s->nzl;
+    const int64_t V = s->nx * s->ny * nzl;
     for (int p = 0; p < NV; ++p) {
         const int v = s->gc.node_of_pos[p];
         for (int k = 0; k < nd; ++k) {
-            float *dst = q + ((int64_t)(v - 1) * nd + k) * nzl * P;
-            CK(copy_planes(dst, P, s->q[s->cur] + ((int64_t)k * NV + p) * P, (int64_t)nd * NV * P, P, nzl, s->stream),
+            float *dst = q + ((int64_t)(v - 1) * nd + k) * V;
+            CK(copy_volume(false, s->q[s->cur] + ((int64_t)k * NV + p) * P, (int64_t)nd * NV, dst, s->nx, s->ny, s->pitch,
+                           nzl, s->stream),
                "download q");
         }
     }
@@ -583,6 +723,7 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
     a.S = s->S_alloc;
     a.nx = (int)s->nx;
     a.ny = (int)s->ny;
+    a.pitch = (int)s->pitch;
     a.nzl = (int)s->nzl;
     a.zg0 = (int)s->z0;
     a.nzg = (int)s->nz;
@@ -694,16 +835,18 @@ pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n) {
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     if (!s || !info) return fail(PF_ERR_INVALID, "NULL argument");
     info->tile_x = kTX;
-    info->tile_y = s->kinfo.tile_y;
+    info->tile_y = s->staged ? s->sinfo.tile_y : s->kinfo.tile_y;
     info->z_chunk = s->zchunk;
-    info->threads_per_cta = s->kinfo.threads;
+    info->threads_per_cta = s->staged ? s->sinfo.threads : s->kinfo.threads;
     info->ctas = (int)(s->grid.x * s->grid.y * s->grid.z);
     info->regs_per_thread = s->regs;
-    info->smem_bytes = s->kinfo.smem_bytes;
+    info->smem_bytes = s->staged ? s->sinfo.smem_bytes : s->kinfo.smem_bytes;
+    info->staged = s->staged ? 1 : 0;
+    info->work_items = s->staged ? s->items : info->ctas;
     info->ctas_per_sm = s->ctas_per_sm;
     // algorithmic bytes per iteration: per end label u r/w + D r + q r/w,
     // per internal node q r/w, plus the capacity fields
-    const int64_t V = s->P * s->nzl;
+    const int64_t V = s->nx * s->ny * s->nzl;
     const int64_t per_leaf = 4 + 4 + 4 + 8 * s->ndim, per_int = 8 * s->ndim;
     int64_t b = V * (per_leaf * s->gc.NL + per_int * s->gc.NI);
     if (s->s_kind == PF_S_SHARED_FIELD) b += 4 * V;

@@ -13,12 +13,14 @@ __global__ void fill_kernel(float *p, int64_t n, float v) {
 }
 
 // argmax over end labels, lowest label id wins ties ("thresholded").
-__global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__ out, int NL, int64_t P,
-                              int64_t nz) {
-    const int64_t V = P * nz;
+__global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__ out, int NL, int nx, int ny,
+                              int pitch, int64_t nz) {
+    const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i / P, pix = i - z * P;
-        const float *b = u + z * NL * P + pix;
+        const int64_t z = i / ((int64_t)nx * ny);
+        const int r = (int)(i - z * (int64_t)nx * ny);
+        const int y = r / nx, x = r - y * nx;
+        const float *b = u + z * NL * P + (int64_t)y * pitch + x;
         float best = b[0];
         int arg = 0;
         for (int l = 1; l < NL; ++l) {
@@ -59,14 +61,16 @@ __device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, 
 }
 
 __global__ void energy_kernel(const EnergyArgs a, double *partial) {
-    const int64_t P = (int64_t)a.nx * a.ny;
-    const int64_t V = P * a.nzl;
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int64_t V = (int64_t)a.nx * a.ny * a.nzl;
     const int NV = a.NV, NI = a.NI, NL = a.NL;
     const int64_t ups = (int64_t)NL * P, qps = (int64_t)a.ndim * NV * P;
     double e_acc = 0.0, f_acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i / P, pix = i - z * P;
-        const int x = (int)(pix % a.nx), y = (int)(pix / a.nx);
+        const int64_t z = i / ((int64_t)a.nx * a.ny);
+        const int r = (int)(i - z * (int64_t)a.nx * a.ny);
+        const int y = r / a.nx, x = r - y * a.nx;
+        const int64_t pix = (int64_t)y * a.pitch + x;
         const int64_t zg = a.zg0 + z;
         // ---- primal: sum_L D_L u_L + sum_v S_v |nabla u_v|
         float uc[kMaxNodes], un[kMaxNodes];
@@ -79,7 +83,7 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
             for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
         }
         if (y < a.ny - 1) {
-            labels_at(a, a.u + z * ups + pix + a.nx, P, un);
+            labels_at(a, a.u + z * ups + pix + a.pitch, P, un);
             for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
         }
         if (a.ndim == 3 && zg < a.nzg - 1) {
@@ -98,7 +102,7 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
         const float *qb = a.q + z * qps + pix;
         for (int v = 0; v < NV; ++v) {
             double dv = (double)qb[v * P] - (x > 0 ? (double)qb[v * P - 1] : 0.0);
-            dv += (double)qb[(NV + v) * P] - (y > 0 ? (double)qb[(NV + v) * P - a.nx] : 0.0);
+            dv += (double)qb[(NV + v) * P] - (y > 0 ? (double)qb[(NV + v) * P - a.pitch] : 0.0);
             if (a.ndim == 3)
                 dv += (double)qb[(2 * NV + v) * P] - (zg > 0 ? (double)qb[(2 * NV + v) * P - qps] : 0.0);
             d[v] = dv;
@@ -135,8 +139,9 @@ cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int64_t P, int64_t nz, cudaStream_t st) {
-    argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, P, nz);
+cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz,
+                          cudaStream_t st) {
+    argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz);
     return cudaGetLastError();
 }
 

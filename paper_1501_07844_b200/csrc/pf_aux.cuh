@@ -12,7 +12,7 @@ struct EnergyArgs {
     const float *q;   // current q, plane 0 (the plane below must be current for the dual)
     const float *D;
     const float *S;
-    int nx, ny, nzl, zg0, nzg, ndim;
+    int nx, ny, pitch, nzl, zg0, nzg, ndim;
     int NI, NL, NV;
     int s_kind, cap;
     GraphConst g;
@@ -21,7 +21,8 @@ struct EnergyArgs {
 constexpr int kEnergyBlocks = 592;
 
 cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st);
-cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int64_t P, int64_t nz, cudaStream_t st);
+cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz,
+                          cudaStream_t st);
 cudaError_t launch_check_nonneg(const float *p, int64_t n, unsigned int *flag, cudaStream_t st);
 cudaError_t launch_energy(const EnergyArgs &a, double *partial, int nblocks, double *out, cudaStream_t st);
 

@@ -49,6 +49,7 @@ struct IterArgs {
     const float *D;
     const float *S;   // null when capacities are scalars
     int nx, ny, nzl;  // local extents
+    int pitch;        // row pitch in elements (>= nx, multiple of 4 for TMA)
     int zg0, nzg;     // global z of local plane 0, global nz
     int zchunk;
     int ndim;
@@ -64,6 +65,31 @@ struct IterArgs {
 };
 
 __device__ __forceinline__ float ldg(const float *p) { return __ldg(p); }
+
+// Proj_{|q| <= S} (readings R5, R14).  l2: if |q| > S then q*S/|q| else q.  When the
+// fp32 sum of squares is tiny its terms may have under-flowed, so the norm is taken in fp64 there.
+__device__ __forceinline__ void project(int cap, float sv, float &hx, float &hy, float &hz) {
+    if (cap == 0) {
+        const float n2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+        if (n2 >= 1e-30f) {
+            const float n = sqrtf(n2);
+            if (n > sv) {
+                const float f = sv / n;
+                hx *= f; hy *= f; hz *= f;
+            }
+        } else {
+            const double n = sqrt((double)hx * hx + (double)hy * hy + (double)hz * hz);
+            if (n > (double)sv) {
+                const double f = (double)sv / n;
+                hx = (float)(hx * f); hy = (float)(hy * f); hz = (float)(hz * f);
+            }
+        }
+    } else {
+        hx = fminf(fmaxf(hx, -sv), sv);
+        hy = fminf(fmaxf(hy, -sv), sv);
+        hz = fminf(fmaxf(hz, -sv), sv);
+    }
+}
 
 template <int NI, int NL, int TY>
 struct IterSmem {
@@ -93,8 +119,8 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
     }
     const int x = blockIdx.x * kTX + lx, y = blockIdx.y * TY + ly;
     const bool active = (lx >= 0) && (x < a.nx) && (y < a.ny);
-    const int64_t P = (int64_t)a.nx * a.ny;
-    const int pix = active ? y * a.nx + x : 0;
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int pix = active ? y * a.pitch + x : 0;
     const int zc0 = blockIdx.z * a.zchunk;
     const int zc1 = min(zc0 + a.zchunk, a.nzl);
     const bool has_above = (a.zg0 + zc1) < a.nzg;
@@ -125,7 +151,7 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
                 const float qx = ldg(qb + v * P);
                 const float qxm = (x > 0) ? ldg(qb + v * P - 1) : 0.f;
                 const float qy = ldg(qb + (NV + v) * P);
-                const float qym = (y > 0) ? ldg(qb + (NV + v) * P - a.nx) : 0.f;
+                const float qym = (y > 0) ? ldg(qb + (NV + v) * P - a.pitch) : 0.f;
                 float dv = (qx - qxm) + (qy - qym);
                 if (is3) {
                     const float qz = ldg(qb + (2 * NV + v) * P);
@@ -159,8 +185,7 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
             }
             if (is_main && p < zc1) {
                 if (!(sum > 0.f) || !(sum <= 3.402823466e38f)) {
-                    const unsigned long long vox =
-                        (unsigned long long)(a.zg0 + p) * (unsigned long long)P + (unsigned long long)pix;
+                    const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                     atomicMin(a.err_voxel, vox);
                 }
                 const float inv = 1.f / sum;
@@ -208,17 +233,7 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
                 if (a.s_kind == 0) sv = a.g.s[v];
                 else if (a.s_kind == 1) sv = ldg(a.S + (int64_t)z * P + pix);
                 else sv = ldg(a.S + ((int64_t)z * NV + v) * P + pix);
-                if (a.cap == 0) {
-                    const float n = sqrtf(fmaf(hx, hx, fmaf(hy, hy, hz * hz)));
-                    if (n > sv) {
-                        const float f = sv / n;
-                        hx *= f; hy *= f; hz *= f;
-                    }
-                } else {
-                    hx = fminf(fmaxf(hx, -sv), sv);
-                    hy = fminf(fmaxf(hy, -sv), sv);
-                    hz = fminf(fmaxf(hz, -sv), sv);
-                }
+                project(a.cap, sv, hx, hy, hz);
                 qo[v * P] = hx;
                 qo[(NV + v) * P] = hy;
                 if (is3) qo[(2 * NV + v) * P] = hz;
@@ -244,17 +259,7 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
             if (a.s_kind == 0) sv = a.g.s[v];
             else if (a.s_kind == 1) sv = ldg(a.S + (int64_t)z * P + pix);
             else sv = ldg(a.S + ((int64_t)z * NV + v) * P + pix);
-            if (a.cap == 0) {
-                const float n = sqrtf(fmaf(hx, hx, fmaf(hy, hy, hz * hz)));
-                if (n > sv) {
-                    const float f = sv / n;
-                    hx *= f; hy *= f; hz *= f;
-                }
-            } else {
-                hx = fminf(fmaxf(hx, -sv), sv);
-                hy = fminf(fmaxf(hy, -sv), sv);
-                hz = fminf(fmaxf(hz, -sv), sv);
-            }
+            project(a.cap, sv, hx, hy, hz);
             qo[v * P] = hx;
             qo[(NV + v) * P] = hy;
             if (is3) qo[(2 * NV + v) * P] = hz;

@@ -1,0 +1,295 @@
+// pf_staged.cuh -- TMA-staged, persistent version of the fused pseudo-flow iteration (sm_100a).
+//
+// Same arithmetic and same per-voxel order as pf_iter_kernel (see pf_kernels.cuh for the
+// step-by-step mapping to Alg. 1 / Alg. 2), different data movement:
+//   * persistent CTAs (one per SM) walk work items = (32 x TY tile, z-chunk) in a static
+//     round-robin order, so the tiles in flight at any time are spatial neighbours and their
+//     shared halo lines are served from L2;
+//   * every z-plane of the tile is fetched by ONE thread as 3-4 TMA box loads
+//     (cp.async.bulk.tensor.4d) into a 2-deep shared-memory ring guarded by mbarriers: q over
+//     x in [x0-4, x0+36) x y in [y0-1, y0+TY] (the -x/-y neighbours for div and the +1 halo
+//     points), u and D over [x0, x0+36) x [y0, y0+TY], S over the tile.  Out-of-range box
+//     elements are zero-filled by the TMA unit, which is exactly q^k(-1) = 0 (reading R4);
+//   * plane p+2 is in flight while plane p is computed; q(p) and S(p) of the own voxel are kept
+//     in registers until the flow step of plane p runs one plane later.
+#pragma once
+#include <cuda.h>
+
+#include "pf_kernels.cuh"
+#include "pf_tma.cuh"
+
+namespace pf {
+
+struct StagedArgs {
+    CUtensorMap tm_q;   // input q, 4-D (x, y, channel = k*NV+v, plane+1)
+    CUtensorMap tm_u;   // input u, 4-D (x, y, l, plane+1)
+    CUtensorMap tm_D;   // D, 4-D (x, y, l, plane)
+    CUtensorMap tm_S;   // S field, 4-D (x, y, channel, plane); unused when s_ch == 0
+    const float *q_in;  // plane 0 of input q (chunk-start q^z(zc0-1) read)
+    float *u_out;
+    float *q_out;
+    int nx, ny, pitch, nzl, zg0, nzg;
+    int zchunk, tiles_x, tiles, items;
+    int ndim;
+    int s_ch;     // 0: scalar capacities, 1: shared field, NV: field per node
+    int cap, shift, check;
+    unsigned int tx_bytes;
+    float inv_c, ctau;
+    unsigned int *resid_bits;
+    unsigned long long *err_voxel;
+    GraphConst g;
+};
+
+__host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
+
+template <int NI, int NL, int TY>
+struct StagedLayout {
+    static constexpr int NV = NI + NL;
+    static constexpr int QW = 40, UW = 36, SW = 32;
+    static constexpr int QROWS = TY + 2, UROWS = TY + 1;
+    static constexpr int QSZ = round32(3 * NV * QROWS * QW);  // floats per stage (ndim = 3 maximum)
+    static constexpr int USZ = round32(NL * UROWS * UW);
+    static constexpr int SSZ = round32(NV * TY * SW);         // per-node fields maximum
+    static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NV * RPS;
+    static constexpr int kFloats = 2 * QSZ + 4 * USZ + 2 * SSZ + round32(3 * RING);
+    static constexpr int kBytes = kFloats * 4 + 2 * 8;
+    static constexpr int kThreads = 32 * TY + 64;
+};
+
+template <int NI, int NL, int TY>
+__global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
+    using L = StagedLayout<NI, NL, TY>;
+    constexpr int NV = L::NV, QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
+    constexpr int QCS = QROWS * QW;   // q channel stride in smem
+    constexpr int UCS = UROWS * UW;
+    constexpr int RS = L::RS, RPS = L::RPS, RING = L::RING;
+    extern __shared__ __align__(128) float sm[];
+    float *Qs = sm;
+    float *Us = Qs + 2 * L::QSZ;
+    float *Ds = Us + 2 * L::USZ;
+    float *Ss = Ds + 2 * L::USZ;
+    float *R = Ss + 2 * L::SSZ;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L::kFloats);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool is_main = warp < TY;
+    int lx, ly;
+    if (is_main) { lx = lane; ly = warp; }
+    else if (warp == TY) { lx = lane; ly = TY; }
+    else { lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0; }
+    const bool is3 = a.ndim == 3;
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int64_t qps = (int64_t)a.ndim * NV * P;
+    const int64_t ups = (int64_t)NL * P;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+        prefetch_tmap(&a.tm_q);
+        prefetch_tmap(&a.tm_u);
+        prefetch_tmap(&a.tm_D);
+        if (a.s_ch) prefetch_tmap(&a.tm_S);
+    }
+    __syncthreads();
+
+    auto issue = [&](int plane, int stage, int x0, int y0) {
+        mbar_arrive_expect_tx(&bars[stage], a.tx_bytes);
+        tma_load_4d(Qs + stage * L::QSZ, &a.tm_q, &bars[stage], x0 - 4, y0 - 1, 0, plane + 1);
+        tma_load_4d(Us + stage * L::USZ, &a.tm_u, &bars[stage], x0, y0, 0, plane + 1);
+        tma_load_4d(Ds + stage * L::USZ, &a.tm_D, &bars[stage], x0, y0, 0, plane);
+        if (a.s_ch) tma_load_4d(Ss + stage * L::SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
+    };
+
+    float resid = 0.f;
+    int kbase = 0;   // planes consumed so far by this CTA (ring position / mbarrier parity)
+    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+        const int chunk = item / a.tiles, tile = item - chunk * a.tiles;
+        const int x0 = (tile % a.tiles_x) * 32, y0 = (tile / a.tiles_x) * TY;
+        const int zc0 = chunk * a.zchunk, zc1 = min(zc0 + a.zchunk, a.nzl);
+        const bool has_above = (a.zg0 + zc1) < a.nzg;
+        const int pend = has_above ? zc1 : zc1 - 1;
+        const int x = x0 + (lx < 0 ? 0 : lx), y = y0 + ly;
+        const bool valid = (lx >= 0) && x < a.nx && y < a.ny;
+        const int pix = valid ? y * a.pitch + x : 0;
+        const int qoff = (ly + 1) * QW + (lx < 0 ? 0 : lx) + 4;
+        const int uoff = ly * UW + (lx < 0 ? 0 : lx);
+        const int roff = ly * RS + (lx < 0 ? 0 : lx);
+
+        __syncthreads();  // previous item's readers of the ring / stage buffers are done
+        if (tid == 0) {
+            fence_proxy_async();
+            issue(zc0, kbase & 1, x0, y0);
+            if (zc0 + 1 <= pend) issue(zc0 + 1, (kbase + 1) & 1, x0, y0);
+        }
+        // q at the plane below the chunk (div of its first plane)
+        float qc[3][NV];
+        float svc[(NV > 0) ? NV : 1];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) { qc[0][v] = 0.f; qc[1][v] = 0.f; qc[2][v] = 0.f; svc[v] = 0.f; }
+        if (valid && is3 && (a.zg0 + zc0) > 0) {
+            const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + 2 * NV * P + pix;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) qc[2][v] = __ldg(qb + v * P);
+        }
+
+        for (int p = zc0; p <= pend; ++p) {
+            const int k = kbase + (p - zc0);
+            const int st = k & 1;
+            mbar_wait(&bars[st], (k >> 1) & 1);
+            const float *Qb = Qs + st * L::QSZ;
+            const float *Ub = Us + st * L::USZ;
+            const float *Db = Ds + st * L::USZ;
+            float *Rp = R + (p % 3) * RING;
+            float qn[3][NV];
+            float Mv[NV];
+            float svn[(NV > 0) ? NV : 1];
+            // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
+            if (lx >= 0) {
+                float d[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float qx = Qb[v * QCS + qoff];
+                    const float qxm = Qb[v * QCS + qoff - 1];
+                    const float qy = Qb[(NV + v) * QCS + qoff];
+                    const float qym = Qb[(NV + v) * QCS + qoff - QW];
+                    float dv = (qx - qxm) + (qy - qym);
+                    float qz = 0.f;
+                    if (is3) {
+                        qz = Qb[(2 * NV + v) * QCS + qoff];
+                        dv += qz - qc[2][v];
+                    }
+                    qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
+                    d[v] = dv;
+                }
+#pragma unroll
+                for (int l = 0; l < NL; ++l) d[NI + l] = Db[l * UCS + uoff] + d[NI + l];
+#pragma unroll
+                for (int i = 0; i < NI; ++i)
+#pragma unroll
+                    for (int j = i + 1; j < NV; ++j) d[j] = fmaf(a.g.w[i][j], d[i], d[j]);
+                float m = 0.f;
+                if (a.shift == 0) {
+                    m = d[NI];
+#pragma unroll
+                    for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
+                }
+                float ut[NL], uold[NL];
+                float sum = 0.f;
+#pragma unroll
+                for (int l = 0; l < NL; ++l) {
+                    uold[l] = Ub[l * UCS + uoff];
+                    ut[l] = uold[l] * expf((m - d[NI + l]) * a.inv_c);
+                    sum += ut[l];
+                }
+                if (is_main && valid && p < zc1) {
+                    if (!(sum > 0.f) || !(sum <= 3.402823466e38f)) {
+                        const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
+                        atomicMin(a.err_voxel, vox);
+                    }
+                    const float inv = 1.f / sum;
+                    float *uo = a.u_out + (int64_t)p * ups + pix;
+#pragma unroll
+                    for (int l = 0; l < NL; ++l) {
+                        const float nu = ut[l] * inv;
+                        uo[l * P] = nu;
+                        resid = fmaxf(resid, fabsf(nu - uold[l]));
+                    }
+                }
+#pragma unroll
+                for (int l = 0; l < NL; ++l) Mv[NI + l] = ut[l];
+#pragma unroll
+                for (int i = NI - 1; i >= 0; --i) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int j = i + 1; j < NV; ++j) acc = fmaf(a.g.w[i][j], Mv[j], acc);
+                    Mv[i] = acc;
+                }
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Rp[v * RPS + roff] = Mv[v];
+                if (is_main) {
+                    const float *Sb = Ss + st * L::SSZ + ly * SW + lx;
+                    if (a.s_ch == 0) {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) svn[v] = a.g.s[v];
+                    } else if (a.s_ch == 1) {
+                        const float sv = Sb[0];
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) svn[v] = sv;
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) svn[v] = Sb[v * TY * SW];
+                    }
+                }
+            }
+            __syncthreads();  // ring slot p complete; stage st fully consumed
+            if (tid == 0 && p + 2 <= pend) {
+                fence_proxy_async();
+                issue(p + 2, st, x0, y0);
+            }
+            // ---------------- stage B(p-1): flow step + projection of plane p-1
+            if (is_main && valid && p > zc0) {
+                const int z = p - 1;
+                const float *Rz = R + (z % 3) * RING;
+                const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = is3 && (a.zg0 + z < a.nzg - 1);
+                float *qo = a.q_out + (int64_t)z * qps + pix;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float mc = Rz[v * RPS + roff];
+                    const float gx = gxv ? Rz[v * RPS + roff + 1] - mc : 0.f;
+                    const float gy = gyv ? Rz[v * RPS + roff + RS] - mc : 0.f;
+                    const float gz = gzv ? Mv[v] - mc : 0.f;
+                    float hx = fmaf(-a.ctau, gx, qc[0][v]);
+                    float hy = fmaf(-a.ctau, gy, qc[1][v]);
+                    float hz = is3 ? fmaf(-a.ctau, gz, qc[2][v]) : 0.f;
+                    project(a.cap, svc[v], hx, hy, hz);
+                    qo[v * P] = hx;
+                    qo[(NV + v) * P] = hy;
+                    if (is3) qo[(2 * NV + v) * P] = hz;
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                qc[0][v] = qn[0][v]; qc[1][v] = qn[1][v]; qc[2][v] = qn[2][v];
+                svc[v] = svn[v];
+            }
+        }
+        // last plane of the volume: no plane above, nabla_z = 0
+        if (!has_above && is_main && valid) {
+            const int z = zc1 - 1;
+            const float *Rz = R + (z % 3) * RING;
+            const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1;
+            float *qo = a.q_out + (int64_t)z * qps + pix;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float mc = Rz[v * RPS + roff];
+                const float gx = gxv ? Rz[v * RPS + roff + 1] - mc : 0.f;
+                const float gy = gyv ? Rz[v * RPS + roff + RS] - mc : 0.f;
+                float hx = fmaf(-a.ctau, gx, qc[0][v]);
+                float hy = fmaf(-a.ctau, gy, qc[1][v]);
+                float hz = qc[2][v];
+                project(a.cap, svc[v], hx, hy, hz);
+                qo[v * P] = hx;
+                qo[(NV + v) * P] = hy;
+                if (is3) qo[(2 * NV + v) * P] = hz;
+            }
+        }
+        kbase += pend - zc0 + 1;
+    }
+    if (a.check) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) resid = fmaxf(resid, __shfl_xor_sync(0xffffffffu, resid, o));
+        if (lane == 0 && resid > 0.f) atomicMax(a.resid_bits, __float_as_uint(resid));
+    }
+}
+
+struct StagedKernelInfo {
+    const void *func;
+    int threads;
+    int smem_bytes;
+    int tile_y;
+};
+
+bool staged_kernel_lookup(int NI, int NL, StagedKernelInfo *info);
+
+}  // namespace pf

@@ -13,6 +13,13 @@ from helpers import compare, solver_from_inputs, with_field_per_node
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["staged", "global"], autouse=True)
+def kernel_variant(request, monkeypatch):
+    """Run every test against both iteration kernels (TMA-staged default, global-load variant)."""
+    monkeypatch.setenv("PF_ITER_KERNEL", request.param)
+    return request.param
+
+
 def _run_both(inp, n, shift=O.SHIFT_MIN, cap=None, **kw):
     s = solver_from_inputs(inp, shift=shift, cap=cap, **kw)
     s.iterate(n)
@@ -201,3 +208,18 @@ def test_graph_and_input_validation():
     with pytest.raises(pf.PFError) as ei:
         pf.Solver(base["dims"], 3, (4, [0, 0, 0], [1, 2, 3], [1, 1, 1]), D, s_scalars=[0, .1, .1, .1], c=0.0)
     assert ei.value.status == pf.PF_ERR_INVALID
+
+
+def test_staged_and_global_kernels_bitwise_equal(monkeypatch):
+    """The two data-movement variants perform the same arithmetic in the same order."""
+    for name, dims in (("C2", (70, 45, 33)), ("C4", (41, 38, 29)), ("C1", (64, 64, 1)), ("C5", (35, 21, 12))):
+        inp = P.generate(P.config(name).resized(*dims))
+        out = {}
+        for kv in ("staged", "global"):
+            monkeypatch.setenv("PF_ITER_KERNEL", kv)
+            s = solver_from_inputs(inp)
+            assert s.kernel_info()["staged"] == (1 if kv == "staged" else 0)
+            s.iterate(17)
+            out[kv] = (s.labeling()[0], s.flows())
+            s.close()
+        assert np.array_equal(out["staged"][0], out["global"][0]) and np.array_equal(out["staged"][1], out["global"][1])

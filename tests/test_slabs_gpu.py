@@ -11,6 +11,13 @@ from helpers import solver_from_inputs
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["staged", "global"], autouse=True)
+def kernel_variant(request, monkeypatch):
+    """Run every test against both iteration kernels (TMA-staged default, global-load variant)."""
+    monkeypatch.setenv("PF_ITER_KERNEL", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("name,dims,parts", [("C2", (48, 40, 36), 2), ("C2", (48, 40, 37), 3), ("C4", (40, 33, 29), 4),
                                              ("C3", (33, 30, 24), 8), ("C5", (36, 33, 20), 5)])
 def test_slabs_bitwise_equal_single_domain(name, dims, parts):

@@ -1,0 +1,53 @@
+"""Summarise an ncu --set full report (raw page) for the pseudo-flow kernel into profiles/.
+usage: python tools/ncu_summary.py gpurun_out/prof.ncu-rep out.json [algorithmic_bytes_per_launch] [workload] [tile_x tile_y zchunk]"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep, out = sys.argv[1], sys.argv[2]
+alg = float(sys.argv[3]) if len(sys.argv) > 3 else None
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units, data = rows[0], rows[1], rows[2:]
+want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "l1tex__t_sector_hit_rate.pct", "launch__occupancy_limit_registers", "launch__grid_size",
+        "launch__block_size", "smsp__inst_executed.sum", "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "lts__t_bytes.sum", "l1tex__t_bytes.sum", "smsp__average_warp_latency_issue_stalled_long_scoreboard",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+res = []
+for r in data:
+    d = {}
+    for w in want:
+        if w in hdr:
+            i = hdr.index(w)
+            d[w] = r[i] + (f" {units[i]}" if units[i] else "")
+    # stall reasons
+    for i, h in enumerate(hdr):
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("_not_issued"):
+            try:
+                if float(r[i]) > 0:
+                    d.setdefault("stalls", {})[h.replace("smsp__pcsamp_warps_issue_stalled_", "")] = float(r[i])
+            except ValueError:
+                pass
+    res.append(d)
+summary = {"report": rep, "kernels": res}
+if alg and res:
+    def num(s):
+        return float(s.split()[0].replace(",", ""))
+    k = res[-1]
+    rb = num(k["dram__bytes_read.sum"]) * (1e6 if "MB" in k["dram__bytes_read.sum"] else (1e9 if "GB" in k["dram__bytes_read.sum"] else 1))
+    wb = num(k["dram__bytes_write.sum"]) * (1e6 if "MB" in k["dram__bytes_write.sum"] else (1e9 if "GB" in k["dram__bytes_write.sum"] else 1))
+    summary["dram_bytes_per_launch"] = rb + wb
+    summary["algorithmic_bytes_per_launch"] = alg
+    summary["traffic_over_algorithmic"] = (rb + wb) / alg
+if len(sys.argv) > 5:
+    summary["workload"] = sys.argv[4]
+    summary["kernel_config"] = [int(v) for v in sys.argv[5:8]]
+json.dump(summary, open(out, "w"), indent=1)
+print(json.dumps(summary, indent=1)[:4000])
