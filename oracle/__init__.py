@@ -31,6 +31,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 SHIFT_MIN, SHIFT_NONE = 0, 1
+U_FLOOR = 2.0 ** -126   # reading R18: labels below the fp32 normal range are dead (0)
 CAP_L2, CAP_LINF = 0, 1
 
 
@@ -51,10 +52,10 @@ def _load():
         i64, i32, dp, ip = ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
         lib.oracle_potts.restype = i64
         lib.oracle_potts.argtypes = [i32, i64, i64, i64, i32, dp, dp, dp, dp, ctypes.c_double, ctypes.c_double,
-                                     i32, i32, i32]
+                                     i32, i32, i32, ctypes.c_double]
         lib.oracle_dag.restype = i64
         lib.oracle_dag.argtypes = [i32, i64, i64, i64, i32, i32, ip, ip, dp, dp, dp, dp, dp, ctypes.c_double,
-                                   ctypes.c_double, i32, i32, i32]
+                                   ctypes.c_double, i32, i32, i32, ctypes.c_double]
         lib.oracle_topo_order.restype = i32
         lib.oracle_topo_order.argtypes = [i32, i32, ip, ip, dp, ip]
         lib.oracle_grad.restype = i32
@@ -97,23 +98,25 @@ def init_state(num_leaves: int, num_flow_nodes: int, shape: Sequence[int], ndim:
 
 
 def potts_iterate(D: np.ndarray, S: np.ndarray, u: np.ndarray, q: np.ndarray, ndim: int, c: float, tau: float,
-                  niter: int, shift: int = SHIFT_MIN, cap: int = CAP_L2):
+                  niter: int, shift: int = SHIFT_MIN, cap: int = CAP_L2, u_floor: float = U_FLOOR):
     """Algorithm 1 in place.  D,S,u: [K][nz][ny][nx]; q: [K][ndim][nz][ny][nx] (fp64, C order)."""
     K, nz, ny, nx = D.shape
-    st = _load().oracle_potts(ndim, nx, ny, nz, K, _dp(D), _dp(S), _dp(u), _dp(q), c, tau, shift, cap, niter)
+    st = _load().oracle_potts(ndim, nx, ny, nz, K, _dp(D), _dp(S), _dp(u), _dp(q), c, tau, shift, cap, niter,
+                              u_floor)
     _status(st)
     return u, q
 
 
 def dag_iterate(num_nodes: int, parent, child, weight, D: np.ndarray, S: np.ndarray, u: np.ndarray, q: np.ndarray,
-                ndim: int, c: float, tau: float, niter: int, shift: int = SHIFT_MIN, cap: int = CAP_L2):
+                ndim: int, c: float, tau: float, niter: int, shift: int = SHIFT_MIN, cap: int = CAP_L2,
+                u_floor: float = U_FLOOR):
     """Algorithm 2 in place.  D,u: [NL][...]; S: [num_nodes][...] (row 0 unused); q: [num_nodes-1][ndim][...]."""
     NL, nz, ny, nx = D.shape
     par = np.ascontiguousarray(parent, dtype=np.int32)
     chi = np.ascontiguousarray(child, dtype=np.int32)
     w = np.ascontiguousarray(weight, dtype=np.float64)
     st = _load().oracle_dag(ndim, nx, ny, nz, num_nodes, len(par), _ip(par), _ip(chi), _dp(w), _dp(D), _dp(S),
-                            _dp(u), _dp(q), c, tau, shift, cap, niter)
+                            _dp(u), _dp(q), c, tau, shift, cap, niter, u_floor)
     _status(st)
     return u, q
 

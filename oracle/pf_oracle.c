@@ -20,6 +20,9 @@
  *   R5  |q| <= S: cap==0 Euclidean ball, cap==1 box (|q^k| <= S, dual of l1-TV).
  *   R14 Proj: if |q| > S then q*S/|q| else q (S = 0, q = 0 gives 0).
  *   R8  q starts at 0; u starts at 1/|L| -- set by the caller.
+ *   R18 u is stored in fp32 (BASELINE north_star): a normalised label value below the fp32
+ *       normal range (u_floor, 2^-126 by default; 0 disables) is set to 0 -- "the label has died"
+ *       is decided at the precision the labels are stored in.
  *
  * Layouts (the C-ABI boundary layout): every field is one volume of V = nx*ny*nz
  * values, x fastest.  u: [NL][V] (end labels in node-id order), q: [node][k][V]
@@ -119,7 +122,7 @@ static int check_dims(const odims *d) {
  * D: [K][V]; S: [K][V] (capacity of each label's flow); u: [K][V]; q: [K][ndim][V].
  */
 int64_t oracle_potts(int ndim, int64_t nx, int64_t ny, int64_t nz, int K, const double *D, const double *S,
-                     double *u, double *q, double c, double tau, int shift, int cap, int niter) {
+                     double *u, double *q, double c, double tau, int shift, int cap, int niter, double u_floor) {
     odims d = {ndim, nx, ny, nz};
     if (!check_dims(&d) || K < 2 || !(c > 0) || !(tau > 0)) return BAD_ARGS;
     const int64_t n = vol(&d);
@@ -154,7 +157,10 @@ int64_t oracle_potts(int ndim, int64_t nx, int64_t ny, int64_t nz, int K, const 
         /* line 150 */
         if (status == 0)
             for (int L = 0; L < K; ++L)
-                for (int64_t i = 0; i < n; ++i) u[(int64_t)L * n + i] = u[(int64_t)L * n + i] / a[i];
+                for (int64_t i = 0; i < n; ++i) {
+                    u[(int64_t)L * n + i] = u[(int64_t)L * n + i] / a[i];
+                    if (u[(int64_t)L * n + i] < u_floor) u[(int64_t)L * n + i] = 0.0; /* R18 */
+                }
     }
     free(arg); free(m); free(a); free(tmp);
     return status;
@@ -211,7 +217,7 @@ static int graph_setup(ograph *g, int nn, int ne, const int *par, const int *chi
  */
 int64_t oracle_dag(int ndim, int64_t nx, int64_t ny, int64_t nz, int nn, int ne, const int *par, const int *chi,
                    const double *w, const double *D, const double *S, double *u, double *q, double c, double tau,
-                   int shift, int cap, int niter) {
+                   int shift, int cap, int niter, double u_floor) {
     odims d = {ndim, nx, ny, nz};
     ograph g;
     if (!check_dims(&d) || !graph_setup(&g, nn, ne, par, chi, w) || g.nleaf < 2 || !(c > 0) || !(tau > 0))
@@ -266,7 +272,10 @@ int64_t oracle_dag(int ndim, int64_t nx, int64_t ny, int64_t nz, int nn, int ne,
         /* P:293  u_L <- u_L / a */
         for (int v = 1; v < nn; ++v)
             if (g.is_leaf[v])
-                for (int64_t i = 0; i < n; ++i) UOF(v)[i] = UOF(v)[i] / a[i];
+                for (int64_t i = 0; i < n; ++i) {
+                    UOF(v)[i] = UOF(v)[i] / a[i];
+                    if (UOF(v)[i] < u_floor) UOF(v)[i] = 0.0; /* R18 */
+                }
         /* P:295  forall L not in end labels: d_L <- 0 */
         for (int v = 0; v < nn; ++v)
             if (!g.is_leaf[v])

@@ -226,7 +226,8 @@ pf_status cuda_fail(pf_solver *s, cudaError_t e, const char *what) {
     } while (0)
 
 int64_t ups(const pf_solver *s) { return (int64_t)s->gc.NL * s->P; }
-int64_t qps(const pf_solver *s) { return (int64_t)s->ndim * s->gc.NV * s->P; }
+// q always carries 3 components internally (q^z == 0 for 2-D volumes), so the kernels need no ndim branch
+int64_t qps(const pf_solver *s) { return (int64_t)3 * s->gc.NV * s->P; }
 
 void free_all(pf_solver *s) {
     for (int i = 0; i < 2; ++i) {
@@ -460,10 +461,10 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     for (int i = 0; i < 2; ++i) {
         if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u")) != PF_OK)
             return bail(st);
-        if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * s->ndim * NV * P) * sizeof(float), "q")) != PF_OK)
+        if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * 3 * NV * P) * sizeof(float), "q")) != PF_OK)
             return bail(st);
         s->u[i] = s->u_alloc[i] + NL * P;
-        s->q[i] = s->q_alloc[i] + (int64_t)s->ndim * NV * P;
+        s->q[i] = s->q_alloc[i] + (int64_t)3 * NV * P;
     }
     const int64_t nzD = std::min(z1 + 1, dims->nz) - z0;  // owned + static halo plane above
     if ((st = alloc(s, (void **)&s->D_alloc, (size_t)((nzl + 1) * NL * P) * sizeof(float), "D")) != PF_OK)
@@ -529,15 +530,15 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         s->s_ch = S->kind == PF_S_SHARED_FIELD ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? NV : 0);
         bool ok = true;
         for (int i = 0; i < 2; ++i) {
-            ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)s->ndim * NV, nzl + 2, 40,
-                                ty + 2, s->ndim * NV);
+            ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NV, nzl + 2, 40,
+                                ty + 2, 3 * NV);
             ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, NL);
         }
         ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
         if (s->s_ch) ok = ok && encode4d(&s->tm_S, s->S_alloc, s->nx, s->ny, s->pitch, s->s_ch, nzl, 32, ty, s->s_ch);
         else memset(&s->tm_S, 0, sizeof(s->tm_S));
         if (!ok) return bail(fail(PF_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
-        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * s->ndim * NV + 2 * 36 * (ty + 1) * NL + 32 * ty * s->s_ch));
+        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * NV + 2 * 36 * (ty + 1) * NL + 32 * ty * s->s_ch));
     }
     choose_chunking(s);
     e = cudaStreamSynchronize(s->stream);
@@ -582,7 +583,6 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     a.zg0 = (int)s->z0;
     a.nzg = (int)s->nz;
     a.zchunk = s->zchunk;
-    a.ndim = s->ndim;
     a.s_kind = s->s_kind;
     a.cap = s->cfg.cap;
     a.shift = s->cfg.shift;
@@ -606,7 +606,6 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
         sa.tiles_x = s->tiles_x;
         sa.tiles = s->tiles;
         sa.items = s->items;
-        sa.ndim = s->ndim;
         sa.s_ch = s->s_ch;
         sa.cap = a.cap;
         sa.shift = a.shift;
@@ -703,7 +702,7 @@ pf_status pf_get_flows(pf_solver *s, float *q) {
         const int v = s->gc.node_of_pos[p];
         for (int k = 0; k < nd; ++k) {
             float *dst = q + ((int64_t)(v - 1) * nd + k) * V;
-            CK(copy_volume(false, s->q[s->cur] + ((int64_t)k * NV + p) * P, (int64_t)nd * NV, dst, s->nx, s->ny, s->pitch,
+            CK(copy_volume(false, s->q[s->cur] + ((int64_t)k * NV + p) * P, (int64_t)3 * NV, dst, s->nx, s->ny, s->pitch,
                            nzl, s->stream),
                "download q");
         }
@@ -727,7 +726,7 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
     a.nzl = (int)s->nzl;
     a.zg0 = (int)s->z0;
     a.nzg = (int)s->nz;
-    a.ndim = s->ndim;
+    a.ndim = 3;
     a.NI = s->gc.NI;
     a.NL = s->gc.NL;
     a.NV = s->gc.NV;

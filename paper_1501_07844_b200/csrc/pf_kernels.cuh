@@ -36,6 +36,10 @@ constexpr int kMaxNodes = 16;     // non-source nodes handled by the compiled ke
 constexpr int kMaxInternal = 4;   // internal (non-end) nodes
 constexpr int kTX = 32;
 
+}  // namespace pf
+#include "pf_math.cuh"
+namespace pf {
+
 struct GraphConst {
     float w[kMaxInternal][kMaxNodes];  // w[i][j]: weight of edge (position i -> position j); 0 = no edge; S excluded
     float s[kMaxNodes];                // capacity scalar per position (PF_S_SCALAR_PER_NODE)
@@ -52,7 +56,6 @@ struct IterArgs {
     int pitch;        // row pitch in elements (>= nx, multiple of 4 for TMA)
     int zg0, nzg;     // global z of local plane 0, global nz
     int zchunk;
-    int ndim;
     int s_kind;       // 0 scalar per node, 1 shared field, 2 field per node
     int cap;          // 0 l2, 1 box
     int shift;        // 0 min, 1 none
@@ -66,37 +69,34 @@ struct IterArgs {
 
 __device__ __forceinline__ float ldg(const float *p) { return __ldg(p); }
 
-// Proj_{|q| <= S} (readings R5, R14).  l2: if |q| > S then q*S/|q| else q.  When the
-// fp32 sum of squares is tiny its terms may have under-flowed, so the norm is taken in fp64 there.
-__device__ __forceinline__ void project(int cap, float sv, float &hx, float &hy, float &hz) {
-    if (cap == 0) {
-        const float n2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
-        if (n2 >= 1e-30f) {
-            const float n = sqrtf(n2);
-            if (n > sv) {
-                const float f = sv / n;
-                hx *= f; hy *= f; hz *= f;
-            }
-        } else {
-            const double n = sqrt((double)hx * hx + (double)hy * hy + (double)hz * hz);
-            if (n > (double)sv) {
-                const double f = (double)sv / n;
-                hx = (float)(hx * f); hy = (float)(hy * f); hz = (float)(hz * f);
-            }
-        }
-    } else {
-        hx = fminf(fmaxf(hx, -sv), sv);
-        hy = fminf(fmaxf(hy, -sv), sv);
-        hz = fminf(fmaxf(hz, -sv), sv);
-    }
-}
-
 template <int NI, int NL, int TY>
 struct IterSmem {
     static constexpr int NV = NI + NL;
     static constexpr int kPlane = NV * (TY + 1) * (kTX + 1);
     static constexpr int kBytes = 3 * kPlane * (int)sizeof(float);
 };
+
+template <int NI, int NL, int TY, int CAP>
+__device__ __forceinline__ void flow_out_global(const IterArgs &a, const float *Mz, const float *Mp, bool has_z,
+                                                int sme, int x, int y, int zg, int64_t P, const float *qb, float *qo,
+                                                const float *Sb) {
+    constexpr int NV = NI + NL;
+    constexpr int RS = kTX + 1, PS = (TY + 1) * RS;
+    const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const float mc = Mz[v * PS + sme];
+        const float gx = gxv ? Mz[v * PS + sme + 1] - mc : 0.f;
+        const float gy = gyv ? Mz[v * PS + sme + RS] - mc : 0.f;
+        const float gz = gzv ? Mp[v * PS + sme] - mc : 0.f;
+        float hx = ldg(qb + v * P), hy = ldg(qb + (NV + v) * P), hz = ldg(qb + (2 * NV + v) * P);
+        const float sv = a.s_kind == 0 ? a.g.s[v] : (a.s_kind == 1 ? ldg(Sb) : ldg(Sb + v * P));
+        flow_step<CAP>(a.ctau, gx, gy, gz, sv, hx, hy, hz);
+        st_stream(qo + v * P, hx);
+        st_stream(qo + (NV + v) * P, hy);
+        st_stream(qo + (2 * NV + v) * P, hz);
+    }
+}
 
 template <int NI, int NL, int TY>
 __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a) {
@@ -125,14 +125,14 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
     const int zc1 = min(zc0 + a.zchunk, a.nzl);
     const bool has_above = (a.zg0 + zc1) < a.nzg;
     const int64_t ups = (int64_t)NL * P;
-    const int64_t qps = (int64_t)a.ndim * NV * P;
-    const bool is3 = a.ndim == 3;
+    const int64_t qps = (int64_t)3 * NV * P;
     const int sme = ly * RS + (lx < 0 ? 0 : lx);
+    const float k2 = kLog2e * a.inv_c;
 
     float qzp[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) qzp[v] = 0.f;
-    if (active && is3 && (a.zg0 + zc0) > 0) {
+    if (active && (a.zg0 + zc0) > 0) {
         const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + 2 * NV * P + pix;
 #pragma unroll
         for (int v = 0; v < NV; ++v) qzp[v] = ldg(qb + v * P);
@@ -152,62 +152,35 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
                 const float qxm = (x > 0) ? ldg(qb + v * P - 1) : 0.f;
                 const float qy = ldg(qb + (NV + v) * P);
                 const float qym = (y > 0) ? ldg(qb + (NV + v) * P - a.pitch) : 0.f;
-                float dv = (qx - qxm) + (qy - qym);
-                if (is3) {
-                    const float qz = ldg(qb + (2 * NV + v) * P);
-                    dv += qz - qzp[v];
-                    qzp[v] = qz;
-                }
-                d[v] = dv;
+                const float qz = ldg(qb + (2 * NV + v) * P);
+                d[v] = ((qx - qxm) + (qy - qym)) + (qz - qzp[v]);
+                qzp[v] = qz;
             }
             const float *Db = a.D + (int64_t)p * ups + pix;
 #pragma unroll
             for (int l = 0; l < NL; ++l) d[NI + l] = ldg(Db + l * P) + d[NI + l];
-            // top-down pushes along O \ {S}
-#pragma unroll
-            for (int i = 0; i < NI; ++i)
-#pragma unroll
-                for (int j = i + 1; j < NV; ++j) d[j] = fmaf(a.g.w[i][j], d[i], d[j]);
-            float m = 0.f;
-            if (a.shift == 0) {
-                m = d[NI];
-#pragma unroll
-                for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
-            }
+            push_down<NI, NV>(d, a.g.w);
             const float *ub = a.u_in + (int64_t)p * ups + pix;
-            float ut[NL], uold[NL];
-            float sum = 0.f;
+            float uold[NL], ut[NL], un[NL];
 #pragma unroll
-            for (int l = 0; l < NL; ++l) {
-                uold[l] = ldg(ub + l * P);
-                ut[l] = uold[l] * expf((m - d[NI + l]) * a.inv_c);
-                sum += ut[l];
-            }
+            for (int l = 0; l < NL; ++l) uold[l] = ldg(ub + l * P);
+            const float sum = label_update<NI, NL>(d, uold, ut, un, a.shift, k2);
             if (is_main && p < zc1) {
-                if (!(sum > 0.f) || !(sum <= 3.402823466e38f)) {
+                if (!(sum > 0.f) || !(sum <= FLT_MAX)) {
                     const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                     atomicMin(a.err_voxel, vox);
                 }
-                const float inv = 1.f / sum;
                 float *uo = a.u_out + (int64_t)p * ups + pix;
 #pragma unroll
                 for (int l = 0; l < NL; ++l) {
-                    const float nu = ut[l] * inv;
-                    uo[l * P] = nu;
-                    resid = fmaxf(resid, fabsf(nu - uold[l]));
+                    st_stream(uo + l * P, un[l]);
+                    resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                 }
             }
-            // bottom-up masses along O^-1 \ {S}
             float M[NV];
 #pragma unroll
             for (int l = 0; l < NL; ++l) M[NI + l] = ut[l];
-#pragma unroll
-            for (int i = NI - 1; i >= 0; --i) {
-                float acc = 0.f;
-#pragma unroll
-                for (int j = i + 1; j < NV; ++j) acc = fmaf(a.g.w[i][j], M[j], acc);
-                M[i] = acc;
-            }
+            push_up<NI, NV>(M, a.g.w);
 #pragma unroll
             for (int v = 0; v < NV; ++v) Mp[v * PS + sme] = M[v];
         }
@@ -216,54 +189,22 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
         if (is_main && active && p > zc0) {
             const int z = p - 1;
             const float *Mz = Ms + (z % 3) * RING;
-            const int zg = a.zg0 + z;
-            const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = is3 && (zg < a.nzg - 1);
             const float *qb = a.q_in + (int64_t)z * qps + pix;
             float *qo = a.q_out + (int64_t)z * qps + pix;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const float mc = Mz[v * PS + sme];
-                const float gx = gxv ? Mz[v * PS + sme + 1] - mc : 0.f;
-                const float gy = gyv ? Mz[v * PS + sme + RS] - mc : 0.f;
-                const float gz = gzv ? Mp[v * PS + sme] - mc : 0.f;
-                float hx = fmaf(-a.ctau, gx, ldg(qb + v * P));
-                float hy = fmaf(-a.ctau, gy, ldg(qb + (NV + v) * P));
-                float hz = is3 ? fmaf(-a.ctau, gz, ldg(qb + (2 * NV + v) * P)) : 0.f;
-                float sv;
-                if (a.s_kind == 0) sv = a.g.s[v];
-                else if (a.s_kind == 1) sv = ldg(a.S + (int64_t)z * P + pix);
-                else sv = ldg(a.S + ((int64_t)z * NV + v) * P + pix);
-                project(a.cap, sv, hx, hy, hz);
-                qo[v * P] = hx;
-                qo[(NV + v) * P] = hy;
-                if (is3) qo[(2 * NV + v) * P] = hz;
-            }
+            const float *Sb = a.S ? a.S + (int64_t)z * (a.s_kind == 1 ? 1 : NV) * P + pix : nullptr;
+            if (a.cap == 0) flow_out_global<NI, NL, TY, 0>(a, Mz, Mp, true, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
+            else flow_out_global<NI, NL, TY, 1>(a, Mz, Mp, true, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
         }
     }
     // last plane of the volume: no plane above, nabla_z = 0
     if (!has_above && is_main && active) {
         const int z = zc1 - 1;
         const float *Mz = Ms + (z % 3) * RING;
-        const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1;
         const float *qb = a.q_in + (int64_t)z * qps + pix;
         float *qo = a.q_out + (int64_t)z * qps + pix;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const float mc = Mz[v * PS + sme];
-            const float gx = gxv ? Mz[v * PS + sme + 1] - mc : 0.f;
-            const float gy = gyv ? Mz[v * PS + sme + RS] - mc : 0.f;
-            float hx = fmaf(-a.ctau, gx, ldg(qb + v * P));
-            float hy = fmaf(-a.ctau, gy, ldg(qb + (NV + v) * P));
-            float hz = is3 ? ldg(qb + (2 * NV + v) * P) : 0.f;
-            float sv;
-            if (a.s_kind == 0) sv = a.g.s[v];
-            else if (a.s_kind == 1) sv = ldg(a.S + (int64_t)z * P + pix);
-            else sv = ldg(a.S + ((int64_t)z * NV + v) * P + pix);
-            project(a.cap, sv, hx, hy, hz);
-            qo[v * P] = hx;
-            qo[(NV + v) * P] = hy;
-            if (is3) qo[(2 * NV + v) * P] = hz;
-        }
+        const float *Sb = a.S ? a.S + (int64_t)z * (a.s_kind == 1 ? 1 : NV) * P + pix : nullptr;
+        if (a.cap == 0) flow_out_global<NI, NL, TY, 0>(a, Mz, Mz, false, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
+        else flow_out_global<NI, NL, TY, 1>(a, Mz, Mz, false, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
     }
     if (a.check) {
 #pragma unroll

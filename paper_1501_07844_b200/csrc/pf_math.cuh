@@ -1,0 +1,105 @@
+// pf_math.cuh -- the per-voxel arithmetic of one pseudo-flow iteration, shared by both data-movement
+// variants of the fused kernel (pf_kernels.cuh global-load, pf_staged.cuh TMA-staged) so that the two
+// are bitwise identical.  Paper references: PAPER.md P:144-153 (Alg. 1), P:279-305 (Alg. 2).
+#pragma once
+#include <cfloat>
+#include <cstdint>
+
+namespace pf {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// 2^x on the SFU (MUFU.EX2, max rel. error ~2^-22); subnormal results flush to 0, consistent with the
+// u floor below.
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Streaming (evict-first) store: the new state is not re-read in this launch, keep it out of L2's way.
+__device__ __forceinline__ void st_stream(float *p, float v) {
+    asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// Label update of one voxel (P:147-150 / P:290-293, Eq. 7 / Eq. 15; reading R1):
+//   m = min_L d_L (SHIFT_MIN) or 0;  u~_L = u_L exp(-(d_L - m)/c);  a = sum u~;  u'_L = u~_L / a,
+// with u' below the fp32 normal range flushed to 0 (reading R18: u is stored in fp32).
+// d[NI..NI+NL) holds the end-label excesses on entry; ut receives u~ (the unnormalised masses).
+// Returns a; writes u' to unew.
+template <int NI, int NL>
+__device__ __forceinline__ float label_update(const float (&d)[NI + NL], const float (&uold)[NL], float (&ut)[NL],
+                                              float (&unew)[NL], int shift, float k2 /* log2(e)/c */) {
+    float m = 0.f;
+    if (shift == 0) {
+        m = d[NI];
+#pragma unroll
+        for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        ut[l] = uold[l] * ex2_approx((m - d[NI + l]) * k2);
+        sum += ut[l];
+    }
+    const float inv = __frcp_rn(sum);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        const float nu = ut[l] * inv;
+        unew[l] = nu < FLT_MIN ? 0.f : nu;
+    }
+    return sum;
+}
+
+// Top-down excess pushes along O \ {S}: d_j += w_ij d_i for internal i (positions < NI).
+template <int NI, int NV>
+__device__ __forceinline__ void push_down(float (&d)[NV], const float (&w)[kMaxInternal][kMaxNodes]) {
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int j = i + 1; j < NV; ++j) d[j] = fmaf(w[i][j], d[i], d[j]);
+}
+
+// Bottom-up masses along O^-1 \ {S}: M_i = sum_j w_ij M_j for internal i.
+template <int NI, int NV>
+__device__ __forceinline__ void push_up(float (&M)[NV], const float (&w)[kMaxInternal][kMaxNodes]) {
+#pragma unroll
+    for (int i = NI - 1; i >= 0; --i) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = i + 1; j < NV; ++j) acc = fmaf(w[i][j], M[j], acc);
+        M[i] = acc;
+    }
+}
+
+// Flow step + capacity projection of one node at one voxel (P:148 / P:298; Eq. 8 / Eq. 16; R5, R14):
+//   q^ = q - c tau nabla M;  q' = q^ if |q^| <= S else q^ S/|q^|  (CAP 0, l2)  |  clamp(q^, -S, S) (CAP 1).
+template <int CAP>
+__device__ __forceinline__ void flow_step(float ctau, float gx, float gy, float gz, float sv, float &hx, float &hy,
+                                          float &hz) {
+    hx = fmaf(-ctau, gx, hx);
+    hy = fmaf(-ctau, gy, hy);
+    hz = fmaf(-ctau, gz, hz);
+    if (CAP == 0) {
+        const float n2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+        if (n2 >= 1e-30f) {
+            if (n2 > sv * sv) {
+                const float f = sv * rsqrtf(n2);
+                hx *= f; hy *= f; hz *= f;
+            }
+        } else if (fabsf(hx) + fabsf(hy) + fabsf(hz) > sv) {
+            // squares may have under-flowed: exact norm in fp64 (rare)
+            const double n = sqrt((double)hx * hx + (double)hy * hy + (double)hz * hz);
+            if (n > (double)sv) {
+                const double f = (double)sv / n;
+                hx = (float)(hx * f); hy = (float)(hy * f); hz = (float)(hz * f);
+            }
+        }
+    } else {
+        hx = fminf(fmaxf(hx, -sv), sv);
+        hy = fminf(fmaxf(hy, -sv), sv);
+        hz = fminf(fmaxf(hz, -sv), sv);
+    }
+}
+
+}  // namespace pf

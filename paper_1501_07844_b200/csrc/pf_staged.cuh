@@ -30,7 +30,6 @@ struct StagedArgs {
     float *q_out;
     int nx, ny, pitch, nzl, zg0, nzg;
     int zchunk, tiles_x, tiles, items;
-    int ndim;
     int s_ch;     // 0: scalar capacities, 1: shared field, NV: field per node
     int cap, shift, check;
     unsigned int tx_bytes;
@@ -56,6 +55,26 @@ struct StagedLayout {
     static constexpr int kThreads = 32 * TY + 64;
 };
 
+template <int NV, int CAP>
+__device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int roff, int rps, int rs,
+                                                const float (&Mn)[NV], bool has_z, int x, int y, int zg,
+                                                const float (&qc)[3][NV], const float (&svc)[NV], float *qo,
+                                                int64_t P) {
+    const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const float mc = Rz[v * rps + roff];
+        const float gx = gxv ? Rz[v * rps + roff + 1] - mc : 0.f;
+        const float gy = gyv ? Rz[v * rps + roff + rs] - mc : 0.f;
+        const float gz = gzv ? Mn[v] - mc : 0.f;
+        float hx = qc[0][v], hy = qc[1][v], hz = qc[2][v];
+        flow_step<CAP>(a.ctau, gx, gy, gz, svc[v], hx, hy, hz);
+        st_stream(qo + v * P, hx);
+        st_stream(qo + (NV + v) * P, hy);
+        st_stream(qo + (2 * NV + v) * P, hz);
+    }
+}
+
 template <int NI, int NL, int TY>
 __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY>;
@@ -77,10 +96,10 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
     if (is_main) { lx = lane; ly = warp; }
     else if (warp == TY) { lx = lane; ly = TY; }
     else { lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0; }
-    const bool is3 = a.ndim == 3;
     const int64_t P = (int64_t)a.pitch * a.ny;
-    const int64_t qps = (int64_t)a.ndim * NV * P;
+    const int64_t qps = (int64_t)3 * NV * P;
     const int64_t ups = (int64_t)NL * P;
+    const float k2 = kLog2e * a.inv_c;
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -122,12 +141,12 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             issue(zc0, kbase & 1, x0, y0);
             if (zc0 + 1 <= pend) issue(zc0 + 1, (kbase + 1) & 1, x0, y0);
         }
-        // q at the plane below the chunk (div of its first plane)
+        // q of the plane below the chunk (its z-component enters div of the first plane)
         float qc[3][NV];
-        float svc[(NV > 0) ? NV : 1];
+        float svc[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) { qc[0][v] = 0.f; qc[1][v] = 0.f; qc[2][v] = 0.f; svc[v] = 0.f; }
-        if (valid && is3 && (a.zg0 + zc0) > 0) {
+        if (valid && (a.zg0 + zc0) > 0) {
             const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + 2 * NV * P + pix;
 #pragma unroll
             for (int v = 0; v < NV; ++v) qc[2][v] = __ldg(qb + v * P);
@@ -143,7 +162,9 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             float *Rp = R + (p % 3) * RING;
             float qn[3][NV];
             float Mv[NV];
-            float svn[(NV > 0) ? NV : 1];
+            float svn[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) svn[v] = 0.f;
             // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
             if (lx >= 0) {
                 float d[NV];
@@ -153,58 +174,32 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
                     const float qxm = Qb[v * QCS + qoff - 1];
                     const float qy = Qb[(NV + v) * QCS + qoff];
                     const float qym = Qb[(NV + v) * QCS + qoff - QW];
-                    float dv = (qx - qxm) + (qy - qym);
-                    float qz = 0.f;
-                    if (is3) {
-                        qz = Qb[(2 * NV + v) * QCS + qoff];
-                        dv += qz - qc[2][v];
-                    }
+                    const float qz = Qb[(2 * NV + v) * QCS + qoff];
+                    d[v] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
                     qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
-                    d[v] = dv;
                 }
 #pragma unroll
                 for (int l = 0; l < NL; ++l) d[NI + l] = Db[l * UCS + uoff] + d[NI + l];
+                push_down<NI, NV>(d, a.g.w);
+                float uold[NL], ut[NL], un[NL];
 #pragma unroll
-                for (int i = 0; i < NI; ++i)
-#pragma unroll
-                    for (int j = i + 1; j < NV; ++j) d[j] = fmaf(a.g.w[i][j], d[i], d[j]);
-                float m = 0.f;
-                if (a.shift == 0) {
-                    m = d[NI];
-#pragma unroll
-                    for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
-                }
-                float ut[NL], uold[NL];
-                float sum = 0.f;
-#pragma unroll
-                for (int l = 0; l < NL; ++l) {
-                    uold[l] = Ub[l * UCS + uoff];
-                    ut[l] = uold[l] * expf((m - d[NI + l]) * a.inv_c);
-                    sum += ut[l];
-                }
+                for (int l = 0; l < NL; ++l) uold[l] = Ub[l * UCS + uoff];
+                const float sum = label_update<NI, NL>(d, uold, ut, un, a.shift, k2);
                 if (is_main && valid && p < zc1) {
-                    if (!(sum > 0.f) || !(sum <= 3.402823466e38f)) {
+                    if (!(sum > 0.f) || !(sum <= FLT_MAX)) {
                         const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                         atomicMin(a.err_voxel, vox);
                     }
-                    const float inv = 1.f / sum;
                     float *uo = a.u_out + (int64_t)p * ups + pix;
 #pragma unroll
                     for (int l = 0; l < NL; ++l) {
-                        const float nu = ut[l] * inv;
-                        uo[l * P] = nu;
-                        resid = fmaxf(resid, fabsf(nu - uold[l]));
+                        st_stream(uo + l * P, un[l]);
+                        resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                     }
                 }
 #pragma unroll
                 for (int l = 0; l < NL; ++l) Mv[NI + l] = ut[l];
-#pragma unroll
-                for (int i = NI - 1; i >= 0; --i) {
-                    float acc = 0.f;
-#pragma unroll
-                    for (int j = i + 1; j < NV; ++j) acc = fmaf(a.g.w[i][j], Mv[j], acc);
-                    Mv[i] = acc;
-                }
+                push_up<NI, NV>(Mv, a.g.w);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) Rp[v * RPS + roff] = Mv[v];
                 if (is_main) {
@@ -231,22 +226,11 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             if (is_main && valid && p > zc0) {
                 const int z = p - 1;
                 const float *Rz = R + (z % 3) * RING;
-                const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = is3 && (a.zg0 + z < a.nzg - 1);
                 float *qo = a.q_out + (int64_t)z * qps + pix;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const float mc = Rz[v * RPS + roff];
-                    const float gx = gxv ? Rz[v * RPS + roff + 1] - mc : 0.f;
-                    const float gy = gyv ? Rz[v * RPS + roff + RS] - mc : 0.f;
-                    const float gz = gzv ? Mv[v] - mc : 0.f;
-                    float hx = fmaf(-a.ctau, gx, qc[0][v]);
-                    float hy = fmaf(-a.ctau, gy, qc[1][v]);
-                    float hz = is3 ? fmaf(-a.ctau, gz, qc[2][v]) : 0.f;
-                    project(a.cap, svc[v], hx, hy, hz);
-                    qo[v * P] = hx;
-                    qo[(NV + v) * P] = hy;
-                    if (is3) qo[(2 * NV + v) * P] = hz;
-                }
+                if (a.cap == 0)
+                    flow_out_staged<NV, 0>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
+                else
+                    flow_out_staged<NV, 1>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
             }
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
@@ -258,21 +242,14 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
         if (!has_above && is_main && valid) {
             const int z = zc1 - 1;
             const float *Rz = R + (z % 3) * RING;
-            const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1;
             float *qo = a.q_out + (int64_t)z * qps + pix;
+            float Mdummy[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const float mc = Rz[v * RPS + roff];
-                const float gx = gxv ? Rz[v * RPS + roff + 1] - mc : 0.f;
-                const float gy = gyv ? Rz[v * RPS + roff + RS] - mc : 0.f;
-                float hx = fmaf(-a.ctau, gx, qc[0][v]);
-                float hy = fmaf(-a.ctau, gy, qc[1][v]);
-                float hz = qc[2][v];
-                project(a.cap, svc[v], hx, hy, hz);
-                qo[v * P] = hx;
-                qo[(NV + v) * P] = hy;
-                if (is3) qo[(2 * NV + v) * P] = hz;
-            }
+            for (int v = 0; v < NV; ++v) Mdummy[v] = 0.f;
+            if (a.cap == 0)
+                flow_out_staged<NV, 0>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo, P);
+            else
+                flow_out_staged<NV, 1>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo, P);
         }
         kbase += pend - zc0 + 1;
     }

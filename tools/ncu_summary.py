@@ -38,11 +38,13 @@ for r in data:
     res.append(d)
 summary = {"report": rep, "kernels": res}
 if alg and res:
-    def num(s):
-        return float(s.split()[0].replace(",", ""))
+    def nbytes(s):
+        v, u = s.split()[0].replace(",", ""), s.split()[1] if len(s.split()) > 1 else "byte"
+        mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
+        return float(v) * mul
     k = res[-1]
-    rb = num(k["dram__bytes_read.sum"]) * (1e6 if "MB" in k["dram__bytes_read.sum"] else (1e9 if "GB" in k["dram__bytes_read.sum"] else 1))
-    wb = num(k["dram__bytes_write.sum"]) * (1e6 if "MB" in k["dram__bytes_write.sum"] else (1e9 if "GB" in k["dram__bytes_write.sum"] else 1))
+    rb = nbytes(k["dram__bytes_read.sum"])
+    wb = nbytes(k["dram__bytes_write.sum"])
     summary["dram_bytes_per_launch"] = rb + wb
     summary["algorithmic_bytes_per_launch"] = alg
     summary["traffic_over_algorithmic"] = (rb + wb) / alg
