@@ -362,6 +362,12 @@ pf_status check_numeric(pf_solver *s) {
 cudaError_t copy_volume(bool to_internal, float *internal_c, int64_t nch, float *dense, int64_t nx, int64_t ny,
                         int64_t pitch, int64_t nz, cudaStream_t st) {
     if (nz <= 0) return cudaSuccess;
+    if (pitch == nx) {  // unpadded rows: one contiguous x-y plane per (z, channel) -> large 2-D copy
+        const size_t plane = (size_t)(nx * ny) * 4;
+        if (to_internal)
+            return cudaMemcpy2DAsync(internal_c, plane * nch, dense, plane, plane, (size_t)nz, cudaMemcpyDefault, st);
+        return cudaMemcpy2DAsync(dense, plane, internal_c, plane * nch, plane, (size_t)nz, cudaMemcpyDefault, st);
+    }
     cudaMemcpy3DParms p;
     memset(&p, 0, sizeof(p));
     cudaPitchedPtr ip = make_cudaPitchedPtr(internal_c, (size_t)pitch * 4, (size_t)nx, (size_t)(ny * nch));

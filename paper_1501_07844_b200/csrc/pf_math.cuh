@@ -81,18 +81,18 @@ __device__ __forceinline__ void flow_step(float ctau, float gx, float gy, float 
     hy = fmaf(-ctau, gy, hy);
     hz = fmaf(-ctau, gz, hz);
     if (CAP == 0) {
-        const float n2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
-        if (n2 >= 1e-30f) {
-            if (n2 > sv * sv) {
-                const float f = sv * rsqrtf(n2);
+        // Norm on a power-of-two rescaled copy (exact scaling), so tiny flows next to tiny capacities
+        // (S(x) down to 1e-38 in the configs' edge-weighted S) neither under-flow their squares nor
+        // need a slow path; for normal ranges the result is bitwise that of the unscaled formula.
+        const float m = fmaxf(fabsf(hx), fmaxf(fabsf(hy), fabsf(hz)));
+        if (m > 0.f) {
+            const float sc = __int_as_float(0x7f000000 - (__float_as_int(m) & 0x7f800000));  // ~1/m, 2^k
+            const float sx = hx * sc, sy = hy * sc, sz = hz * sc;
+            const float n2 = fmaf(sx, sx, fmaf(sy, sy, sz * sz));
+            const float ss = sv * sc;
+            if (n2 > ss * ss) {
+                const float f = ss * rsqrtf(n2);  // = S / |q^|
                 hx *= f; hy *= f; hz *= f;
-            }
-        } else if (fabsf(hx) + fabsf(hy) + fabsf(hz) > sv) {
-            // squares may have under-flowed: exact norm in fp64 (rare)
-            const double n = sqrt((double)hx * hx + (double)hy * hy + (double)hz * hz);
-            if (n > (double)sv) {
-                const double f = (double)sv / n;
-                hx = (float)(hx * f); hy = (float)(hy * f); hz = (float)(hz * f);
             }
         }
     } else {
