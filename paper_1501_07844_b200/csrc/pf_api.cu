@@ -395,8 +395,8 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     if ((dims->ndim != 2 && dims->ndim != 3) || dims->nx < 1 || dims->ny < 1 || dims->nz < 1 ||
         (dims->ndim == 2 && dims->nz != 1))
         return fail(PF_ERR_INVALID, "dims: ndim must be 2 or 3, extents >= 1, nz == 1 for ndim == 2");
-    if (dims->nx * dims->ny >= (int64_t)1 << 31)
-        return fail(PF_ERR_INVALID, "dims: an x-y plane must have < 2^31 voxels");
+    if (((dims->nx + 3) / 4 * 4) * dims->ny * 3 * kMaxNodes >= (int64_t)1 << 31)
+        return fail(PF_ERR_INVALID, "dims: an x-y plane must have < 2^31 / 48 voxels (32-bit channel offsets)");
     if (!(cfg->c > 0.f) || !(cfg->tau > 0.f) || !std::isfinite(cfg->c) || !std::isfinite(cfg->tau))
         return fail(PF_ERR_INVALID, "config: c and tau must be finite and > 0");
     if ((cfg->cap != PF_CAP_L2 && cfg->cap != PF_CAP_LINF) || (cfg->shift != PF_SHIFT_MIN && cfg->shift != PF_SHIFT_NONE) ||

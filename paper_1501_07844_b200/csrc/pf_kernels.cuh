@@ -83,6 +83,7 @@ __device__ __forceinline__ void flow_out_global(const IterArgs &a, const float *
     constexpr int NV = NI + NL;
     constexpr int RS = kTX + 1, PS = (TY + 1) * RS;
     const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
+    const int Pi = (int)P;  // channel stride fits 32 bits (an x-y plane has < 2^31 / 48 voxels)
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const float mc = Mz[v * PS + sme];
@@ -92,9 +93,9 @@ __device__ __forceinline__ void flow_out_global(const IterArgs &a, const float *
         float hx = ldg(qb + v * P), hy = ldg(qb + (NV + v) * P), hz = ldg(qb + (2 * NV + v) * P);
         const float sv = a.s_kind == 0 ? a.g.s[v] : (a.s_kind == 1 ? ldg(Sb) : ldg(Sb + v * P));
         flow_step<CAP>(a.ctau, gx, gy, gz, sv, hx, hy, hz);
-        st_stream(qo + v * P, hx);
-        st_stream(qo + (NV + v) * P, hy);
-        st_stream(qo + (2 * NV + v) * P, hz);
+        st_stream(qo + v * Pi, hx);
+        st_stream(qo + (NV + v) * Pi, hy);
+        st_stream(qo + (2 * NV + v) * Pi, hz);
     }
 }
 
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
                 float *uo = a.u_out + (int64_t)p * ups + pix;
 #pragma unroll
                 for (int l = 0; l < NL; ++l) {
-                    st_stream(uo + l * P, un[l]);
+                    st_stream(uo + l * (int)P, un[l]);
                     resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                 }
             }

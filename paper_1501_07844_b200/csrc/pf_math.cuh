@@ -84,17 +84,14 @@ __device__ __forceinline__ void flow_step(float ctau, float gx, float gy, float 
         // Norm on a power-of-two rescaled copy (exact scaling), so tiny flows next to tiny capacities
         // (S(x) down to 1e-38 in the configs' edge-weighted S) neither under-flow their squares nor
         // need a slow path; for normal ranges the result is bitwise that of the unscaled formula.
+        // (branch-free: m = 0 gives n2 = 0, which never exceeds ss^2, so f = 1 and q^ = 0 is kept)
         const float m = fmaxf(fabsf(hx), fmaxf(fabsf(hy), fabsf(hz)));
-        if (m > 0.f) {
-            const float sc = __int_as_float(0x7f000000 - (__float_as_int(m) & 0x7f800000));  // ~1/m, 2^k
-            const float sx = hx * sc, sy = hy * sc, sz = hz * sc;
-            const float n2 = fmaf(sx, sx, fmaf(sy, sy, sz * sz));
-            const float ss = sv * sc;
-            if (n2 > ss * ss) {
-                const float f = ss * rsqrtf(n2);  // = S / |q^|
-                hx *= f; hy *= f; hz *= f;
-            }
-        }
+        const float sc = __int_as_float(0x7f000000 - (__float_as_int(m) & 0x7f800000));  // ~1/m, a power of 2
+        const float sx = hx * sc, sy = hy * sc, sz = hz * sc;
+        const float n2 = fmaf(sx, sx, fmaf(sy, sy, sz * sz));
+        const float ss = sv * sc;
+        const float f = n2 > ss * ss ? ss * rsqrtf(n2) : 1.f;  // S / |q^| when projecting
+        hx *= f; hy *= f; hz *= f;
     } else {
         hx = fminf(fmaxf(hx, -sv), sv);
         hy = fminf(fmaxf(hy, -sv), sv);

@@ -61,6 +61,7 @@ __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float
                                                 const float (&qc)[3][NV], const float (&svc)[NV], float *qo,
                                                 int64_t P) {
     const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
+    const int Pi = (int)P;  // channel stride fits 32 bits (an x-y plane has < 2^31 / 48 voxels)
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const float mc = Rz[v * rps + roff];
@@ -69,9 +70,9 @@ __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float
         const float gz = gzv ? Mn[v] - mc : 0.f;
         float hx = qc[0][v], hy = qc[1][v], hz = qc[2][v];
         flow_step<CAP>(a.ctau, gx, gy, gz, svc[v], hx, hy, hz);
-        st_stream(qo + v * P, hx);
-        st_stream(qo + (NV + v) * P, hy);
-        st_stream(qo + (2 * NV + v) * P, hz);
+        st_stream(qo + v * Pi, hx);
+        st_stream(qo + (NV + v) * Pi, hy);
+        st_stream(qo + (2 * NV + v) * Pi, hz);
     }
 }
 
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
                     float *uo = a.u_out + (int64_t)p * ups + pix;
 #pragma unroll
                     for (int l = 0; l < NL; ++l) {
-                        st_stream(uo + l * P, un[l]);
+                        st_stream(uo + l * (int)P, un[l]);
                         resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                     }
                 }
