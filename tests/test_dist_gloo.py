@@ -1,0 +1,111 @@
+"""Host-side logic of the multi-GPU z-slab exchange (row e), world size 2 and 3 on CPU with gloo.
+
+`paper_1501_07844_b200.dist.halo_exchange` is the routine the GPU ranks use (there over NCCL on the
+library's device ranges).  Here every rank holds CPU tensors laid out like one slab of the library's
+internal state (planes -1 .. nz_local, u: [plane][l][y][x], q: [plane][k][v][y][x]) and a toy update
+with exactly the pseudo-flow stencil's plane dependencies (u, q of plane z+1; q^z of plane z-1); the
+decomposed run must equal the single-domain run bit for bit.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+L, V, NY, NX = 3, 2, 4, 5   # labels, flow nodes, plane size
+
+
+def _toy_step(u, q, zg0, nzg):
+    """One 'iteration' on planes 0..n-1 reading plane n (above) and plane -1's q^z (below).
+    u: [n+2][L][NY][NX], q: [n+2][3][V][NY][NX] with index 0 = plane -1."""
+    n = u.shape[0] - 2
+    un, qn = u.copy(), q.copy()
+    for z in range(n):
+        i = z + 1
+        zg = zg0 + z
+        above = zg < nzg - 1
+        qz_below = q[i - 1, 2] if zg > 0 else 0.0
+        div = q[i, 0] + q[i, 1] + (q[i, 2] - qz_below)                 # uses plane z-1 (q^z)
+        un[i] = u[i] * 0.9 + 0.1 * np.tanh(div.sum(0))[None] + (0.05 * u[i + 1] if above else 0.0)
+        qn[i] = q[i] * 0.8 + 0.01 * (u[i + 1].sum(0)[None, None] if above else 0.0) + 0.001 * (z + zg0)
+    return un, qn
+
+
+def _regions(u, q, rank, world):
+    t = lambda a: torch.from_numpy(a)
+    r = {"send_down_u": None, "send_down_q": None, "recv_up_u": None, "recv_up_q": None, "send_up_qz": None,
+         "recv_down_qz": None}
+    n = u.shape[0] - 2
+    if rank > 0:
+        r["send_down_u"] = t(u[1].reshape(-1))
+        r["send_down_q"] = t(q[1].reshape(-1))
+        r["recv_down_qz"] = t(q[0, 2].reshape(-1))
+    if rank < world - 1:
+        r["recv_up_u"] = t(u[n + 1].reshape(-1))
+        r["recv_up_q"] = t(q[n + 1].reshape(-1))
+        r["send_up_qz"] = t(q[n, 2].reshape(-1))
+    return r
+
+
+def _worker(rank, world, port, nzg, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1501_07844_b200.dist import halo_exchange
+    from paper_1501_07844_b200.solver import slab_bounds
+    z0, z1 = slab_bounds(nzg, world)[rank]
+    n = z1 - z0
+    rng = np.random.default_rng(0)
+    U = rng.uniform(size=(nzg, L, NY, NX))
+    Q = rng.uniform(size=(nzg, 3, V, NY, NX))
+    u = np.zeros((n + 2, L, NY, NX))
+    q = np.zeros((n + 2, 3, V, NY, NX))
+    u[1:n + 1] = U[z0:z1]
+    q[1:n + 1] = Q[z0:z1]
+    # initial halos (the library's init state is uniform, so its halos start correct; here exchange once)
+    halo_exchange(_regions(u, q, rank, world), rank, world)
+    for _ in range(steps):
+        u, q = _toy_step(u, q, z0, nzg)
+        u = np.ascontiguousarray(u); q = np.ascontiguousarray(q)
+        halo_exchange(_regions(u, q, rank, world), rank, world)
+    out[rank] = (u[1:n + 1].copy(), q[1:n + 1].copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,nzg", [(2, 7), (3, 9), (2, 2)])
+def test_gloo_slab_exchange_matches_single_domain(world, nzg):
+    steps = 4
+    rng = np.random.default_rng(0)
+    U = rng.uniform(size=(nzg, L, NY, NX))
+    Q = rng.uniform(size=(nzg, 3, V, NY, NX))
+    u = np.zeros((nzg + 2, L, NY, NX)); u[1:nzg + 1] = U
+    q = np.zeros((nzg + 2, 3, V, NY, NX)); q[1:nzg + 1] = Q
+    for _ in range(steps):
+        u, q = _toy_step(u, q, 0, nzg)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, nzg, steps, out), nprocs=world, join=True)
+    ud = np.concatenate([out[r][0] for r in range(world)])
+    qd = np.concatenate([out[r][1] for r in range(world)])
+    assert np.array_equal(ud, u[1:nzg + 1]) and np.array_equal(qd, q[1:nzg + 1])
+
+
+def test_slab_bounds():
+    from paper_1501_07844_b200.solver import slab_bounds
+    assert slab_bounds(256, 8) == [(32 * i, 32 * (i + 1)) for i in range(8)]
+    assert slab_bounds(10, 3) == [(0, 4), (4, 8), (8, 10)]
+    b = slab_bounds(768, 8)
+    assert all(z1 - z0 == 96 for z0, z1 in b)
