@@ -206,7 +206,8 @@ struct pf_solver {
     // TMA-staged persistent kernel (default) -- see pf_staged.cuh
     bool staged = false;
     StagedKernelInfo sinfo{};
-    CUtensorMap tm_q[2], tm_u[2], tm_D, tm_S;
+    CUtensorMap tm_q[2], tm_u[2], tm_D, tm_S, tm_qo[2], tm_uo[2];
+    int staged_smem = 0;
     int s_ch = 0;
     int tiles_x = 0, tiles = 0, items = 0, sgrid = 0;
     unsigned int tx_bytes = 0;
@@ -446,6 +447,13 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         const char *env = getenv("PF_ITER_KERNEL");
         const bool want_global = env && strcmp(env, "global") == 0;
         s->staged = !want_global && staged_kernel_lookup(gc.NI, gc.NL, &s->sinfo) && encode_fn() != nullptr;
+        if (s->staged) {
+            const int s_ch = S->kind == PF_S_SHARED_FIELD ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NV : 0);
+            s->staged_smem = s->sinfo.smem_bytes + 8 * ((s_ch * s->sinfo.tile_y * 32 + 31) / 32 * 32);
+            int maxsm = 0;
+            cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device);
+            if (s->staged_smem > maxsm) s->staged = false;  // e.g. per-node S fields with many nodes
+        }
     }
     cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -524,7 +532,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     {
         const void *fn = s->staged ? s->sinfo.func : s->kinfo.func;
         const int thr = s->staged ? s->sinfo.threads : s->kinfo.threads;
-        const int smb = s->staged ? s->sinfo.smem_bytes : s->kinfo.smem_bytes;
+        const int smb = s->staged ? s->staged_smem : s->kinfo.smem_bytes;
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);
         if (e != cudaSuccess) { cuda_fail(s, e, "cudaFuncSetAttribute"); return bail(PF_ERR_CUDA); }
         cudaFuncAttributes fa;
@@ -539,6 +547,11 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
             ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NV, nzl + 2, 40,
                                 ty + 2, 3 * NV);
             ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, NL);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NV, nzl + 2, 32, ty,
+                                3 * NV);
+            ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, NL);
         }
         ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
         if (s->s_ch) ok = ok && encode4d(&s->tm_S, s->S_alloc, s->nx, s->ny, s->pitch, s->s_ch, nzl, 32, ty, s->s_ch);
@@ -633,12 +646,14 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
         if (s->staged) {
             sa.tm_q = s->tm_q[s->cur];
             sa.tm_u = s->tm_u[s->cur];
+            sa.tm_qo = s->tm_qo[1 - s->cur];
+            sa.tm_uo = s->tm_uo[1 - s->cur];
             sa.q_in = s->q[s->cur];
             sa.u_out = s->u[1 - s->cur];
             sa.q_out = s->q[1 - s->cur];
             sa.check = a.check;
             void *args[] = {(void *)&sa};
-            CK(cudaLaunchKernel(s->sinfo.func, s->grid, dim3(s->sinfo.threads), args, s->sinfo.smem_bytes, s->stream),
+            CK(cudaLaunchKernel(s->sinfo.func, s->grid, dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
                "launch pf_iter_staged");
         } else {
             a.u_in = s->u[s->cur];
@@ -845,7 +860,7 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     info->threads_per_cta = s->staged ? s->sinfo.threads : s->kinfo.threads;
     info->ctas = (int)(s->grid.x * s->grid.y * s->grid.z);
     info->regs_per_thread = s->regs;
-    info->smem_bytes = s->staged ? s->sinfo.smem_bytes : s->kinfo.smem_bytes;
+    info->smem_bytes = s->staged ? s->staged_smem : s->kinfo.smem_bytes;
     info->staged = s->staged ? 1 : 0;
     info->work_items = s->staged ? s->items : info->ctas;
     info->ctas_per_sm = s->ctas_per_sm;

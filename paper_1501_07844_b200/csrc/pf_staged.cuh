@@ -25,6 +25,8 @@ struct StagedArgs {
     CUtensorMap tm_u;   // input u, 4-D (x, y, l, plane+1)
     CUtensorMap tm_D;   // D, 4-D (x, y, l, plane)
     CUtensorMap tm_S;   // S field, 4-D (x, y, channel, plane); unused when s_ch == 0
+    CUtensorMap tm_uo;  // output u, store box (32, TY, NL)        [OSTAGE]
+    CUtensorMap tm_qo;  // output q, store box (32, TY, 3*NV)      [OSTAGE]
     const float *q_in;  // plane 0 of input q (chunk-start q^z(zc0-1) read)
     float *u_out;
     float *q_out;
@@ -41,27 +43,36 @@ struct StagedArgs {
 
 __host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 
-template <int NI, int NL, int TY>
+template <int NI, int NL, int TY, int OSTAGE>
 struct StagedLayout {
     static constexpr int NV = NI + NL;
     static constexpr int QW = 40, UW = 36, SW = 32;
     static constexpr int QROWS = TY + 2, UROWS = TY + 1;
-    static constexpr int QSZ = round32(3 * NV * QROWS * QW);  // floats per stage (ndim = 3 maximum)
+    static constexpr int QSZ = round32(3 * NV * QROWS * QW);  // floats per stage
     static constexpr int USZ = round32(NL * UROWS * UW);
-    static constexpr int SSZ = round32(NV * TY * SW);         // per-node fields maximum
     static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NV * RPS;
-    static constexpr int kFloats = 2 * QSZ + 4 * USZ + 2 * SSZ + round32(3 * RING);
-    static constexpr int kBytes = kFloats * 4 + 2 * 8;
+    static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // output staging (per buffer)
+    static constexpr int QOSZ = OSTAGE ? round32(3 * NV * TY * 32) : 0;
     static constexpr int kThreads = 32 * TY + 64;
+    // runtime part: the S staging ring holds s_ch channels (0, 1 or NV)
+    __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
+    __host__ __device__ static constexpr int off_U() { return 2 * QSZ; }
+    __host__ __device__ static constexpr int off_D() { return 2 * QSZ + 2 * USZ; }
+    __host__ __device__ static constexpr int off_S() { return 2 * QSZ + 4 * USZ; }
+    __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + 2 * ssz(s_ch); }
+    __host__ __device__ static constexpr int off_Uo(int s_ch) { return off_R(s_ch) + round32(3 * RING); }
+    __host__ __device__ static constexpr int off_Qo(int s_ch) { return off_Uo(s_ch) + 2 * UOSZ; }
+    __host__ __device__ static constexpr int floats(int s_ch) { return off_Qo(s_ch) + 2 * QOSZ; }
+    __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 16; }
 };
 
-template <int NV, int CAP>
+template <int NV, int CAP, int OSTAGE, int TY>
 __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int roff, int rps, int rs,
                                                 const float (&Mn)[NV], bool has_z, int x, int y, int zg,
                                                 const float (&qc)[3][NV], const float (&svc)[NV], float *qo,
                                                 int64_t P) {
     const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
-    const int Pi = (int)P;  // channel stride fits 32 bits (an x-y plane has < 2^31 / 48 voxels)
+    const int Pi = OSTAGE ? TY * 32 : (int)P;  // channel stride: smem staging tile, or global (fits 32 bits)
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
         const float mc = Rz[v * rps + roff];
@@ -70,26 +81,35 @@ __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float
         const float gz = gzv ? Mn[v] - mc : 0.f;
         float hx = qc[0][v], hy = qc[1][v], hz = qc[2][v];
         flow_step<CAP>(a.ctau, gx, gy, gz, svc[v], hx, hy, hz);
-        st_stream(qo + v * Pi, hx);
-        st_stream(qo + (NV + v) * Pi, hy);
-        st_stream(qo + (2 * NV + v) * Pi, hz);
+        if (OSTAGE) {
+            qo[v * Pi] = hx;
+            qo[(NV + v) * Pi] = hy;
+            qo[(2 * NV + v) * Pi] = hz;
+        } else {
+            st_stream(qo + v * Pi, hx);
+            st_stream(qo + (NV + v) * Pi, hy);
+            st_stream(qo + (2 * NV + v) * Pi, hz);
+        }
     }
 }
 
-template <int NI, int NL, int TY>
+template <int NI, int NL, int TY, int OSTAGE>
 __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
-    using L = StagedLayout<NI, NL, TY>;
+    using L = StagedLayout<NI, NL, TY, OSTAGE>;
     constexpr int NV = L::NV, QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
     constexpr int QCS = QROWS * QW;   // q channel stride in smem
     constexpr int UCS = UROWS * UW;
     constexpr int RS = L::RS, RPS = L::RPS, RING = L::RING;
     extern __shared__ __align__(128) float sm[];
     float *Qs = sm;
-    float *Us = Qs + 2 * L::QSZ;
-    float *Ds = Us + 2 * L::USZ;
-    float *Ss = Ds + 2 * L::USZ;
-    float *R = Ss + 2 * L::SSZ;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L::kFloats);
+    float *Us = sm + L::off_U();
+    float *Ds = sm + L::off_D();
+    float *Ss = sm + L::off_S();
+    float *R = sm + L::off_R(a.s_ch);
+    float *Uo = sm + L::off_Uo(a.s_ch);
+    float *Qo = sm + L::off_Qo(a.s_ch);
+    const int SSZ = L::ssz(a.s_ch);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L::floats(a.s_ch));
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool is_main = warp < TY;
@@ -118,8 +138,9 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
         tma_load_4d(Qs + stage * L::QSZ, &a.tm_q, &bars[stage], x0 - 4, y0 - 1, 0, plane + 1);
         tma_load_4d(Us + stage * L::USZ, &a.tm_u, &bars[stage], x0, y0, 0, plane + 1);
         tma_load_4d(Ds + stage * L::USZ, &a.tm_D, &bars[stage], x0, y0, 0, plane);
-        if (a.s_ch) tma_load_4d(Ss + stage * L::SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
+        if (a.s_ch) tma_load_4d(Ss + stage * SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
     };
+    const uint64_t pol_out = OSTAGE ? policy_evict_first() : 0;
 
     float resid = 0.f;
     int kbase = 0;   // planes consumed so far by this CTA (ring position / mbarrier parity)
@@ -191,12 +212,17 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
                         const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                         atomicMin(a.err_voxel, vox);
                     }
-                    float *uo = a.u_out + (int64_t)p * ups + pix;
+                    if (OSTAGE) {
+                        float *uo = Uo + (p & 1) * L::UOSZ + ly * 32 + lx;
 #pragma unroll
-                    for (int l = 0; l < NL; ++l) {
-                        st_stream(uo + l * (int)P, un[l]);
-                        resid = fmaxf(resid, fabsf(un[l] - uold[l]));
+                        for (int l = 0; l < NL; ++l) uo[l * TY * 32] = un[l];
+                    } else {
+                        float *uo = a.u_out + (int64_t)p * ups + pix;
+#pragma unroll
+                        for (int l = 0; l < NL; ++l) st_stream(uo + l * (int)P, un[l]);
                     }
+#pragma unroll
+                    for (int l = 0; l < NL; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                 }
 #pragma unroll
                 for (int l = 0; l < NL; ++l) Mv[NI + l] = ut[l];
@@ -204,7 +230,7 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
 #pragma unroll
                 for (int v = 0; v < NV; ++v) Rp[v * RPS + roff] = Mv[v];
                 if (is_main) {
-                    const float *Sb = Ss + st * L::SSZ + ly * SW + lx;
+                    const float *Sb = Ss + st * SSZ + ly * SW + lx;
                     if (a.s_ch == 0) {
 #pragma unroll
                         for (int v = 0; v < NV; ++v) svn[v] = a.g.s[v];
@@ -218,20 +244,32 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
                     }
                 }
             }
-            __syncthreads();  // ring slot p complete; stage st fully consumed
-            if (tid == 0 && p + 2 <= pend) {
-                fence_proxy_async();
-                issue(p + 2, st, x0, y0);
+            if (OSTAGE) {
+                fence_proxy_async();                // staged outputs -> visible to the TMA (async proxy)
+                if (tid == 0) bulk_wait_read_all(); // stores of the buffers about to be rewritten have read them
+            }
+            __syncthreads();  // ring slot p complete; stage st fully consumed; staged outputs complete
+            if (tid == 0) {
+                if (p + 2 <= pend) {
+                    fence_proxy_async();
+                    issue(p + 2, st, x0, y0);
+                }
+                if (OSTAGE) {
+                    if (p < zc1) tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, 0, p + 1, pol_out);
+                    if (p - 2 >= zc0) tma_store_4d(&a.tm_qo, Qo + (p & 1) * L::QOSZ, x0, y0, 0, p - 1, pol_out);
+                    bulk_commit();
+                }
             }
             // ---------------- stage B(p-1): flow step + projection of plane p-1
             if (is_main && valid && p > zc0) {
                 const int z = p - 1;
                 const float *Rz = R + (z % 3) * RING;
                 float *qo = a.q_out + (int64_t)z * qps + pix;
+                if (OSTAGE) qo = Qo + (z & 1) * L::QOSZ + ly * 32 + lx;
                 if (a.cap == 0)
-                    flow_out_staged<NV, 0>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
+                    flow_out_staged<NV, 0, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
                 else
-                    flow_out_staged<NV, 1>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
+                    flow_out_staged<NV, 1, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
             }
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
@@ -247,13 +285,27 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             float Mdummy[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) Mdummy[v] = 0.f;
+            if (OSTAGE) qo = Qo + (z & 1) * L::QOSZ + ly * 32 + lx;
             if (a.cap == 0)
-                flow_out_staged<NV, 0>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo, P);
+                flow_out_staged<NV, 0, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo,
+                                                   P);
             else
-                flow_out_staged<NV, 1>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo, P);
+                flow_out_staged<NV, 1, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo,
+                                                   P);
+        }
+        if (OSTAGE) {  // flush the item's last staged flow planes
+            fence_proxy_async();
+            __syncthreads();
+            if (tid == 0) {
+                for (int z = max(zc0, pend - 1); z < zc1; ++z)
+                    tma_store_4d(&a.tm_qo, Qo + (z & 1) * L::QOSZ, x0, y0, 0, z + 1, pol_out);
+                bulk_commit();
+                bulk_wait_read_all();
+            }
         }
         kbase += pend - zc0 + 1;
     }
+    if (OSTAGE && tid == 0) bulk_wait_all();
     if (a.check) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) resid = fmaxf(resid, __shfl_xor_sync(0xffffffffu, resid, o));
@@ -264,8 +316,9 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
 struct StagedKernelInfo {
     const void *func;
     int threads;
-    int smem_bytes;
+    int smem_bytes;  // with s_ch = 0; add 2 * round32(s_ch * tile_y * 32) floats for an S field
     int tile_y;
+    int ostage;      // 1: outputs staged in smem and written by TMA stores
 };
 
 bool staged_kernel_lookup(int NI, int NL, StagedKernelInfo *info);
