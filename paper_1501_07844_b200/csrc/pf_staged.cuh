@@ -163,18 +163,20 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             issue(zc0, kbase & 1, x0, y0);
             if (zc0 + 1 <= pend) issue(zc0 + 1, (kbase + 1) & 1, x0, y0);
         }
-        // q of the plane below the chunk (its z-component enters div of the first plane)
-        float qc[3][NV];
-        float svc[NV];
+        // q of the plane below the chunk (its z-component enters div of the first plane).  Two register
+        // sets alternate between "current plane" and "plane awaiting its flow step" (no copies).
+        float qA[3][NV], qB[3][NV];
+        float sA[NV], sB[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) { qc[0][v] = 0.f; qc[1][v] = 0.f; qc[2][v] = 0.f; svc[v] = 0.f; }
+        for (int v = 0; v < NV; ++v) { qA[0][v] = 0.f; qA[1][v] = 0.f; qA[2][v] = 0.f; sA[v] = 0.f; }
         if (valid && (a.zg0 + zc0) > 0) {
             const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + 2 * NV * P + pix;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) qc[2][v] = __ldg(qb + v * P);
+            for (int v = 0; v < NV; ++v) qA[2][v] = __ldg(qb + v * P);
         }
 
-        for (int p = zc0; p <= pend; ++p) {
+        auto plane_step = [&](const int p, float (&qc)[3][NV], float (&svc)[NV], float (&qn)[3][NV],
+                              float (&svn)[NV]) {
             const int k = kbase + (p - zc0);
             const int st = k & 1;
             mbar_wait(&bars[st], (k >> 1) & 1);
@@ -182,9 +184,7 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             const float *Ub = Us + st * L::USZ;
             const float *Db = Ds + st * L::USZ;
             float *Rp = R + (p % 3) * RING;
-            float qn[3][NV];
             float Mv[NV];
-            float svn[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) svn[v] = 0.f;
             // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
@@ -271,14 +271,16 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
                 else
                     flow_out_staged<NV, 1, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
             }
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                qc[0][v] = qn[0][v]; qc[1][v] = qn[1][v]; qc[2][v] = qn[2][v];
-                svc[v] = svn[v];
-            }
+        };
+        int p = zc0;
+        for (; p + 1 <= pend; p += 2) {
+            plane_step(p, qA, sA, qB, sB);
+            plane_step(p + 1, qB, sB, qA, sA);
         }
+        const bool last_in_B = p <= pend;
+        if (last_in_B) plane_step(p, qA, sA, qB, sB);
         // last plane of the volume: no plane above, nabla_z = 0
-        if (!has_above && is_main && valid) {
+        auto tail_step = [&](const float (&qc)[3][NV], const float (&svc)[NV]) {
             const int z = zc1 - 1;
             const float *Rz = R + (z % 3) * RING;
             float *qo = a.q_out + (int64_t)z * qps + pix;
@@ -292,6 +294,10 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             else
                 flow_out_staged<NV, 1, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo,
                                                    P);
+        };
+        if (!has_above && is_main && valid) {
+            if (last_in_B) tail_step(qB, sB);
+            else tail_step(qA, sA);
         }
         if (OSTAGE) {  // flush the item's last staged flow planes
             fence_proxy_async();

@@ -1,0 +1,104 @@
+"""Measure every BASELINE.json config on one GPU (same method as bench.py) -> JSON lines.
+
+usage: python tools/bench_configs.py [C1 C2 C3 C4 C5slab] [--steps K] [--oracle]
+C5 (768^3, K=16) does not fit one GPU in the fused layout; "C5slab" is one rank's 768x768x96 z-slab
+of it (the weak-scaling unit of the 8-GPU run).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1501_07844_b200 as pf  # noqa: E402
+import phantoms as P  # noqa: E402
+
+
+def cfg_of(name):
+    if name == "C5slab":
+        return P.config("C5").resized(768, 768, 96, name="C5slab")
+    return P.config(name)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5slab"])
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--oracle", action="store_true")
+    args = ap.parse_args()
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    dev = torch.device("cuda", 0)
+    for name in args.configs:
+        cfg = cfg_of(name)
+        inp = P.generate(cfg)
+        g = inp.graph
+        D = [torch.from_numpy(np.ascontiguousarray(inp.D[l])).to(dev) for l in range(inp.D.shape[0])]
+        kw = {"s_shared": torch.from_numpy(inp.s_field).to(dev)} if inp.s_kind == "shared_field" else \
+            {"s_scalars": inp.s_scalars}
+        s = pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.child, g.weight), D, c=cfg.c,
+                      tau=cfg.tau, check_every=10, **kw)
+        stream = torch.cuda.current_stream(dev)
+        s.set_stream(stream.cuda_stream)
+        labels = torch.empty((cfg.nz, cfg.ny, cfg.nx), dtype=torch.uint8, device=dev)
+        n = cfg.iters
+
+        def step(ev=None):
+            s.reset()
+            if ev:
+                ev[0].record(stream)
+            s.iterate(n)
+            if ev:
+                ev[1].record(stream)
+            pf.pf_get_labeling(s.h, None, labels)
+
+        step()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / args.steps
+        it_ms = sum(a.elapsed_time(b) for a, b in evs) / (args.steps * n)
+        info = s.kernel_info()
+        NL = len(D)
+        V = cfg.V
+        r = s.iterate(0, True)
+        e, f = s.energy()
+        s.close()
+        line = {"config": name, "dims": [cfg.nx, cfg.ny, cfg.nz], "end_labels": NL, "nodes": g.num_nodes - 1,
+                "iterations": n, "ms_per_solve": ms, "ms_per_iteration": it_ms,
+                "gvl_it_per_s": V * NL * n / (ms / 1e3) / 1e9,
+                "gvnode_it_per_s": V * (g.num_nodes - 1) * n / (ms / 1e3) / 1e9,
+                "algorithmic_bytes_per_iteration": info["algorithmic_bytes_per_iteration"],
+                "achieved_gbs": info["algorithmic_bytes_per_iteration"] / (it_ms / 1e3) / 1e9,
+                "frac_of_measured_peak": info["algorithmic_bytes_per_iteration"] / (it_ms / 1e3) / 1e9 / peak,
+                "kernel": {k: info[k] for k in ("staged", "tile_y", "z_chunk", "ctas", "regs_per_thread",
+                                                "smem_bytes", "work_items")},
+                "device_bytes": info["device_bytes"], "final_primal": e, "final_dual": f}
+        if args.oracle:
+            import oracle as O
+            planes = max(1, min(cfg.nz, int(4e6 // (cfg.nx * cfg.ny))))
+            sub = P.generate(cfg, (0, planes, 0, cfg.ny, 0, cfg.nx))
+            t = time.perf_counter()
+            O.run_inputs(sub, 2)
+            dt = time.perf_counter() - t
+            rate = sub.D.size * 2 / dt
+            line["oracle_1thread_gvl_it_per_s"] = rate / 1e9
+            line["oracle_1thread_full_run_s_extrapolated"] = V * NL * n / rate
+        print(json.dumps(line), flush=True)
+        del D, kw, labels
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
