@@ -56,6 +56,9 @@ def _load():
         lib.oracle_dag.restype = i64
         lib.oracle_dag.argtypes = [i32, i64, i64, i64, i32, i32, ip, ip, dp, dp, dp, dp, dp, ctypes.c_double,
                                    ctypes.c_double, i32, i32, i32, ctypes.c_double]
+        lib.oracle_ishikawa.restype = i64
+        lib.oracle_ishikawa.argtypes = [i32, i64, i64, i64, i32, dp, dp, dp, dp, ctypes.c_double, ctypes.c_double,
+                                        i32, i32, i32, ctypes.c_double]
         lib.oracle_topo_order.restype = i32
         lib.oracle_topo_order.argtypes = [i32, i32, ip, ip, dp, ip]
         lib.oracle_grad.restype = i32
@@ -121,6 +124,16 @@ def dag_iterate(num_nodes: int, parent, child, weight, D: np.ndarray, S: np.ndar
     return u, q
 
 
+def ishikawa_iterate(D: np.ndarray, S: np.ndarray, u: np.ndarray, q: np.ndarray, ndim: int, c: float, tau: float,
+                     niter: int, shift: int = SHIFT_MIN, cap: int = CAP_L2, u_floor: float = U_FLOOR):
+    """Algorithm 3 in place.  D,u: [N+1][...]; S: [N][...] (level flows 1..N); q: [N][ndim][...]."""
+    NL, nz, ny, nx = D.shape
+    st = _load().oracle_ishikawa(ndim, nx, ny, nz, NL - 1, _dp(D), _dp(S), _dp(u), _dp(q), c, tau, shift, cap,
+                                 niter, u_floor)
+    _status(st)
+    return u, q
+
+
 def topo_order(num_nodes: int, parent, child, weight) -> Optional[List[int]]:
     """O by Kahn's algorithm with lowest-id tie-break; None if invalid."""
     par = np.ascontiguousarray(parent, dtype=np.int32)
@@ -182,6 +195,10 @@ def run_inputs(inp, niter: int, shift: int = SHIFT_MIN, cap: Optional[int] = Non
         u, q = state
     if cfg.kind == "potts":
         potts_iterate(D, np.ascontiguousarray(S[1:]), u, q, cfg.ndim, c, tau, niter, shift, cap)
+    elif cfg.kind == "ishikawa":
+        # Alg. 3 on the level flows (node ids 1..N); end labels (ids N+1..) carry no flow and stay 0
+        N = NL - 1
+        ishikawa_iterate(D, np.ascontiguousarray(S[1:N + 1]), u, q[:N], cfg.ndim, c, tau, niter, shift, cap)
     else:
         dag_iterate(g.num_nodes, g.parent, g.child, g.weight.astype(np.float64), D, S, u, q, cfg.ndim, c, tau,
                     niter, shift, cap)

@@ -10,6 +10,7 @@
  * line of the paper's listings, in the listings' order and notation.
  *   oracle_potts    -- Algorithm 1
  *   oracle_dag      -- Algorithm 2, d_L recursion P:190-197
+ *   oracle_ishikawa -- Algorithm 3
  *
  * Readings of what the paper leaves open:
  *   R1  exponent shift: shift==0 (SHIFT_MIN) subtracts m(x) = min over end
@@ -327,4 +328,73 @@ int oracle_project(int ndim, int64_t nx, int64_t ny, int64_t nz, double *q, cons
     if (!check_dims(&d)) return 0;
     project(&d, q, S, cap);
     return 1;
+}
+
+/*
+ * Algorithm 3: continuous Ishikawa model with N levels and N+1 labels L_0..L_N,
+ * `niter` passes of the while-loop body, in the listing's order:
+ *   P:318  d_0 <- 0
+ *   P:319  for i = 1..N: d_i <- d_{i-1} + div q_i                 (prefix of the level flows)
+ *   P:322  forall i: d_i <- d_i + D_i
+ *   P:324  forall i: u_i <- u_i exp(-d_i/c)                        [R1: minus m(x) = min_i d_i]
+ *   P:325  forall i: d_i <- u_i                                    (unnormalised masses)
+ *   P:326  a <- sum_i u_i
+ *   P:327  forall i: u_i <- u_i / a                                [R18 floor]
+ *   P:329  for i = N-1 .. 1: d_i <- d_i + d_{i+1}                  (reading of the stray prime on
+ *                                                                   d_{L_{i+1}}': the value just
+ *                                                                   accumulated, i.e. a suffix sum)
+ *   P:332  for i = 1..N: q_i <- Proj(q_i - c tau nabla d_i)
+ * D: [N+1][V]; S: [N][V] (capacity of level flow q_i, i = 1..N); u: [N+1][V]; q: [N][ndim][V].
+ */
+int64_t oracle_ishikawa(int ndim, int64_t nx, int64_t ny, int64_t nz, int N, const double *D, const double *S,
+                        double *u, double *q, double c, double tau, int shift, int cap, int niter, double u_floor) {
+    odims d = {ndim, nx, ny, nz};
+    if (!check_dims(&d) || N < 1 || !(c > 0) || !(tau > 0)) return BAD_ARGS;
+    const int64_t n = vol(&d);
+    const int NL = N + 1;
+    double *dd = (double *)malloc(sizeof(double) * n * NL);
+    double *m = (double *)malloc(sizeof(double) * n);
+    double *a = (double *)malloc(sizeof(double) * n);
+    double *tmp = (double *)malloc(sizeof(double) * n);
+#define DI(i) (dd + (int64_t)(i) * n)
+#define UI(i) (u + (int64_t)(i) * n)
+#define QI(i) (q + (int64_t)((i) - 1) * ndim * n)
+    int64_t status = 0;
+    for (int it = 0; it < niter && status == 0; ++it) {
+        for (int64_t x = 0; x < n; ++x) DI(0)[x] = 0.0;
+        for (int i = 1; i <= N; ++i) {
+            divergence(&d, QI(i), tmp);
+            for (int64_t x = 0; x < n; ++x) DI(i)[x] = DI(i - 1)[x] + tmp[x];
+        }
+        for (int i = 0; i <= N; ++i)
+            for (int64_t x = 0; x < n; ++x) DI(i)[x] = DI(i)[x] + D[(int64_t)i * n + x];
+        for (int64_t x = 0; x < n; ++x) {
+            double mm = DI(0)[x];
+            for (int i = 1; i <= N; ++i) mm = fmin(mm, DI(i)[x]);
+            m[x] = (shift == 0) ? mm : 0.0;
+        }
+        for (int i = 0; i <= N; ++i)
+            for (int64_t x = 0; x < n; ++x) UI(i)[x] = UI(i)[x] * exp(-(DI(i)[x] - m[x]) / c);
+        for (int i = 0; i <= N; ++i) memcpy(DI(i), UI(i), sizeof(double) * n);
+        for (int64_t x = 0; x < n; ++x) {
+            a[x] = 0.0;
+            for (int i = 0; i <= N; ++i) a[x] += UI(i)[x];
+            if (!(a[x] > 0.0) || !isfinite(a[x])) { status = -1 - x; break; }
+        }
+        if (status != 0) break;
+        for (int i = 0; i <= N; ++i)
+            for (int64_t x = 0; x < n; ++x) {
+                UI(i)[x] = UI(i)[x] / a[x];
+                if (UI(i)[x] < u_floor) UI(i)[x] = 0.0;
+            }
+        for (int i = N - 1; i >= 1; --i)
+            for (int64_t x = 0; x < n; ++x) DI(i)[x] = DI(i)[x] + DI(i + 1)[x];
+        for (int i = 1; i <= N; ++i)
+            flow_step(&d, QI(i), DI(i), S + (int64_t)(i - 1) * n, c * tau, cap, tmp);
+    }
+#undef DI
+#undef UI
+#undef QI
+    free(dd); free(m); free(a); free(tmp);
+    return status;
 }

@@ -136,6 +136,20 @@ def dag_graph() -> Graph:
     return Graph(10, e, ["S", "A", "B", "C", "L0", "L1", "L2", "L3", "L4", "L5"])
 
 
+def ishikawa_graph(N: int) -> Graph:
+    """Ishikawa model with N levels / N+1 ordered labels as a DAG chain: level nodes
+    N_1..N_N (ids 1..N) with N_i -> N_{i+1}; end labels L_0..L_N (ids N+1..2N+1) with S -> L_0,
+    S -> N_1, N_i -> L_i; all weights 1 (so W_(N_i, L_j) = 1 for j >= i: u_{N_i} = sum_{j>=i} u_j).
+    Only the level nodes carry spatial flows; end labels get capacity 0."""
+    e = [(0, N + 1, 1.0), (0, 1, 1.0)]
+    for i in range(1, N + 1):
+        e.append((i, N + 1 + i, 1.0))
+        if i < N:
+            e.append((i, i + 1, 1.0))
+    names = ["S"] + [f"N{i}" for i in range(1, N + 1)] + [f"L{i}" for i in range(N + 1)]
+    return Graph(2 * N + 2, e, names)
+
+
 # --------------------------------------------------------------------------
 # Configs (BASELINE.json configs[0..4]; unspecified details = SURVEY §8.4.1)
 # --------------------------------------------------------------------------
@@ -174,6 +188,8 @@ class Config:
             return hmf_graph()
         if self.kind == "dag":
             return dag_graph()
+        if self.kind == "ishikawa":
+            return ishikawa_graph(self.classes - 1)
         raise ValueError(self.kind)
 
     def mu(self) -> np.ndarray:
@@ -189,6 +205,8 @@ CONFIGS: Dict[str, Config] = {
     "C3": Config("C3", 3, 256, 256, 256, "hmf", 6, 20, 0.15, "sq", "per_node_uniform", 0.0, 300, seed=1003),
     "C4": Config("C4", 3, 320, 320, 320, "dag", 6, 20, 0.15, "sq", "per_node_uniform", 0.0, 300, seed=1004),
     "C5": Config("C5", 3, 768, 768, 768, "potts", 16, 60, 0.15, "abs", "edge", 0.05, 200, seed=1005),
+    # the Ishikawa model (Alg. 3) on C2's phantom -- 8 ordered labels = 7 levels
+    "I2": Config("I2", 3, 256, 256, 256, "ishikawa", 8, 28, 0.15, "sq", "edge", 0.05, 300, seed=1002),
 }
 
 
@@ -280,8 +298,11 @@ class Inputs:
     def s_fields(self) -> List[np.ndarray]:
         """One capacity field per node id (index 0 = None), as float32 arrays (views where possible)."""
         out: List[Optional[np.ndarray]] = [None]
+        leaves = set(self.graph.leaves())
         for v in range(1, self.graph.num_nodes):
-            if self.s_kind == "shared_field":
+            if self.cfg.kind == "ishikawa" and v in leaves:
+                out.append(np.zeros(self.shape, dtype=np.float32))   # end labels carry no flow (Alg. 3)
+            elif self.s_kind == "shared_field":
                 out.append(self.s_field)
             else:
                 out.append(np.full(self.shape, self.s_scalars[v], dtype=np.float32))

@@ -451,3 +451,94 @@ def test_weak_duality_random_feasible_pairs():
             e = E.primal(u, D, S, 10, g.parent, g.child, g.weight, 3, cap)
             f = E.dual(q, D, 10, g.parent, g.child, g.weight, 3)
             assert e >= f - 1e-12
+
+
+# ---------------------------------------------------------------- Ishikawa (Alg. 3)
+@pytest.mark.parametrize("shift", [O.SHIFT_MIN, O.SHIFT_NONE])
+def test_ishikawa_equals_dag_chain(shift):
+    """Alg. 3 is Alg. 2 on the chain DAG whose end labels carry no flow:
+    prefix excesses = top-down pushes, suffix masses = bottom-up pushes."""
+    for N in (1, 3, 5):
+        cfg = P.Config("ish", 3, 11, 9, 7, "ishikawa", N + 1, 6, 0.15, "sq", "edge", 0.05, 0, seed=17 + N)
+        inp = P.generate(cfg)
+        g = inp.graph
+        u1, q1 = O.run_inputs(inp, 40, shift=shift)
+        D = inp.D.astype(np.float64)
+        S = _S_of(inp)
+        assert np.all(S[N + 1:] == 0)
+        u2, q2 = O.init_state(N + 1, 2 * N + 1, inp.shape, 3)
+        O.dag_iterate(g.num_nodes, g.parent, g.child, g.weight, D, S, u2, q2, 3, 0.25, 0.1, 40, shift)
+        assert np.max(np.abs(u1 - u2)) <= 1e-14 and np.max(np.abs(q1 - q2)) <= 1e-14
+        assert np.all(q2[N:] == 0)
+
+
+def test_ishikawa_zero_smoothness_closed_form():
+    """S = 0: every d_i = D_i and u^t_i = exp(-t D_i/c)/sum (Eq. 15 iterated)."""
+    N, c = 4, 0.25
+    D = RNG.uniform(0, 1, size=(N + 1, 3, 4, 5))
+    S = np.zeros((N,) + D.shape[1:])
+    u, q = O.init_state(N + 1, N, D.shape[1:], 3)
+    for t in range(1, 21):
+        O.ishikawa_iterate(D, S, u, q, 3, c, 0.1, 1, u_floor=0.0)
+        z = -t * D / c
+        np.testing.assert_allclose(u, np.exp(z - z.max(0)) / np.exp(z - z.max(0)).sum(0), rtol=1e-12)
+        assert np.all(q == 0)
+
+
+def test_ishikawa_suffix_masses_first_flow_step():
+    """From q = 0 with huge capacities: q_i = -c tau nabla(sum_{j>=i} u~_j)."""
+    N, c, tau = 3, 0.25, 0.1
+    D = RNG.uniform(0, 1, size=(N + 1, 4, 5, 6))
+    u, q = O.init_state(N + 1, N, D.shape[1:], 3)
+    O.ishikawa_iterate(D, np.full((N,) + D.shape[1:], 1e6), u, q, 3, c, tau, 1)
+    mass = np.exp(-(D - D.min(0)) / c) / (N + 1)
+    for i in range(1, N + 1):
+        np.testing.assert_allclose(q[i - 1], -c * tau * E.grad(mass[i:].sum(0), 3), rtol=1e-12, atol=1e-15)
+
+
+def test_ishikawa_two_labels_equals_potts_half_capacity():
+    """N = 1: the Ishikawa energy S|grad u_1| equals the Potts energy with capacity S/2 on both labels
+    (u_0 = 1 - u_1), so both iterations reach the same optimal value (a fixed-point property, not an
+    iterate property); each is certified by its own dual."""
+    r = np.random.default_rng(5)
+    D = r.uniform(0, 1, size=(2, 1, 10, 12))
+    Sf = np.full((1, 10, 12), 0.3)
+    ui, qi = O.init_state(2, 1, D.shape[1:], 2)
+    O.ishikawa_iterate(D, Sf[None], ui, qi, 2, 0.25, 0.1, 30000)
+    up, qp = O.init_state(2, 2, D.shape[1:], 2)
+    O.potts_iterate(D, np.stack([Sf / 2, Sf / 2]), up, qp, 2, 0.25, 0.1, 30000)
+    g = P.ishikawa_graph(1)
+    Si = np.stack([np.zeros_like(Sf), Sf, np.zeros_like(Sf), np.zeros_like(Sf)])
+    qq = np.zeros((3, 2) + D.shape[1:]); qq[:1] = qi
+    Ei = E.primal(ui, D, Si, 4, g.parent, g.child, g.weight, 2)
+    Fi = E.dual(qq, D, 4, g.parent, g.child, g.weight, 2)
+    nn, par, chi, w = E.potts_graph_arrays(2)
+    Sp = np.stack([np.zeros_like(Sf), Sf / 2, Sf / 2])
+    Ep = E.primal(up, D, Sp, nn, par, chi, w, 2)
+    Fp = E.dual(qp, D, nn, par, chi, w, 2)
+    # both models have the same optimal value OPT: Fi <= OPT <= Ei (certified tight) and Fp <= OPT <= Ep
+    assert Ei - Fi < 1e-8 * Ei
+    assert Fp - 1e-9 * Ei <= Ei and Fi <= Ep + 1e-9 * Ei and Ep - Fp < 1e-4 * Ep
+    # the energies are the same function of u_1: evaluate each minimiser under the other model
+    assert abs(E.primal(up, D, Si, 4, g.parent, g.child, g.weight, 2) - Ep) < 1e-12 * Ep
+
+
+def test_ishikawa_exhaustive_and_alm():
+    """3 ordered labels on 2x3 (729 labelings): the converged relaxed energy lower-bounds the discrete
+    optimum; the explicit-flow ALM on the chain DAG reaches the same optimum as Alg. 3."""
+    N = 2
+    g = P.ishikawa_graph(N)
+    r = np.random.default_rng(9)
+    D = r.uniform(0, 1, size=(N + 1, 1, 2, 3))
+    S = np.zeros((g.num_nodes, 1, 2, 3))
+    S[1:N + 1] = 0.2
+    u, q = O.init_state(N + 1, N, D.shape[1:], 2)
+    O.ishikawa_iterate(D, np.ascontiguousarray(S[1:N + 1]), u, q, 2, 0.25, 0.1, 40000)
+    qq = np.zeros((2 * N + 1, 2, 1, 2, 3)); qq[:N] = q
+    Erel = E.primal(u, D, S, g.num_nodes, g.parent, g.child, g.weight, 2)
+    F = E.dual(qq, D, g.num_nodes, g.parent, g.child, g.weight, 2)
+    Eopt, _ = brute.brute_force(D, S, g.num_nodes, g.parent, g.child, g.weight, 2, cap="l2")
+    assert Erel - F <= 1e-9 * Eopt and Erel <= Eopt + 1e-9
+    ua, qa, p = alm.dag_alm(D, S, g.num_nodes, g.parent, g.child, g.weight, 2, 16000)
+    assert abs(float(p[0].sum()) - Erel) <= 1e-8 * Erel
+    assert np.max(np.abs(ua - u)) < 1e-6
