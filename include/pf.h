@@ -83,7 +83,8 @@ typedef struct {
 typedef enum {
     PF_S_SCALAR_PER_NODE = 0, /* scalars[v] for v = 1..num_nodes-1 (scalars[0] ignored) */
     PF_S_SHARED_FIELD = 1,    /* fields[0]: one local volume shared by every node (Eq. 1 writes S(x)) */
-    PF_S_FIELD_PER_NODE = 2   /* fields[v-1]: one local volume per non-source node v (S_L(x)) */
+    PF_S_FIELD_PER_NODE = 2,  /* fields[v-1]: one local volume per non-source node v (S_L(x)) */
+    PF_S_SCALED_FIELD = 3     /* S_v(x) = scalars[v] * fields[0](x): one shared field, per-node factors */
 } pf_s_kind;
 
 typedef struct {
@@ -107,6 +108,12 @@ typedef struct {
 typedef struct {
     int64_t z_begin, z_end;
 } pf_slab;
+
+/* Ishikawa model (Alg. 3).  A graph that is the Ishikawa chain -- level nodes N_1..N_N with
+ * S -> N_1 -> ... -> N_N, end labels L_0..L_N (increasing node ids) with S -> L_0 and N_i -> L_i, all
+ * weights 1 -- whose end labels have identically zero capacity (scalar 0, or factor 0 of a
+ * PF_S_SCALED_FIELD) is solved by the dedicated Ishikawa kernels: flows are stored for the N level
+ * nodes only (prefix excesses, suffix masses), N <= 15.  Any other graph runs Algorithm 2. */
 
 /* Create a solver for the (slab of the) volume and initialise the state:
  * u_L = 1/|L|, q = 0 (reading R8).
@@ -173,6 +180,8 @@ typedef struct {
     int64_t kernel_launches;                 /* this solver's own kernels launched so far */
     int32_t staged;                          /* 1: TMA-staged persistent kernel, 0: global-load kernel */
     int32_t work_items;                      /* (tile, z-chunk) items per iteration */
+    int32_t model;                           /* 0: Alg. 1/2 (star / tree / DAG), 1: Alg. 3 (Ishikawa chain) */
+    int32_t flow_nodes;                      /* nodes whose spatial flow is stored */
 } pf_kernel_info;
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info);

@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 PF_OK, PF_ERR_INVALID, PF_ERR_GRAPH, PF_ERR_OOM, PF_ERR_CUDA, PF_ERR_UNSUPPORTED, PF_ERR_NUMERIC, PF_ERR_STATE = range(8)
 PF_CAP_L2, PF_CAP_LINF = 0, 1
 PF_SHIFT_MIN, PF_SHIFT_NONE = 0, 1
-PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE = 0, 1, 2
+PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE, PF_S_SCALED_FIELD = 0, 1, 2, 3
 _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_CUDA", 5: "PF_ERR_UNSUPPORTED",
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
@@ -72,7 +72,8 @@ class pf_kernel_info(ctypes.Structure):
                 ("threads_per_cta", ctypes.c_int32), ("ctas", ctypes.c_int32), ("regs_per_thread", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("algorithmic_bytes_per_iteration", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64), ("staged", ctypes.c_int32), ("work_items", ctypes.c_int32)]
+                ("kernel_launches", ctypes.c_int64), ("staged", ctypes.c_int32), ("work_items", ctypes.c_int32),
+                ("model", ctypes.c_int32), ("flow_nodes", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p

@@ -61,6 +61,9 @@ bool is_device_ptr(const void *p) {
 // --------------------------------------------------------------------------
 struct Compiled {
     int num_nodes = 0, NI = 0, NL = 0, NV = 0;
+    bool chain = false;  // Ishikawa chain shape (see pf.h); model 1 also needs zero end-label capacities
+    int model = 0;       // 0: Alg. 1/2, 1: Alg. 3 (Ishikawa chain)
+    int NF = 0;          // flow-carrying nodes (positions 0..NF-1)
     std::vector<int> pos_of_node;  // node id -> position, S -> -1
     std::vector<int> node_of_pos;
     GraphConst g;
@@ -138,9 +141,31 @@ pf_status compile_graph(const pf_graph *gr, Compiled *out) {
                 " != 1 (sum of end labels must equal u_S = 1, reading R9)");
     if (!errs.empty()) return fail(PF_ERR_GRAPH, "graph: %s", errs.c_str());
     const int NI = (int)internals.size();
-    if (NI > kMaxInternal || NI + NL > kMaxNodes)
+    // Ishikawa chain: internals in topological order N_1..N_N, S -> {N_1, L_0}, N_i -> {N_{i+1}, L_i},
+    // N_N -> L_N, all weights 1, end labels in increasing id order L_0..L_N
+    bool chain = NL == NI + 1 && NI >= 1 && kids[0].size() == 2;
+    std::vector<int> lev;
+    for (int k = 0; k < n && chain; ++k)
+        if (order[k] != 0 && !kids[order[k]].empty()) lev.push_back(order[k]);
+    auto has_edge = [&](int p, int c) {
+        for (auto &e : kids[p])
+            if (e.first == c && e.second == 1.f) return true;
+        return false;
+    };
+    if (chain) {
+        chain = (int)lev.size() == NI && has_edge(0, lev[0]) && has_edge(0, leaves[0]);
+        for (int i = 0; i < NI && chain; ++i) {
+            const bool last = i == NI - 1;
+            chain = kids[lev[i]].size() == (last ? 1u : 2u) && has_edge(lev[i], leaves[i + 1]) &&
+                    (last || has_edge(lev[i], lev[i + 1]));
+        }
+    }
+    if (!chain && (NI > kMaxInternal || NI + NL > kMaxNodes))
         return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes exceeds the compiled kernel set "
                                         "(<= %d internal, <= %d non-source nodes)", NI, NL, kMaxInternal, kMaxNodes);
+    if (chain && NL > kMaxNodes)
+        return fail(PF_ERR_UNSUPPORTED, "graph: Ishikawa chain with %d labels exceeds %d", NL, kMaxNodes);
+    out->chain = chain;
     out->num_nodes = n;
     out->NI = NI;
     out->NL = NL;
@@ -159,12 +184,12 @@ pf_status compile_graph(const pf_graph *gr, Compiled *out) {
         out->node_of_pos.push_back(v);
     }
     memset(&out->g, 0, sizeof(out->g));
-    for (int v = 1; v < n; ++v) {
+    for (int v = 1; v < n && NI <= kMaxInternal; ++v) {  // dense weights (unused by the chain kernels)
         if (kids[v].empty()) continue;
         const int i = out->pos_of_node[v];
         for (auto &c : kids[v]) out->g.w[i][out->pos_of_node[c.first]] += c.second;
     }
-    out->W.assign(out->NV, std::vector<float>(NL, 0.f));
+    out->W.assign(out->NV, std::vector<float>(NL, 0.f));  // W_(v, B), for reports
     for (int p = 0; p < out->NV; ++p)
         for (int l = 0; l < NL; ++l) out->W[p][l] = (float)Wd[out->node_of_pos[p]][l];
     return PF_OK;
@@ -228,7 +253,7 @@ pf_status cuda_fail(pf_solver *s, cudaError_t e, const char *what) {
 
 int64_t ups(const pf_solver *s) { return (int64_t)s->gc.NL * s->P; }
 // q always carries 3 components internally (q^z == 0 for 2-D volumes), so the kernels need no ndim branch
-int64_t qps(const pf_solver *s) { return (int64_t)3 * s->gc.NV * s->P; }
+int64_t qps(const pf_solver *s) { return (int64_t)3 * s->gc.NF * s->P; }
 
 void free_all(pf_solver *s) {
     for (int i = 0; i < 2; ++i) {
@@ -412,9 +437,12 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     Compiled gc;
     pf_status st = compile_graph(graph, &gc);
     if (st != PF_OK) return st;
-    if (S->kind != PF_S_SCALAR_PER_NODE && S->kind != PF_S_SHARED_FIELD && S->kind != PF_S_FIELD_PER_NODE)
+    if (S->kind != PF_S_SCALAR_PER_NODE && S->kind != PF_S_SHARED_FIELD && S->kind != PF_S_FIELD_PER_NODE &&
+        S->kind != PF_S_SCALED_FIELD)
         return fail(PF_ERR_INVALID, "smoothness: bad kind");
-    if (S->kind == PF_S_SCALAR_PER_NODE) {
+    if (S->kind == PF_S_SCALED_FIELD && (!S->scalars || !S->fields))
+        return fail(PF_ERR_INVALID, "smoothness: scaled field needs scalars and fields[0]");
+    if (S->kind == PF_S_SCALAR_PER_NODE || S->kind == PF_S_SCALED_FIELD) {
         if (!S->scalars) return fail(PF_ERR_INVALID, "smoothness: scalars is NULL");
         for (int v = 1; v < gc.num_nodes; ++v)
             if (!(S->scalars[v] >= 0.f) || !std::isfinite(S->scalars[v]))
@@ -424,6 +452,17 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     }
     for (int l = 0; l < gc.NL; ++l)
         if (!D[l]) return fail(PF_ERR_INVALID, "D[%d] is NULL", l);
+    // Ishikawa model (Alg. 3): chain shape and identically-zero end-label capacities
+    if (gc.chain) {
+        bool zero = S->kind == PF_S_SCALAR_PER_NODE || S->kind == PF_S_SCALED_FIELD;
+        for (int l = 0; l < gc.NL && zero; ++l) zero = S->scalars[gc.node_of_pos[gc.NI + l]] == 0.f;
+        gc.model = zero ? 1 : 0;
+    }
+    if (gc.model == 0 && (gc.NI > kMaxInternal || gc.NV > kMaxNodes))
+        return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes exceeds the compiled kernel set "
+                                        "(<= %d internal, <= %d non-source nodes)", gc.NI, gc.NL, kMaxInternal,
+                    kMaxNodes);
+    gc.NF = gc.model == 1 ? gc.NI : gc.NV;
 
     pf_solver *s = new pf_solver();
     cudaGetDevice(&s->device);
@@ -439,16 +478,17 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     s->gc = gc;
     s->cfg = *cfg;
     s->s_kind = S->kind;
-    if (!iter_kernel_lookup(gc.NI, gc.NL, &s->kinfo)) {
+    if (!iter_kernel_lookup(gc.NI, gc.NL, gc.model, &s->kinfo)) {
         delete s;
         return fail(PF_ERR_UNSUPPORTED, "no compiled kernel for %d internal / %d end nodes", gc.NI, gc.NL);
     }
     {
         const char *env = getenv("PF_ITER_KERNEL");
         const bool want_global = env && strcmp(env, "global") == 0;
-        s->staged = !want_global && staged_kernel_lookup(gc.NI, gc.NL, &s->sinfo) && encode_fn() != nullptr;
+        s->staged = !want_global && staged_kernel_lookup(gc.NI, gc.NL, gc.model, &s->sinfo) && encode_fn() != nullptr;
         if (s->staged) {
-            const int s_ch = S->kind == PF_S_SHARED_FIELD ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NV : 0);
+            const int s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD)
+                                 ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NF : 0);
             s->staged_smem = s->sinfo.smem_bytes + 8 * ((s_ch * s->sinfo.tile_y * 32 + 31) / 32 * 32);
             int maxsm = 0;
             cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device);
@@ -461,7 +501,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         return fail(PF_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
     }
     s->own_stream = true;
-    const int NL = gc.NL, NV = gc.NV;
+    const int NL = gc.NL, NF = gc.NF;
     const int64_t P = s->P, nzl = s->nzl;
     auto bail = [&](pf_status st2) {
         std::string msg = g_last_error;
@@ -475,15 +515,16 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     for (int i = 0; i < 2; ++i) {
         if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u")) != PF_OK)
             return bail(st);
-        if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * 3 * NV * P) * sizeof(float), "q")) != PF_OK)
+        if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * 3 * NF * P) * sizeof(float), "q")) != PF_OK)
             return bail(st);
         s->u[i] = s->u_alloc[i] + NL * P;
-        s->q[i] = s->q_alloc[i] + (int64_t)3 * NV * P;
+        s->q[i] = s->q_alloc[i] + (int64_t)3 * NF * P;
     }
     const int64_t nzD = std::min(z1 + 1, dims->nz) - z0;  // owned + static halo plane above
     if ((st = alloc(s, (void **)&s->D_alloc, (size_t)((nzl + 1) * NL * P) * sizeof(float), "D")) != PF_OK)
         return bail(st);
-    const int64_t nS = S->kind == PF_S_SHARED_FIELD ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? NV : 0);
+    const int64_t nS = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD)
+                           ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? NF : 0);
     if (nS > 0 && (st = alloc(s, (void **)&s->S_alloc, (size_t)(nzl * nS * P) * sizeof(float), "S")) != PF_OK)
         return bail(st);
     if ((st = alloc(s, (void **)&s->d_resid, 64, "resid")) != PF_OK) return bail(st);
@@ -502,20 +543,22 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         e = cudaMemsetAsync(s->S_alloc, 0, (size_t)(nzl * nS * P) * sizeof(float), s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "zero S"); return bail(PF_ERR_CUDA); }
     }
-    if (S->kind == PF_S_SHARED_FIELD) {
+    if (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD) {
         if (!S->fields[0]) return bail(fail(PF_ERR_INVALID, "smoothness: fields[0] is NULL"));
+        for (int p = 0; p < NF; ++p)  // per-node factor of the shared field
+            s->gc.g.s[p] = S->kind == PF_S_SHARED_FIELD ? 1.f : S->scalars[gc.node_of_pos[p]];
         e = copy_volume(true, s->S_alloc, 1, (float *)S->fields[0], s->nx, s->ny, s->pitch, nzl, s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
     } else if (S->kind == PF_S_FIELD_PER_NODE) {
-        for (int p = 0; p < NV; ++p) {
+        for (int p = 0; p < NF; ++p) {
             const int v = gc.node_of_pos[p];
             if (!S->fields[v - 1]) return bail(fail(PF_ERR_INVALID, "smoothness: fields[%d] is NULL", v - 1));
-            e = copy_volume(true, s->S_alloc + p * P, NV, (float *)S->fields[v - 1], s->nx, s->ny, s->pitch, nzl,
+            e = copy_volume(true, s->S_alloc + p * P, NF, (float *)S->fields[v - 1], s->nx, s->ny, s->pitch, nzl,
                             s->stream);
             if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
         }
     } else {
-        for (int p = 0; p < NV; ++p) s->gc.g.s[p] = S->scalars[gc.node_of_pos[p]];
+        for (int p = 0; p < NF; ++p) s->gc.g.s[p] = S->scalars[gc.node_of_pos[p]];
     }
     if (nS > 0) {
         cudaMemsetAsync(s->d_flag, 0, 4, s->stream);
@@ -541,23 +584,24 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     }
     if (s->staged) {
         const int ty = s->sinfo.tile_y;
-        s->s_ch = S->kind == PF_S_SHARED_FIELD ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? NV : 0);
+        s->s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD) ? 1
+                                                                                   : (S->kind == PF_S_FIELD_PER_NODE ? NF : 0);
         bool ok = true;
         for (int i = 0; i < 2; ++i) {
-            ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NV, nzl + 2, 40,
-                                ty + 2, 3 * NV);
+            ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 40,
+                                ty + 2, 3 * NF);
             ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, NL);
         }
         for (int i = 0; i < 2; ++i) {
-            ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NV, nzl + 2, 32, ty,
-                                3 * NV);
+            ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 32, ty,
+                                3 * NF);
             ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, NL);
         }
         ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
         if (s->s_ch) ok = ok && encode4d(&s->tm_S, s->S_alloc, s->nx, s->ny, s->pitch, s->s_ch, nzl, 32, ty, s->s_ch);
         else memset(&s->tm_S, 0, sizeof(s->tm_S));
         if (!ok) return bail(fail(PF_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
-        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * NV + 2 * 36 * (ty + 1) * NL + 32 * ty * s->s_ch));
+        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * NF + 2 * 36 * (ty + 1) * NL + 32 * ty * s->s_ch));
     }
     choose_chunking(s);
     e = cudaStreamSynchronize(s->stream);
@@ -602,7 +646,7 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     a.zg0 = (int)s->z0;
     a.nzg = (int)s->nz;
     a.zchunk = s->zchunk;
-    a.s_kind = s->s_kind;
+    a.s_kind = s->s_kind == PF_S_SCALED_FIELD ? 1 : s->s_kind;
     a.cap = s->cfg.cap;
     a.shift = s->cfg.shift;
     a.inv_c = 1.0f / s->cfg.c;
@@ -716,14 +760,18 @@ pf_status pf_get_flows(pf_solver *s, float *q) {
     if (st != PF_OK) return st;
     if (!q) return fail(PF_ERR_INVALID, "q is NULL");
     DeviceGuard dg(s->device);
-    const int NV = s->gc.NV, nd = s->ndim;
+    const int NV = s->gc.NV, NF = s->gc.NF, nd = s->ndim;
     const int64_t P = s->P, nzl = s->nzl;
     const int64_t V = s->nx * s->ny * nzl;
     for (int p = 0; p < NV; ++p) {
         const int v = s->gc.node_of_pos[p];
         for (int k = 0; k < nd; ++k) {
             float *dst = q + ((int64_t)(v - 1) * nd + k) * V;
-            CK(copy_volume(false, s->q[s->cur] + ((int64_t)k * NV + p) * P, (int64_t)3 * NV, dst, s->nx, s->ny, s->pitch,
+            if (p >= NF) {  // node without a stored flow (Ishikawa end labels): identically 0
+                CK(cudaMemsetAsync(dst, 0, (size_t)V * sizeof(float), s->stream), "zero flows");
+                continue;
+            }
+            CK(copy_volume(false, s->q[s->cur] + ((int64_t)k * NF + p) * P, (int64_t)3 * NF, dst, s->nx, s->ny, s->pitch,
                            nzl, s->stream),
                "download q");
         }
@@ -751,7 +799,9 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
     a.NI = s->gc.NI;
     a.NL = s->gc.NL;
     a.NV = s->gc.NV;
-    a.s_kind = s->s_kind;
+    a.NF = s->gc.NF;
+    a.model = s->gc.model;
+    a.s_kind = s->s_kind == PF_S_SCALED_FIELD ? 1 : s->s_kind;
     a.cap = s->cfg.cap;
     a.g = s->gc.g;
     CK(launch_energy(a, s->d_energy + 2, kEnergyBlocks, s->d_energy, s->stream), "energy kernel");
@@ -775,7 +825,7 @@ pf_status pf_halo_regions(pf_solver *s, pf_halo *h) {
     if (st != PF_OK) return st;
     if (!h) return fail(PF_ERR_INVALID, "h is NULL");
     memset(h, 0, sizeof(*h));
-    const int NV = s->gc.NV;
+    const int NV = s->gc.NF;  // flow-carrying nodes
     const int64_t P = s->P, nzl = s->nzl;
     float *u = s->u[s->cur], *q = s->q[s->cur];
     h->bytes_u = ups(s) * (int64_t)sizeof(float);
@@ -802,7 +852,7 @@ pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n) {
     }
     for (int i = 0; i + 1 < n; ++i) {
         pf_solver *lo = solvers[i], *hi = solvers[i + 1];
-        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->gc.NV != hi->gc.NV)
+        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->gc.NF != hi->gc.NF)
             return fail(PF_ERR_INVALID, "exchange: solvers %d and %d are not consecutive slabs of one volume", i, i + 1);
     }
     // order: every receiver waits for every sender's pending work, copies on the receiver's stream,
@@ -867,13 +917,17 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     // algorithmic bytes per iteration: per end label u r/w + D r + q r/w,
     // per internal node q r/w, plus the capacity fields
     const int64_t V = s->nx * s->ny * s->nzl;
-    const int64_t per_leaf = 4 + 4 + 4 + 8 * s->ndim, per_int = 8 * s->ndim;
-    int64_t b = V * (per_leaf * s->gc.NL + per_int * s->gc.NI);
-    if (s->s_kind == PF_S_SHARED_FIELD) b += 4 * V;
-    if (s->s_kind == PF_S_FIELD_PER_NODE) b += 4 * V * s->gc.NV;
+    // per end label: u r/w + D r (+ its flow r/w unless it carries none); per flow-carrying internal node:
+    // its flow r/w
+    const int64_t per_leaf = 4 + 4 + 4, per_flow = 8 * s->ndim;
+    int64_t b = V * (per_leaf * s->gc.NL + per_flow * s->gc.NF);
+    if (s->s_kind == PF_S_SHARED_FIELD || s->s_kind == PF_S_SCALED_FIELD) b += 4 * V;
+    if (s->s_kind == PF_S_FIELD_PER_NODE) b += 4 * V * s->gc.NF;
     info->algorithmic_bytes_per_iteration = b;
     info->device_bytes = s->device_bytes;
     info->kernel_launches = s->launches;
+    info->model = s->gc.model;
+    info->flow_nodes = s->gc.NF;
     return PF_OK;
 }
 

@@ -50,9 +50,18 @@ struct NodeVals {
 };
 
 __device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, int64_t P, float *out) {
-    // u_v for every position: end labels read, internal by bottom-up sums (Eq. 9)
+    // u_v for every position: end labels read, internal by bottom-up sums (Eq. 9);
+    // Ishikawa chain: u_{N_i} = sum_{j >= i} u_{L_j}
     const int NV = a.NV, NI = a.NI;
     for (int l = 0; l < a.NL; ++l) out[NI + l] = ub[l * P];
+    if (a.model == 1) {
+        double acc = 0.0;
+        for (int f = NI - 1; f >= 0; --f) {
+            acc += (double)out[NI + f + 1];
+            out[f] = (float)acc;
+        }
+        return;
+    }
     for (int i = NI - 1; i >= 0; --i) {
         double acc = 0.0;
         for (int j = i + 1; j < NV; ++j) acc += (double)a.g.w[i][j] * out[j];
@@ -63,8 +72,8 @@ __device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, 
 __global__ void energy_kernel(const EnergyArgs a, double *partial) {
     const int64_t P = (int64_t)a.pitch * a.ny;
     const int64_t V = (int64_t)a.nx * a.ny * a.nzl;
-    const int NV = a.NV, NI = a.NI, NL = a.NL;
-    const int64_t ups = (int64_t)NL * P, qps = (int64_t)a.ndim * NV * P;
+    const int NV = a.NV, NI = a.NI, NL = a.NL, NF = a.NF;
+    const int64_t ups = (int64_t)NL * P, qps = (int64_t)3 * NF * P;
     double e_acc = 0.0, f_acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = i / ((int64_t)a.nx * a.ny);
@@ -73,10 +82,10 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
         const int64_t pix = (int64_t)y * a.pitch + x;
         const int64_t zg = a.zg0 + z;
         // ---- primal: sum_L D_L u_L + sum_v S_v |nabla u_v|
-        float uc[kMaxNodes], un[kMaxNodes];
+        float uc[2 * kMaxNodes], un[2 * kMaxNodes];
         labels_at(a, a.u + z * ups + pix, P, uc);
         for (int l = 0; l < NL; ++l) e_acc += (double)a.D[z * ups + l * P + pix] * (double)uc[NI + l];
-        double g2[kMaxNodes], g1[kMaxNodes];
+        double g2[2 * kMaxNodes], g1[2 * kMaxNodes];
         for (int v = 0; v < NV; ++v) { g2[v] = 0.0; g1[v] = 0.0; }
         if (x < a.nx - 1) {
             labels_at(a, a.u + z * ups + pix + 1, P, un);
@@ -90,26 +99,37 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
             labels_at(a, a.u + (z + 1) * ups + pix, P, un);
             for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
         }
-        for (int v = 0; v < NV; ++v) {
+        for (int v = 0; v < NF; ++v) {  // nodes without a flow have zero capacity
             float sv;
             if (a.s_kind == 0) sv = a.g.s[v];
-            else if (a.s_kind == 1) sv = a.S[z * P + pix];
-            else sv = a.S[(z * NV + v) * P + pix];
+            else if (a.s_kind == 1) sv = a.S[z * P + pix] * a.g.s[v];
+            else sv = a.S[(z * NF + v) * P + pix];
             e_acc += (double)sv * (a.cap == 0 ? sqrt(g2[v]) : g1[v]);
         }
         // ---- dual: min over end labels of d_L
-        double d[kMaxNodes];
+        double d[2 * kMaxNodes];
         const float *qb = a.q + z * qps + pix;
         for (int v = 0; v < NV; ++v) {
-            double dv = (double)qb[v * P] - (x > 0 ? (double)qb[v * P - 1] : 0.0);
-            dv += (double)qb[(NV + v) * P] - (y > 0 ? (double)qb[(NV + v) * P - a.pitch] : 0.0);
-            if (a.ndim == 3)
-                dv += (double)qb[(2 * NV + v) * P] - (zg > 0 ? (double)qb[(2 * NV + v) * P - qps] : 0.0);
+            double dv = 0.0;
+            if (v < NF) {
+                dv = (double)qb[v * P] - (x > 0 ? (double)qb[v * P - 1] : 0.0);
+                dv += (double)qb[(NF + v) * P] - (y > 0 ? (double)qb[(NF + v) * P - a.pitch] : 0.0);
+                if (a.ndim == 3)
+                    dv += (double)qb[(2 * NF + v) * P] - (zg > 0 ? (double)qb[(2 * NF + v) * P - qps] : 0.0);
+            }
             d[v] = dv;
         }
         for (int l = 0; l < NL; ++l) d[NI + l] += (double)a.D[z * ups + l * P + pix];
-        for (int ii = 0; ii < NI; ++ii)
-            for (int j = ii + 1; j < NV; ++j) d[j] += (double)a.g.w[ii][j] * d[ii];
+        if (a.model == 1) {  // prefix: d_{L_i} += sum_{j <= i} div q_j
+            double run = 0.0;
+            for (int i = 1; i < NL; ++i) {
+                run += d[i - 1];
+                d[NI + i] += run;
+            }
+        } else {
+            for (int ii = 0; ii < NI; ++ii)
+                for (int j = ii + 1; j < NV; ++j) d[j] += (double)a.g.w[ii][j] * d[ii];
+        }
         double mn = d[NI];
         for (int l = 1; l < NL; ++l) mn = fmin(mn, d[NI + l]);
         f_acc += mn;

@@ -14,6 +14,8 @@ struct EnergyArgs {
     const float *S;
     int nx, ny, pitch, nzl, zg0, nzg, ndim;
     int NI, NL, NV;
+    int NF;      // flow-carrying nodes (positions 0..NF-1)
+    int model;   // 0: DAG (dense weights), 1: Ishikawa chain
     int s_kind, cap;
     GraphConst g;
 };

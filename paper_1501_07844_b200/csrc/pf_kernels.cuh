@@ -69,18 +69,17 @@ struct IterArgs {
 
 __device__ __forceinline__ float ldg(const float *p) { return __ldg(p); }
 
-template <int NI, int NL, int TY>
+template <int NI, int NL, int TY, int MODEL>
 struct IterSmem {
-    static constexpr int NV = NI + NL;
+    static constexpr int NV = Model<MODEL, NI, NL>::NF;
     static constexpr int kPlane = NV * (TY + 1) * (kTX + 1);
     static constexpr int kBytes = 3 * kPlane * (int)sizeof(float);
 };
 
-template <int NI, int NL, int TY, int CAP>
+template <int NV /* flow nodes */, int TY, int CAP>
 __device__ __forceinline__ void flow_out_global(const IterArgs &a, const float *Mz, const float *Mp, bool has_z,
                                                 int sme, int x, int y, int zg, int64_t P, const float *qb, float *qo,
                                                 const float *Sb) {
-    constexpr int NV = NI + NL;
     constexpr int RS = kTX + 1, PS = (TY + 1) * RS;
     const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
     const int Pi = (int)P;  // channel stride fits 32 bits (an x-y plane has < 2^31 / 48 voxels)
@@ -91,7 +90,7 @@ __device__ __forceinline__ void flow_out_global(const IterArgs &a, const float *
         const float gy = gyv ? Mz[v * PS + sme + RS] - mc : 0.f;
         const float gz = gzv ? Mp[v * PS + sme] - mc : 0.f;
         float hx = ldg(qb + v * P), hy = ldg(qb + (NV + v) * P), hz = ldg(qb + (2 * NV + v) * P);
-        const float sv = a.s_kind == 0 ? a.g.s[v] : (a.s_kind == 1 ? ldg(Sb) : ldg(Sb + v * P));
+        const float sv = a.s_kind == 0 ? a.g.s[v] : (a.s_kind == 1 ? ldg(Sb) * a.g.s[v] : ldg(Sb + v * P));
         flow_step<CAP>(a.ctau, gx, gy, gz, sv, hx, hy, hz);
         st_stream(qo + v * Pi, hx);
         st_stream(qo + (NV + v) * Pi, hy);
@@ -99,9 +98,9 @@ __device__ __forceinline__ void flow_out_global(const IterArgs &a, const float *
     }
 }
 
-template <int NI, int NL, int TY>
+template <int NI, int NL, int TY, int MODEL>
 __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a) {
-    constexpr int NV = NI + NL;
+    constexpr int NV = Model<MODEL, NI, NL>::NF;  // node loops run over the flow-carrying nodes
     constexpr int RS = kTX + 1;              // smem row stride
     constexpr int PS = (TY + 1) * RS;        // smem per-node plane stride
     constexpr int RING = NV * PS;            // smem per ring slot
@@ -146,7 +145,7 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
         // ---------------- stage A: masses of plane p (tile + halo)
         if (active) {
             const float *qb = a.q_in + (int64_t)p * qps + pix;
-            float d[NV];
+            float dq[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const float qx = ldg(qb + v * P);
@@ -154,13 +153,14 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
                 const float qy = ldg(qb + (NV + v) * P);
                 const float qym = (y > 0) ? ldg(qb + (NV + v) * P - a.pitch) : 0.f;
                 const float qz = ldg(qb + (2 * NV + v) * P);
-                d[v] = ((qx - qxm) + (qy - qym)) + (qz - qzp[v]);
+                dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qzp[v]);
                 qzp[v] = qz;
             }
             const float *Db = a.D + (int64_t)p * ups + pix;
+            float Dv[NL], d[NI + NL];
 #pragma unroll
-            for (int l = 0; l < NL; ++l) d[NI + l] = ldg(Db + l * P) + d[NI + l];
-            push_down<NI, NV>(d, a.g.w);
+            for (int l = 0; l < NL; ++l) Dv[l] = ldg(Db + l * P);
+            label_excess<MODEL, NI, NL>(dq, Dv, d, a.g.w);
             const float *ub = a.u_in + (int64_t)p * ups + pix;
             float uold[NL], ut[NL], un[NL];
 #pragma unroll
@@ -179,9 +179,7 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
                 }
             }
             float M[NV];
-#pragma unroll
-            for (int l = 0; l < NL; ++l) M[NI + l] = ut[l];
-            push_up<NI, NV>(M, a.g.w);
+            node_masses<MODEL, NI, NL>(ut, M, a.g.w);
 #pragma unroll
             for (int v = 0; v < NV; ++v) Mp[v * PS + sme] = M[v];
         }
@@ -193,8 +191,8 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
             const float *qb = a.q_in + (int64_t)z * qps + pix;
             float *qo = a.q_out + (int64_t)z * qps + pix;
             const float *Sb = a.S ? a.S + (int64_t)z * (a.s_kind == 1 ? 1 : NV) * P + pix : nullptr;
-            if (a.cap == 0) flow_out_global<NI, NL, TY, 0>(a, Mz, Mp, true, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
-            else flow_out_global<NI, NL, TY, 1>(a, Mz, Mp, true, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
+            if (a.cap == 0) flow_out_global<NV, TY, 0>(a, Mz, Mp, true, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
+            else flow_out_global<NV, TY, 1>(a, Mz, Mp, true, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
         }
     }
     // last plane of the volume: no plane above, nabla_z = 0
@@ -204,8 +202,8 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
         const float *qb = a.q_in + (int64_t)z * qps + pix;
         float *qo = a.q_out + (int64_t)z * qps + pix;
         const float *Sb = a.S ? a.S + (int64_t)z * (a.s_kind == 1 ? 1 : NV) * P + pix : nullptr;
-        if (a.cap == 0) flow_out_global<NI, NL, TY, 0>(a, Mz, Mz, false, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
-        else flow_out_global<NI, NL, TY, 1>(a, Mz, Mz, false, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
+        if (a.cap == 0) flow_out_global<NV, TY, 0>(a, Mz, Mz, false, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
+        else flow_out_global<NV, TY, 1>(a, Mz, Mz, false, sme, x, y, a.zg0 + z, P, qb, qo, Sb);
     }
     if (a.check) {
 #pragma unroll
@@ -222,6 +220,6 @@ struct IterKernelInfo {
     int tile_y;
 };
 
-bool iter_kernel_lookup(int NI, int NL, IterKernelInfo *info);
+bool iter_kernel_lookup(int NI, int NL, int MODEL, IterKernelInfo *info);
 
 }  // namespace pf

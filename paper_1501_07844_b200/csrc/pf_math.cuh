@@ -72,6 +72,55 @@ __device__ __forceinline__ void push_up(float (&M)[NV], const float (&w)[kMaxInt
     }
 }
 
+// Label models.  MODEL 0: general DAG (Potts = star, HMF = tree), every non-source node carries a flow,
+// positions 0..NI-1 internal (topological order), NI..NI+NL-1 end labels.  MODEL 1: Ishikawa chain
+// (Alg. 3): NI = N level nodes carry the flows q_1..q_N, the NL = N+1 ordered labels carry none.
+template <int MODEL, int NI, int NL>
+struct Model {
+    static constexpr int NV = NI + NL;
+    static constexpr int NF = MODEL == 1 ? NI : NV;   // nodes with a spatial flow
+};
+
+// End-label excesses from the flow divergences dq and data terms Dv into dlab[NI + l].
+//   MODEL 0: d_v = div q_v; d_L += D_L; top-down pushes
+//   MODEL 1: d_0 = D_0; d_i = (d_{i-1} + div q_i) + D_i (prefix)
+template <int MODEL, int NI, int NL>
+__device__ __forceinline__ void label_excess(const float (&dq)[Model<MODEL, NI, NL>::NF], const float (&Dv)[NL],
+                                             float (&dlab)[NI + NL], const float (&w)[kMaxInternal][kMaxNodes]) {
+    if constexpr (MODEL == 0) {
+#pragma unroll
+        for (int v = 0; v < NI + NL; ++v) dlab[v] = dq[v];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) dlab[NI + l] = Dv[l] + dlab[NI + l];
+        push_down<NI, NI + NL>(dlab, w);
+    } else {
+        float run = 0.f;
+        dlab[NI] = Dv[0];
+#pragma unroll
+        for (int i = 1; i < NL; ++i) {
+            run = run + dq[i - 1];
+            dlab[NI + i] = run + Dv[i];
+        }
+    }
+}
+
+// Unnormalised masses M of the flow-carrying nodes from the end-label masses ut.
+//   MODEL 0: M_L = u~_L; bottom-up pushes
+//   MODEL 1: M_N = u~_N; M_i = u~_i + M_{i+1} (suffix)
+template <int MODEL, int NI, int NL>
+__device__ __forceinline__ void node_masses(const float (&ut)[NL], float (&M)[Model<MODEL, NI, NL>::NF],
+                                            const float (&w)[kMaxInternal][kMaxNodes]) {
+    if constexpr (MODEL == 0) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) M[NI + l] = ut[l];
+        push_up<NI, NI + NL>(M, w);
+    } else {
+        M[NI - 1] = ut[NL - 1];
+#pragma unroll
+        for (int f = NI - 2; f >= 0; --f) M[f] = ut[f + 1] + M[f + 1];
+    }
+}
+
 // Flow step + capacity projection of one node at one voxel (P:148 / P:298; Eq. 8 / Eq. 16; R5, R14):
 //   q^ = q - c tau nabla M;  q' = q^ if |q^| <= S else q^ S/|q^|  (CAP 0, l2)  |  clamp(q^, -S, S) (CAP 1).
 template <int CAP>

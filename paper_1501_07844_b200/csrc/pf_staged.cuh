@@ -21,18 +21,18 @@
 namespace pf {
 
 struct StagedArgs {
-    CUtensorMap tm_q;   // input q, 4-D (x, y, channel = k*NV+v, plane+1)
+    CUtensorMap tm_q;   // input q, 4-D (x, y, channel = k*NF+f, plane+1) over the NF flow-carrying nodes
     CUtensorMap tm_u;   // input u, 4-D (x, y, l, plane+1)
     CUtensorMap tm_D;   // D, 4-D (x, y, l, plane)
     CUtensorMap tm_S;   // S field, 4-D (x, y, channel, plane); unused when s_ch == 0
     CUtensorMap tm_uo;  // output u, store box (32, TY, NL)        [OSTAGE]
-    CUtensorMap tm_qo;  // output q, store box (32, TY, 3*NV)      [OSTAGE]
+    CUtensorMap tm_qo;  // output q, store box (32, TY, 3*NF)      [OSTAGE]
     const float *q_in;  // plane 0 of input q (chunk-start q^z(zc0-1) read)
     float *u_out;
     float *q_out;
     int nx, ny, pitch, nzl, zg0, nzg;
     int zchunk, tiles_x, tiles, items;
-    int s_ch;     // 0: scalar capacities, 1: shared field, NV: field per node
+    int s_ch;     // 0: scalar capacities, 1: shared field (x g.s[f]), NF: field per flow node
     int cap, shift, check;
     unsigned int tx_bytes;
     float inv_c, ctau;
@@ -43,18 +43,19 @@ struct StagedArgs {
 
 __host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 
-template <int NI, int NL, int TY, int OSTAGE>
+template <int NI, int NL, int TY, int OSTAGE, int MODEL>
 struct StagedLayout {
     static constexpr int NV = NI + NL;
+    static constexpr int NF = Model<MODEL, NI, NL>::NF;   // flow-carrying nodes
     static constexpr int QW = 40, UW = 36, SW = 32;
     static constexpr int QROWS = TY + 2, UROWS = TY + 1;
-    static constexpr int QSZ = round32(3 * NV * QROWS * QW);  // floats per stage
+    static constexpr int QSZ = round32(3 * NF * QROWS * QW);  // floats per stage
     static constexpr int USZ = round32(NL * UROWS * UW);
-    static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NV * RPS;
+    static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NF * RPS;
     static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // output staging (per buffer)
-    static constexpr int QOSZ = OSTAGE ? round32(3 * NV * TY * 32) : 0;
+    static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;
     static constexpr int kThreads = 32 * TY + 64;
-    // runtime part: the S staging ring holds s_ch channels (0, 1 or NV)
+    // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
     __host__ __device__ static constexpr int off_U() { return 2 * QSZ; }
     __host__ __device__ static constexpr int off_D() { return 2 * QSZ + 2 * USZ; }
@@ -66,7 +67,7 @@ struct StagedLayout {
     __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 16; }
 };
 
-template <int NV, int CAP, int OSTAGE, int TY>
+template <int NV /* flow nodes */, int CAP, int OSTAGE, int TY>
 __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int roff, int rps, int rs,
                                                 const float (&Mn)[NV], bool has_z, int x, int y, int zg,
                                                 const float (&qc)[3][NV], const float (&svc)[NV], float *qo,
@@ -93,10 +94,11 @@ __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float
     }
 }
 
-template <int NI, int NL, int TY, int OSTAGE>
+template <int NI, int NL, int TY, int OSTAGE, int MODEL>
 __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
-    using L = StagedLayout<NI, NL, TY, OSTAGE>;
-    constexpr int NV = L::NV, QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
+    using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL>;
+    constexpr int NV = L::NF;  // in this kernel "node" loops run over the flow-carrying nodes
+    constexpr int QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
     constexpr int QCS = QROWS * QW;   // q channel stride in smem
     constexpr int UCS = UROWS * UW;
     constexpr int RS = L::RS, RPS = L::RPS, RING = L::RING;
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             for (int v = 0; v < NV; ++v) svn[v] = 0.f;
             // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
             if (lx >= 0) {
-                float d[NV];
+                float dq[NV];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     const float qx = Qb[v * QCS + qoff];
@@ -197,12 +199,13 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
                     const float qy = Qb[(NV + v) * QCS + qoff];
                     const float qym = Qb[(NV + v) * QCS + qoff - QW];
                     const float qz = Qb[(2 * NV + v) * QCS + qoff];
-                    d[v] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
+                    dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
                     qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
                 }
+                float Dv[NL], d[NI + NL];
 #pragma unroll
-                for (int l = 0; l < NL; ++l) d[NI + l] = Db[l * UCS + uoff] + d[NI + l];
-                push_down<NI, NV>(d, a.g.w);
+                for (int l = 0; l < NL; ++l) Dv[l] = Db[l * UCS + uoff];
+                label_excess<MODEL, NI, NL>(dq, Dv, d, a.g.w);
                 float uold[NL], ut[NL], un[NL];
 #pragma unroll
                 for (int l = 0; l < NL; ++l) uold[l] = Ub[l * UCS + uoff];
@@ -224,9 +227,7 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
 #pragma unroll
                     for (int l = 0; l < NL; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                 }
-#pragma unroll
-                for (int l = 0; l < NL; ++l) Mv[NI + l] = ut[l];
-                push_up<NI, NV>(Mv, a.g.w);
+                node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) Rp[v * RPS + roff] = Mv[v];
                 if (is_main) {
@@ -234,10 +235,10 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
                     if (a.s_ch == 0) {
 #pragma unroll
                         for (int v = 0; v < NV; ++v) svn[v] = a.g.s[v];
-                    } else if (a.s_ch == 1) {
+                    } else if (a.s_ch == 1) {  // shared field x per-node multiplier (1 for a plain shared field)
                         const float sv = Sb[0];
 #pragma unroll
-                        for (int v = 0; v < NV; ++v) svn[v] = sv;
+                        for (int v = 0; v < NV; ++v) svn[v] = sv * a.g.s[v];
                     } else {
 #pragma unroll
                         for (int v = 0; v < NV; ++v) svn[v] = Sb[v * TY * SW];
@@ -327,6 +328,6 @@ struct StagedKernelInfo {
     int ostage;      // 1: outputs staged in smem and written by TMA stores
 };
 
-bool staged_kernel_lookup(int NI, int NL, StagedKernelInfo *info);
+bool staged_kernel_lookup(int NI, int NL, int MODEL, StagedKernelInfo *info);
 
 }  // namespace pf

@@ -5,7 +5,8 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
-from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD,
+from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SCALED_FIELD,
+               PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_get_energy, pf_get_flows, pf_get_kernel_info,
                pf_get_labeling, pf_halo_regions, pf_iterate, pf_iterations, pf_reset, pf_set_stream)
 
@@ -16,19 +17,22 @@ class Solver:
     graph = (num_nodes, parent, child, weight) with node 0 the source;
     D = one float32 [z][y][x] volume per end label (numpy or CUDA tensor) covering the
     slab plus the plane above it; capacities: exactly one of `s_scalars` ([num_nodes]),
-    `s_shared` (one volume) or `s_fields` (one volume per non-source node).
+    `s_shared` (one volume), `s_fields` (one volume per non-source node) or `s_scaled` =
+    (factors [num_nodes], volume): S_v(x) = factors[v] * volume(x).
     """
 
     def __init__(self, dims: Sequence[int], ndim: int, graph, D: Sequence, *, s_scalars=None, s_shared=None,
-                 s_fields=None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2, shift: int = PF_SHIFT_MIN,
-                 check_every: int = 10, slab: Optional[Sequence[int]] = None):
+                 s_fields=None, s_scaled=None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2,
+                 shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None):
         num_nodes, parent, child, weight = graph
         self.dims = tuple(int(v) for v in dims)
         self.ndim = ndim
         self.num_nodes = int(num_nodes)
         self.NL = len(D)
         self.slab = (0, self.dims[2]) if slab is None else (int(slab[0]), int(slab[1]))
-        if s_scalars is not None:
+        if s_scaled is not None:
+            kind, s_scalars, fields = PF_S_SCALED_FIELD, s_scaled[0], [s_scaled[1]]
+        elif s_scalars is not None:
             kind, fields = PF_S_SCALAR_PER_NODE, None
         elif s_shared is not None:
             kind, fields = PF_S_SHARED_FIELD, [s_shared]

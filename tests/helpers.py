@@ -16,7 +16,11 @@ def solver_from_inputs(inp, shift=0, cap=None, check_every=10, slab=None, c=None
     wz0 = inp.window[0]
     D = [np.ascontiguousarray(inp.D[l, z0 - wz0:zt - wz0]) for l in range(inp.D.shape[0])]
     kw = {}
-    if inp.s_kind == "shared_field":
+    if cfg.kind == "ishikawa":   # level nodes carry the shared field, end labels no flow (factor 0)
+        factors = np.zeros(g.num_nodes, np.float32)
+        factors[1:len(D)] = 1.0
+        kw["s_scaled"] = (factors, np.ascontiguousarray(inp.s_field[z0 - wz0:z1 - wz0]))
+    elif inp.s_kind == "shared_field":
         kw["s_shared"] = np.ascontiguousarray(inp.s_field[z0 - wz0:z1 - wz0])
     elif inp.s_kind == "field_per_node":
         kw["s_fields"] = [np.ascontiguousarray(f[z0 - wz0:z1 - wz0]) for f in inp.s_fields()[1:]]
@@ -28,6 +32,8 @@ def solver_from_inputs(inp, shift=0, cap=None, check_every=10, slab=None, c=None
         for k in ("s_shared",):
             if k in kw:
                 kw[k] = torch.from_numpy(kw[k]).cuda()
+        if "s_scaled" in kw:
+            kw["s_scaled"] = (kw["s_scaled"][0], torch.from_numpy(kw["s_scaled"][1]).cuda())
     cap = CAP[cfg.cap] if cap is None else cap
     return pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.child, g.weight), D,
                      c=cfg.c if c is None else c, tau=cfg.tau if tau is None else tau, cap=cap, shift=shift,

@@ -29,7 +29,7 @@ def _cfg(name):
     return P.config("C5").resized(768, 768, 96, name="C5slab") if name == "C5slab" else P.config(name)
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5slab"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5slab", "I2"])
 def test_fullsize_sampled_parity(name):
     cfg = _cfg(name)
     inp = P.generate(cfg)

@@ -53,8 +53,10 @@ def test_c1_every_iteration(shift):
     ("C3", (48, 40, 36), 300, O.SHIFT_MIN),
     ("C3", (33, 17, 9), 300, O.SHIFT_NONE),
     ("C4", (40, 40, 40), 300, O.SHIFT_MIN),
-    ("C4", (35, 70, 21), 120, O.SHIFT_NONE),
+    ("C4", (35, 70, 21), 80, O.SHIFT_NONE),      # literal listing on this DAG: fp32 vs fp64 separate after ~90 it (tools/fp32_sensitivity.py)
     ("C5", (40, 36, 24), 200, O.SHIFT_MIN),      # K = 16
+    ("I2", (48, 40, 36), 300, O.SHIFT_MIN),      # Ishikawa, 7 levels (Alg. 3)
+    ("I2", (37, 29, 19), 300, O.SHIFT_NONE),
 ])
 def test_configs_scaled(name, dims, n, shift):
     inp = P.generate(P.config(name).resized(*dims))
@@ -156,7 +158,7 @@ def test_residual_matches_state_difference():
 def test_energies_match_oracle_and_weak_duality():
     """Device energies (fp64 accumulation) of the GPU state vs the oracle energies of the oracle state."""
     from oracle import energy as E
-    for name, dims in (("C2", (30, 28, 26)), ("C4", (26, 24, 22)), ("C1", (64, 64, 1))):
+    for name, dims in (("C2", (30, 28, 26)), ("C4", (26, 24, 22)), ("C1", (64, 64, 1)), ("I2", (27, 25, 23))):
         inp = P.generate(P.config(name).resized(*dims))
         g = inp.graph
         s = solver_from_inputs(inp)
@@ -223,3 +225,31 @@ def test_staged_and_global_kernels_bitwise_equal(monkeypatch):
             out[kv] = (s.labeling()[0], s.flows())
             s.close()
         assert np.array_equal(out["staged"][0], out["global"][0]) and np.array_equal(out["staged"][1], out["global"][1])
+
+
+@pytest.mark.parametrize("N", [1, 3, 7, 15])
+def test_ishikawa_kernels(N):
+    """The Ishikawa chain runs the dedicated Alg. 3 kernels (model 1, flows on the N level nodes only)."""
+    cfg = P.Config("ish", 3, 45, 33, 21, "ishikawa", N + 1, 12, 0.15, "sq", "edge", 0.05, 0, seed=40 + N)
+    inp = P.generate(cfg)
+    s = solver_from_inputs(inp)
+    info = s.kernel_info()
+    assert info["model"] == 1 and info["flow_nodes"] == N
+    s.iterate(120)
+    u, _ = s.labeling()
+    q = s.flows()
+    s.close()
+    assert np.all(q[N:] == 0)
+    ur, qr = O.run_inputs(inp, 120)
+    compare(u, q, ur, qr)
+
+
+def test_ishikawa_chain_with_flowing_labels_uses_dag_kernel():
+    """The same chain with non-zero end-label capacities is a general DAG (Alg. 2): model 0."""
+    import paper_1501_07844_b200 as pf
+    g = P.ishikawa_graph(3)
+    D = [np.random.default_rng(1).uniform(size=(5, 6, 7)).astype(np.float32) for _ in range(4)]
+    s = pf.Solver((7, 6, 5), 3, (g.num_nodes, g.parent, g.child, g.weight), D,
+                  s_scalars=np.full(g.num_nodes, 0.05, np.float32))
+    assert s.kernel_info()["model"] == 0
+    s.close()
