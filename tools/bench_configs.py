@@ -28,7 +28,7 @@ def cfg_of(name):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5slab"])
+    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5slab", "I2"])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--oracle", action="store_true")
     args = ap.parse_args()
@@ -40,8 +40,14 @@ def main():
         inp = P.generate(cfg)
         g = inp.graph
         D = [torch.from_numpy(np.ascontiguousarray(inp.D[l])).to(dev) for l in range(inp.D.shape[0])]
-        kw = {"s_shared": torch.from_numpy(inp.s_field).to(dev)} if inp.s_kind == "shared_field" else \
-            {"s_scalars": inp.s_scalars}
+        if cfg.kind == "ishikawa":
+            fac = np.zeros(g.num_nodes, np.float32)
+            fac[1:len(D)] = 1.0
+            kw = {"s_scaled": (fac, torch.from_numpy(inp.s_field).to(dev))}
+        elif inp.s_kind == "shared_field":
+            kw = {"s_shared": torch.from_numpy(inp.s_field).to(dev)}
+        else:
+            kw = {"s_scalars": inp.s_scalars}
         s = pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.child, g.weight), D, c=cfg.c,
                       tau=cfg.tau, check_every=10, **kw)
         stream = torch.cuda.current_stream(dev)

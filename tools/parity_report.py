@@ -68,8 +68,8 @@ def sampled_case(name, n=6):
 if __name__ == "__main__":
     cases = [("C1", None, 200, 0), ("C1", None, 200, 1), ("C2", (64, 64, 64), 300, 0), ("C2", (67, 45, 37), 300, 1),
              ("C3", (48, 40, 36), 300, 0), ("C4", (40, 40, 40), 300, 0), ("C4", (35, 70, 21), 80, 1),
-             ("C5", (40, 36, 24), 200, 0)]
+             ("C5", (40, 36, 24), 200, 0), ("I2", (48, 40, 36), 300, 0), ("I2", (37, 29, 19), 300, 1)]
     for c in cases:
         print(json.dumps(full_case(*c)), flush=True)
-    for name in ("C2", "C3", "C4", "C5slab"):
+    for name in ("C2", "C3", "C4", "C5slab", "I2"):
         print(json.dumps(sampled_case(name)), flush=True)
