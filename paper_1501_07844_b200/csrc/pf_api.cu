@@ -242,6 +242,7 @@ namespace {
 
 pf_status cuda_fail(pf_solver *s, cudaError_t e, const char *what) {
     if (s) s->poisoned = true;
+    cudaGetLastError();  // clear the (non-sticky) last-error state so it does not leak into other solvers
     return fail(PF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
@@ -768,7 +769,10 @@ pf_status pf_get_flows(pf_solver *s, float *q) {
         for (int k = 0; k < nd; ++k) {
             float *dst = q + ((int64_t)(v - 1) * nd + k) * V;
             if (p >= NF) {  // node without a stored flow (Ishikawa end labels): identically 0
-                CK(cudaMemsetAsync(dst, 0, (size_t)V * sizeof(float), s->stream), "zero flows");
+                if (is_device_ptr(dst))
+                    CK(cudaMemsetAsync(dst, 0, (size_t)V * sizeof(float), s->stream), "zero flows");
+                else
+                    memset(dst, 0, (size_t)V * sizeof(float));
                 continue;
             }
             CK(copy_volume(false, s->q[s->cur] + ((int64_t)k * NF + p) * P, (int64_t)3 * NF, dst, s->nx, s->ny, s->pitch,
