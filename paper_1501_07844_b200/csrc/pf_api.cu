@@ -256,26 +256,42 @@ int64_t ups(const pf_solver *s) { return (int64_t)s->gc.NL * s->P; }
 // q always carries 3 components internally (q^z == 0 for 2-D volumes), so the kernels need no ndim branch
 int64_t qps(const pf_solver *s) { return (int64_t)3 * s->gc.NF * s->P; }
 
-void free_all(pf_solver *s) {
-    for (int i = 0; i < 2; ++i) {
-        if (s->u_alloc[i]) cudaFree(s->u_alloc[i]);
-        if (s->q_alloc[i]) cudaFree(s->q_alloc[i]);
-        s->u_alloc[i] = s->q_alloc[i] = nullptr;
+// Device memory comes from the device's stream-ordered pool, which keeps up to kPoolKeep bytes of freed
+// memory for reuse: a solver created right after another one was destroyed (the end-to-end
+// create / iterate / get_labeling / destroy cycle) does not pay cudaMalloc / cudaFree again.
+constexpr uint64_t kPoolKeep = 64ull << 30;
+
+void pool_setup(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = kPoolKeep;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-    if (s->D_alloc) cudaFree(s->D_alloc);
-    if (s->S_alloc) cudaFree(s->S_alloc);
-    if (s->d_resid) cudaFree(s->d_resid);
-    if (s->d_err) cudaFree(s->d_err);
-    if (s->d_flag) cudaFree(s->d_flag);
-    if (s->d_energy) cudaFree(s->d_energy);
+    cudaGetLastError();
+    done[dev] = true;
+}
+
+void free_all(pf_solver *s) {
+    void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc,
+                    s->d_resid, s->d_err, s->d_flag, s->d_energy};
+    for (void *p : ptrs)
+        if (p) cudaFreeAsync(p, s->stream);
+    cudaGetLastError();
+    for (int i = 0; i < 2; ++i) s->u_alloc[i] = s->q_alloc[i] = nullptr;
     s->D_alloc = s->S_alloc = nullptr;
+    s->d_resid = nullptr;
+    s->d_err = nullptr;
+    s->d_flag = nullptr;
+    s->d_energy = nullptr;
 }
 
 pf_status alloc(pf_solver *s, void **p, size_t bytes, const char *what) {
-    cudaError_t e = cudaMalloc(p, bytes);
+    cudaError_t e = cudaMallocAsync(p, bytes, s->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        return fail(PF_ERR_OOM, "cudaMalloc(%zu bytes) for %s failed: %s", bytes, what, cudaGetErrorString(e));
+        return fail(PF_ERR_OOM, "cudaMallocAsync(%zu bytes) for %s failed: %s", bytes, what, cudaGetErrorString(e));
     }
     s->device_bytes += (int64_t)bytes;
     return PF_OK;
@@ -502,11 +518,13 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         return fail(PF_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
     }
     s->own_stream = true;
+    pool_setup(s->device);
     const int NL = gc.NL, NF = gc.NF;
     const int64_t P = s->P, nzl = s->nzl;
     auto bail = [&](pf_status st2) {
         std::string msg = g_last_error;
         free_all(s);
+        cudaStreamSynchronize(s->stream);
         if (s->own_stream) cudaStreamDestroy(s->stream);
         delete s;
         g_last_error = msg;
@@ -938,8 +956,8 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
 void pf_destroy(pf_solver *s) {
     if (!s) return;
     DeviceGuard dg(s->device);
-    if (s->stream) cudaStreamSynchronize(s->stream);
     free_all(s);
+    if (s->stream) cudaStreamSynchronize(s->stream);
     if (s->own_stream) cudaStreamDestroy(s->stream);
     delete s;
 }

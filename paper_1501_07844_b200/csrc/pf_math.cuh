@@ -36,12 +36,17 @@ __device__ __forceinline__ float label_update(const float (&d)[NI + NL], const f
 #pragma unroll
         for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
     }
-    float sum = 0.f;
+    // a = (sum of the first NL/2 masses) + (sum of the rest): the order a label-split kernel (two warps per
+    // voxel row, pf_staged.cuh G = 2) also uses, so every variant rounds identically
+    constexpr int H = NL / 2;
+    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
         ut[l] = uold[l] * ex2_approx((m - d[NI + l]) * k2);
-        sum += ut[l];
+        if (l < H) s0 += ut[l];
+        else s1 += ut[l];
     }
+    const float sum = s0 + s1;
     const float inv = __frcp_rn(sum);
 #pragma unroll
     for (int l = 0; l < NL; ++l) {

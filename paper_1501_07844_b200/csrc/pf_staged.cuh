@@ -1,7 +1,8 @@
 // pf_staged.cuh -- TMA-staged, persistent version of the fused pseudo-flow iteration (sm_100a).
 //
 // Same arithmetic and same per-voxel order as pf_iter_kernel (see pf_kernels.cuh for the
-// step-by-step mapping to Alg. 1 / Alg. 2), different data movement:
+// step-by-step mapping to Alg. 1 / Alg. 2 / Alg. 3; the shared math is in pf_math.cuh), different
+// data movement:
 //   * persistent CTAs (one per SM) walk work items = (32 x TY tile, z-chunk) in a static
 //     round-robin order, so the tiles in flight at any time are spatial neighbours and their
 //     shared halo lines are served from L2;
@@ -11,7 +12,13 @@
 //     points), u and D over [x0, x0+36) x [y0, y0+TY], S over the tile.  Out-of-range box
 //     elements are zero-filled by the TMA unit, which is exactly q^k(-1) = 0 (reading R4);
 //   * plane p+2 is in flight while plane p is computed; q(p) and S(p) of the own voxel are kept
-//     in registers until the flow step of plane p runs one plane later.
+//     in registers (two alternating sets) until the flow step of plane p runs one plane later;
+//   * OSTAGE: the new u and q are staged in shared memory and written by TMA bulk-tensor stores
+//     with an evict-first L2 policy (no per-thread 64-bit address arithmetic, no L2 pollution);
+//   * G = 2 (Potts with many labels): the labels of a row of 32 voxels are split over a warp pair;
+//     the only per-voxel couplings of the label update -- m = min_L d_L and a = sum_L u~_L -- are
+//     exchanged through shared memory under a 64-thread named barrier.  The sum is always formed
+//     as (first half) + (second half) (also for G = 1, see label_update), so G does not change a bit.
 #pragma once
 #include <cuda.h>
 
@@ -43,7 +50,7 @@ struct StagedArgs {
 
 __host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 
-template <int NI, int NL, int TY, int OSTAGE, int MODEL>
+template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
 struct StagedLayout {
     static constexpr int NV = NI + NL;
     static constexpr int NF = Model<MODEL, NI, NL>::NF;   // flow-carrying nodes
@@ -54,7 +61,8 @@ struct StagedLayout {
     static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NF * RPS;
     static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // output staging (per buffer)
     static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;
-    static constexpr int kThreads = 32 * TY + 64;
+    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // m / a exchange (G = 2)
+    static constexpr int kThreads = 32 * G * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
     __host__ __device__ static constexpr int off_U() { return 2 * QSZ; }
@@ -63,41 +71,51 @@ struct StagedLayout {
     __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + 2 * ssz(s_ch); }
     __host__ __device__ static constexpr int off_Uo(int s_ch) { return off_R(s_ch) + round32(3 * RING); }
     __host__ __device__ static constexpr int off_Qo(int s_ch) { return off_Uo(s_ch) + 2 * UOSZ; }
-    __host__ __device__ static constexpr int floats(int s_ch) { return off_Qo(s_ch) + 2 * QOSZ; }
+    __host__ __device__ static constexpr int off_X(int s_ch) { return off_Qo(s_ch) + 2 * QOSZ; }
+    __host__ __device__ static constexpr int floats(int s_ch) { return off_X(s_ch) + XSZ; }
     __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 16; }
 };
 
-template <int NV /* flow nodes */, int CAP, int OSTAGE, int TY>
-__device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int roff, int rps, int rs,
-                                                const float (&Mn)[NV], bool has_z, int x, int y, int zg,
-                                                const float (&qc)[3][NV], const float (&svc)[NV], float *qo,
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Flow step + projection of the thread's NFG flow nodes (channels f0 .. f0+NFG-1) at one voxel.
+template <int NFG, int NF, int CAP, int OSTAGE, int TY>
+__device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int f0, int roff, int rps,
+                                                int rs, const float (&Mn)[NFG], bool has_z, int x, int y, int zg,
+                                                const float (&qc)[3][NFG], const float (&svc)[NFG], float *qo,
                                                 int64_t P) {
     const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
     const int Pi = OSTAGE ? TY * 32 : (int)P;  // channel stride: smem staging tile, or global (fits 32 bits)
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        const float mc = Rz[v * rps + roff];
-        const float gx = gxv ? Rz[v * rps + roff + 1] - mc : 0.f;
-        const float gy = gyv ? Rz[v * rps + roff + rs] - mc : 0.f;
+    for (int v = 0; v < NFG; ++v) {
+        const int f = f0 + v;
+        const float mc = Rz[f * rps + roff];
+        const float gx = gxv ? Rz[f * rps + roff + 1] - mc : 0.f;
+        const float gy = gyv ? Rz[f * rps + roff + rs] - mc : 0.f;
         const float gz = gzv ? Mn[v] - mc : 0.f;
         float hx = qc[0][v], hy = qc[1][v], hz = qc[2][v];
         flow_step<CAP>(a.ctau, gx, gy, gz, svc[v], hx, hy, hz);
         if (OSTAGE) {
-            qo[v * Pi] = hx;
-            qo[(NV + v) * Pi] = hy;
-            qo[(2 * NV + v) * Pi] = hz;
+            qo[f * Pi] = hx;
+            qo[(NF + f) * Pi] = hy;
+            qo[(2 * NF + f) * Pi] = hz;
         } else {
-            st_stream(qo + v * Pi, hx);
-            st_stream(qo + (NV + v) * Pi, hy);
-            st_stream(qo + (2 * NV + v) * Pi, hz);
+            st_stream(qo + f * Pi, hx);
+            st_stream(qo + (NF + f) * Pi, hy);
+            st_stream(qo + (2 * NF + f) * Pi, hz);
         }
     }
 }
 
-template <int NI, int NL, int TY, int OSTAGE, int MODEL>
-__global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
-    using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL>;
-    constexpr int NV = L::NF;  // in this kernel "node" loops run over the flow-carrying nodes
+template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
+__global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
+    using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
+    constexpr int NF = L::NF;
+    static_assert(G == 1 || (MODEL == 0 && NI == 0 && NL % G == 0), "label split only for Potts");
+    constexpr int NLG = NL / G;   // end labels of this thread's group
+    constexpr int NFG = NF / G;   // flow nodes of this thread's group
     constexpr int QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
     constexpr int QCS = QROWS * QW;   // q channel stride in smem
     constexpr int UCS = UROWS * UW;
@@ -110,17 +128,24 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
     float *R = sm + L::off_R(a.s_ch);
     float *Uo = sm + L::off_Uo(a.s_ch);
     float *Qo = sm + L::off_Qo(a.s_ch);
+    float *X = sm + L::off_X(a.s_ch);
     const int SSZ = L::ssz(a.s_ch);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L::floats(a.s_ch));
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool is_main = warp < TY;
-    int lx, ly;
-    if (is_main) { lx = lane; ly = warp; }
-    else if (warp == TY) { lx = lane; ly = TY; }
-    else { lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0; }
+    const bool is_main = warp < G * TY;
+    const int grp = warp % G;
+    int lx, ly, xr;  // tile coordinates of the thread's point; exchange row
+    if (is_main) {
+        lx = lane; ly = warp / G; xr = ly;
+    } else if ((warp - G * TY) / G == 0) {  // bottom halo row
+        lx = lane; ly = TY; xr = TY;
+    } else {                                 // right halo column
+        lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0; xr = TY + 1;
+    }
+    const int l0 = grp * NLG, f0 = grp * NFG;  // first label / flow node of the group
     const int64_t P = (int64_t)a.pitch * a.ny;
-    const int64_t qps = (int64_t)3 * NV * P;
+    const int64_t qps = (int64_t)3 * NF * P;
     const int64_t ups = (int64_t)NL * P;
     const float k2 = kLog2e * a.inv_c;
 
@@ -167,18 +192,18 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
         }
         // q of the plane below the chunk (its z-component enters div of the first plane).  Two register
         // sets alternate between "current plane" and "plane awaiting its flow step" (no copies).
-        float qA[3][NV], qB[3][NV];
-        float sA[NV], sB[NV];
+        float qA[3][NFG], qB[3][NFG];
+        float sA[NFG], sB[NFG];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) { qA[0][v] = 0.f; qA[1][v] = 0.f; qA[2][v] = 0.f; sA[v] = 0.f; }
+        for (int v = 0; v < NFG; ++v) { qA[0][v] = 0.f; qA[1][v] = 0.f; qA[2][v] = 0.f; sA[v] = 0.f; }
         if (valid && (a.zg0 + zc0) > 0) {
-            const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + 2 * NV * P + pix;
+            const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + (2 * NF + f0) * P + pix;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) qA[2][v] = __ldg(qb + v * P);
+            for (int v = 0; v < NFG; ++v) qA[2][v] = __ldg(qb + v * P);
         }
 
-        auto plane_step = [&](const int p, float (&qc)[3][NV], float (&svc)[NV], float (&qn)[3][NV],
-                              float (&svn)[NV]) {
+        auto plane_step = [&](const int p, float (&qc)[3][NFG], float (&svc)[NFG], float (&qn)[3][NFG],
+                              float (&svn)[NFG]) {
             const int k = kbase + (p - zc0);
             const int st = k & 1;
             mbar_wait(&bars[st], (k >> 1) & 1);
@@ -186,62 +211,112 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             const float *Ub = Us + st * L::USZ;
             const float *Db = Ds + st * L::USZ;
             float *Rp = R + (p % 3) * RING;
-            float Mv[NV];
+            float Mv[NFG];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) svn[v] = 0.f;
+            for (int v = 0; v < NFG; ++v) svn[v] = 0.f;
             // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
+            float dq[NFG];
+            float Dv[NLG], uold[NLG], ut[NLG], un[NLG];
+            float dlab[G == 1 ? NI + NL : NLG];   // end-label excesses (G = 1: positions NI..)
             if (lx >= 0) {
-                float dq[NV];
 #pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const float qx = Qb[v * QCS + qoff];
-                    const float qxm = Qb[v * QCS + qoff - 1];
-                    const float qy = Qb[(NV + v) * QCS + qoff];
-                    const float qym = Qb[(NV + v) * QCS + qoff - QW];
-                    const float qz = Qb[(2 * NV + v) * QCS + qoff];
+                for (int v = 0; v < NFG; ++v) {
+                    const int f = f0 + v;
+                    const float qx = Qb[f * QCS + qoff];
+                    const float qxm = Qb[f * QCS + qoff - 1];
+                    const float qy = Qb[(NF + f) * QCS + qoff];
+                    const float qym = Qb[(NF + f) * QCS + qoff - QW];
+                    const float qz = Qb[(2 * NF + f) * QCS + qoff];
                     dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
                     qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
                 }
-                float Dv[NL], d[NI + NL];
 #pragma unroll
-                for (int l = 0; l < NL; ++l) Dv[l] = Db[l * UCS + uoff];
-                label_excess<MODEL, NI, NL>(dq, Dv, d, a.g.w);
-                float uold[NL], ut[NL], un[NL];
+                for (int l = 0; l < NLG; ++l) {
+                    Dv[l] = Db[(l0 + l) * UCS + uoff];
+                    uold[l] = Ub[(l0 + l) * UCS + uoff];
+                }
+            }
+            float sum = 1.f;
+            if constexpr (G == 1) {
+                if (lx >= 0) {
+                    label_excess<MODEL, NI, NL>(dq, Dv, dlab, a.g.w);
+                    sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
+                }
+            } else {
+                // Potts, labels l0 .. l0+NLG-1: d_L = D_L + div q_L; m and a exchanged with the partner warp
+                float *xm = X + (xr * G) * 32 + lane;
+                float *xa = X + ((TY + 2) * G + xr * G) * 32 + lane;
+                float mpart = 0.f;
+                if (lx >= 0) {
 #pragma unroll
-                for (int l = 0; l < NL; ++l) uold[l] = Ub[l * UCS + uoff];
-                const float sum = label_update<NI, NL>(d, uold, ut, un, a.shift, k2);
+                    for (int l = 0; l < NLG; ++l) dlab[l] = Dv[l] + dq[l];
+                    mpart = dlab[0];
+#pragma unroll
+                    for (int l = 1; l < NLG; ++l) mpart = fminf(mpart, dlab[l]);
+                }
+                if (a.shift == 0) {
+                    xm[grp * 32] = mpart;
+                    named_bar(1 + xr, 32 * G);
+                    mpart = fminf(xm[0], xm[32]);
+                } else {
+                    mpart = 0.f;
+                }
+                float spart = 0.f;
+                if (lx >= 0) {
+#pragma unroll
+                    for (int l = 0; l < NLG; ++l) {
+                        ut[l] = uold[l] * ex2_approx((mpart - dlab[l]) * k2);
+                        spart += ut[l];
+                    }
+                }
+                xa[grp * 32] = spart;
+                named_bar(1 + xr, 32 * G);
+                sum = xa[0] + xa[32];
+                const float inv = __frcp_rn(sum);
+#pragma unroll
+                for (int l = 0; l < NLG; ++l) {
+                    const float nu = ut[l] * inv;
+                    un[l] = nu < FLT_MIN ? 0.f : nu;
+                }
+            }
+            if (lx >= 0) {
                 if (is_main && valid && p < zc1) {
-                    if (!(sum > 0.f) || !(sum <= FLT_MAX)) {
+                    if (grp == 0 && (!(sum > 0.f) || !(sum <= FLT_MAX))) {
                         const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                         atomicMin(a.err_voxel, vox);
                     }
                     if (OSTAGE) {
                         float *uo = Uo + (p & 1) * L::UOSZ + ly * 32 + lx;
 #pragma unroll
-                        for (int l = 0; l < NL; ++l) uo[l * TY * 32] = un[l];
+                        for (int l = 0; l < NLG; ++l) uo[(l0 + l) * TY * 32] = un[l];
                     } else {
                         float *uo = a.u_out + (int64_t)p * ups + pix;
 #pragma unroll
-                        for (int l = 0; l < NL; ++l) st_stream(uo + l * (int)P, un[l]);
+                        for (int l = 0; l < NLG; ++l) st_stream(uo + (l0 + l) * (int)P, un[l]);
                     }
 #pragma unroll
-                    for (int l = 0; l < NL; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
+                    for (int l = 0; l < NLG; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                 }
-                node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
+                if constexpr (G == 1) {
+                    node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
+                } else {
 #pragma unroll
-                for (int v = 0; v < NV; ++v) Rp[v * RPS + roff] = Mv[v];
+                    for (int l = 0; l < NLG; ++l) Mv[l] = ut[l];
+                }
+#pragma unroll
+                for (int v = 0; v < NFG; ++v) Rp[(f0 + v) * RPS + roff] = Mv[v];
                 if (is_main) {
                     const float *Sb = Ss + st * SSZ + ly * SW + lx;
                     if (a.s_ch == 0) {
 #pragma unroll
-                        for (int v = 0; v < NV; ++v) svn[v] = a.g.s[v];
-                    } else if (a.s_ch == 1) {  // shared field x per-node multiplier (1 for a plain shared field)
+                        for (int v = 0; v < NFG; ++v) svn[v] = a.g.s[f0 + v];
+                    } else if (a.s_ch == 1) {  // shared field x per-node factor (1 for a plain shared field)
                         const float sv = Sb[0];
 #pragma unroll
-                        for (int v = 0; v < NV; ++v) svn[v] = sv * a.g.s[v];
+                        for (int v = 0; v < NFG; ++v) svn[v] = sv * a.g.s[f0 + v];
                     } else {
 #pragma unroll
-                        for (int v = 0; v < NV; ++v) svn[v] = Sb[v * TY * SW];
+                        for (int v = 0; v < NFG; ++v) svn[v] = Sb[(f0 + v) * TY * SW];
                     }
                 }
             }
@@ -265,12 +340,13 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
             if (is_main && valid && p > zc0) {
                 const int z = p - 1;
                 const float *Rz = R + (z % 3) * RING;
-                float *qo = a.q_out + (int64_t)z * qps + pix;
-                if (OSTAGE) qo = Qo + (z & 1) * L::QOSZ + ly * 32 + lx;
+                float *qo = OSTAGE ? Qo + (z & 1) * L::QOSZ + ly * 32 + lx : a.q_out + (int64_t)z * qps + pix;
                 if (a.cap == 0)
-                    flow_out_staged<NV, 0, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
+                    flow_out_staged<NFG, NF, 0, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc,
+                                                            svc, qo, P);
                 else
-                    flow_out_staged<NV, 1, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc, svc, qo, P);
+                    flow_out_staged<NFG, NF, 1, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc,
+                                                            svc, qo, P);
             }
         };
         int p = zc0;
@@ -281,20 +357,19 @@ __global__ void __launch_bounds__(32 * TY + 64, 1) pf_iter_staged(const __grid_c
         const bool last_in_B = p <= pend;
         if (last_in_B) plane_step(p, qA, sA, qB, sB);
         // last plane of the volume: no plane above, nabla_z = 0
-        auto tail_step = [&](const float (&qc)[3][NV], const float (&svc)[NV]) {
+        auto tail_step = [&](const float (&qc)[3][NFG], const float (&svc)[NFG]) {
             const int z = zc1 - 1;
             const float *Rz = R + (z % 3) * RING;
-            float *qo = a.q_out + (int64_t)z * qps + pix;
-            float Mdummy[NV];
+            float *qo = OSTAGE ? Qo + (z & 1) * L::QOSZ + ly * 32 + lx : a.q_out + (int64_t)z * qps + pix;
+            float Mdummy[NFG];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) Mdummy[v] = 0.f;
-            if (OSTAGE) qo = Qo + (z & 1) * L::QOSZ + ly * 32 + lx;
+            for (int v = 0; v < NFG; ++v) Mdummy[v] = 0.f;
             if (a.cap == 0)
-                flow_out_staged<NV, 0, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo,
-                                                   P);
+                flow_out_staged<NFG, NF, 0, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z,
+                                                        qc, svc, qo, P);
             else
-                flow_out_staged<NV, 1, OSTAGE, TY>(a, Rz, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z, qc, svc, qo,
-                                                   P);
+                flow_out_staged<NFG, NF, 1, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z,
+                                                        qc, svc, qo, P);
         };
         if (!has_above && is_main && valid) {
             if (last_in_B) tail_step(qB, sB);
@@ -326,6 +401,7 @@ struct StagedKernelInfo {
     int smem_bytes;  // with s_ch = 0; add 2 * round32(s_ch * tile_y * 32) floats for an S field
     int tile_y;
     int ostage;      // 1: outputs staged in smem and written by TMA stores
+    int groups;      // label groups per row (G)
 };
 
 bool staged_kernel_lookup(int NI, int NL, int MODEL, StagedKernelInfo *info);
