@@ -15,6 +15,9 @@
 //     in registers (two alternating sets) until the flow step of plane p runs one plane later;
 //   * OSTAGE: the new u and q are staged in shared memory and written by TMA bulk-tensor stores
 //     with an evict-first L2 policy (no per-thread 64-bit address arithmetic, no L2 pollution);
+//     OSTAGE 1 double-buffers the flow staging tile, OSTAGE 2 (many nodes, tight shared memory) has a
+//     single one whose reuse is guarded by an mbarrier that thread 0 arrives on once the previous
+//     store has read it;
 //   * G = 2 (Potts with many labels): the labels of a row of 32 voxels are split over a warp pair;
 //     the only per-voxel couplings of the label update -- m = min_L d_L and a = sum_L u~_L -- are
 //     exchanged through shared memory under a 64-thread named barrier.  The sum is always formed
@@ -61,6 +64,7 @@ struct StagedLayout {
     static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NF * RPS;
     static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // output staging (per buffer)
     static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;
+    static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         // flow staging buffers
     static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // m / a exchange (G = 2)
     static constexpr int kThreads = 32 * G * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
@@ -71,9 +75,9 @@ struct StagedLayout {
     __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + 2 * ssz(s_ch); }
     __host__ __device__ static constexpr int off_Uo(int s_ch) { return off_R(s_ch) + round32(3 * RING); }
     __host__ __device__ static constexpr int off_Qo(int s_ch) { return off_Uo(s_ch) + 2 * UOSZ; }
-    __host__ __device__ static constexpr int off_X(int s_ch) { return off_Qo(s_ch) + 2 * QOSZ; }
+    __host__ __device__ static constexpr int off_X(int s_ch) { return off_Qo(s_ch) + QOB * QOSZ; }
     __host__ __device__ static constexpr int floats(int s_ch) { return off_X(s_ch) + XSZ; }
-    __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 16; }
+    __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 32; }
 };
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -152,6 +156,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], 1);  // OSTAGE 2: flow staging tile free
         fence_mbar_init();
         prefetch_tmap(&a.tm_q);
         prefetch_tmap(&a.tm_u);
@@ -332,15 +337,22 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                 }
                 if (OSTAGE) {
                     if (p < zc1) tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, 0, p + 1, pol_out);
-                    if (p - 2 >= zc0) tma_store_4d(&a.tm_qo, Qo + (p & 1) * L::QOSZ, x0, y0, 0, p - 1, pol_out);
+                    if (p - 2 >= zc0)
+                        tma_store_4d(&a.tm_qo, Qo + (OSTAGE == 1 ? (p & 1) : 0) * L::QOSZ, x0, y0, 0, p - 1, pol_out);
                     bulk_commit();
+                }
+                if (OSTAGE == 2) {  // the single flow staging tile may be rewritten once the store has read it
+                    bulk_wait_read_all();
+                    mbar_arrive(&bars[2]);
                 }
             }
             // ---------------- stage B(p-1): flow step + projection of plane p-1
+            if (OSTAGE == 2 && is_main && p > zc0) mbar_wait(&bars[2], k & 1);
             if (is_main && valid && p > zc0) {
                 const int z = p - 1;
                 const float *Rz = R + (z % 3) * RING;
-                float *qo = OSTAGE ? Qo + (z & 1) * L::QOSZ + ly * 32 + lx : a.q_out + (int64_t)z * qps + pix;
+                float *qo = OSTAGE ? Qo + (OSTAGE == 1 ? (z & 1) : 0) * L::QOSZ + ly * 32 + lx
+                                   : a.q_out + (int64_t)z * qps + pix;
                 if (a.cap == 0)
                     flow_out_staged<NFG, NF, 0, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc,
                                                             svc, qo, P);
@@ -360,7 +372,8 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
         auto tail_step = [&](const float (&qc)[3][NFG], const float (&svc)[NFG]) {
             const int z = zc1 - 1;
             const float *Rz = R + (z % 3) * RING;
-            float *qo = OSTAGE ? Qo + (z & 1) * L::QOSZ + ly * 32 + lx : a.q_out + (int64_t)z * qps + pix;
+            float *qo = OSTAGE ? Qo + (OSTAGE == 1 ? (z & 1) : 0) * L::QOSZ + ly * 32 + lx
+                               : a.q_out + (int64_t)z * qps + pix;
             float Mdummy[NFG];
 #pragma unroll
             for (int v = 0; v < NFG; ++v) Mdummy[v] = 0.f;
@@ -371,16 +384,31 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                 flow_out_staged<NFG, NF, 1, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z,
                                                         qc, svc, qo, P);
         };
-        if (!has_above && is_main && valid) {
-            if (last_in_B) tail_step(qB, sB);
-            else tail_step(qA, sA);
+        if (!has_above) {
+            if (OSTAGE == 1) {  // the store issued at the last plane step may still be reading the tail's buffer
+                if (tid == 0) bulk_wait_read_all();
+                __syncthreads();
+            } else if (OSTAGE == 2) {  // single tile: store the last stepped plane before the tail rewrites it
+                fence_proxy_async();
+                __syncthreads();
+                if (tid == 0) {
+                    if (pend - 1 >= zc0) tma_store_4d(&a.tm_qo, Qo, x0, y0, 0, pend, pol_out);
+                    bulk_commit();
+                    bulk_wait_read_all();
+                }
+                __syncthreads();
+            }
+            if (is_main && valid) {
+                if (last_in_B) tail_step(qB, sB);
+                else tail_step(qA, sA);
+            }
         }
         if (OSTAGE) {  // flush the item's last staged flow planes
             fence_proxy_async();
             __syncthreads();
             if (tid == 0) {
-                for (int z = max(zc0, pend - 1); z < zc1; ++z)
-                    tma_store_4d(&a.tm_qo, Qo + (z & 1) * L::QOSZ, x0, y0, 0, z + 1, pol_out);
+                for (int z = OSTAGE == 1 ? max(zc0, pend - 1) : zc1 - 1; z < zc1; ++z)
+                    tma_store_4d(&a.tm_qo, Qo + (OSTAGE == 1 ? (z & 1) : 0) * L::QOSZ, x0, y0, 0, z + 1, pol_out);
                 bulk_commit();
                 bulk_wait_read_all();
             }
