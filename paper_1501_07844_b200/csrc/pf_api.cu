@@ -217,7 +217,8 @@ struct pf_solver {
     int cur = 0;
     int64_t iters = 0;
     unsigned int *d_resid = nullptr;
-    unsigned long long *d_err = nullptr;
+    unsigned long long *d_err = nullptr;   // [0] error voxel, [1] work-item ticket counter
+    uint64_t ticket_base = 0;              // ticket counter value at the start of the next launch
     unsigned int *d_flag = nullptr;
     double *d_energy = nullptr;  // partials + result
     IterKernelInfo kinfo{};
@@ -509,7 +510,9 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
             s->staged_smem = s->sinfo.smem_bytes + 8 * ((s_ch * s->sinfo.tile_y * 32 + 31) / 32 * 32);
             int maxsm = 0;
             cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device);
-            if (s->staged_smem > maxsm) s->staged = false;  // e.g. per-node S fields with many nodes
+            cudaFuncAttributes fa{};
+            cudaFuncGetAttributes(&fa, s->sinfo.func);  // static shared words (work-queue slot) count too
+            if (s->staged_smem + (int)fa.sharedSizeBytes > maxsm) s->staged = false;  // e.g. per-node S fields
         }
     }
     cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
@@ -548,6 +551,9 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         return bail(st);
     if ((st = alloc(s, (void **)&s->d_resid, 64, "resid")) != PF_OK) return bail(st);
     if ((st = alloc(s, (void **)&s->d_err, 64, "err")) != PF_OK) return bail(st);
+    e = cudaMemsetAsync(s->d_err, 0, 64, s->stream);
+    if (e != cudaSuccess) { cuda_fail(s, e, "zero ticket"); return bail(PF_ERR_CUDA); }
+    s->ticket_base = 0;
     if ((st = alloc(s, (void **)&s->d_flag, 64, "flag")) != PF_OK) return bail(st);
     if ((st = alloc(s, (void **)&s->d_energy, (size_t)(2 * kEnergyBlocks + 2) * sizeof(double), "energy")) != PF_OK)
         return bail(st);
@@ -612,8 +618,9 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
             ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, NL);
         }
         for (int i = 0; i < 2; ++i) {
-            ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 32, ty,
-                                3 * NF);
+            // OSTAGE 2 stores one flow row per warp, OSTAGE 1 the whole tile
+            ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 32,
+                                s->sinfo.ostage == 2 ? 1 : ty, 3 * NF);
             ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, NL);
         }
         ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
@@ -715,9 +722,12 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
             sa.u_out = s->u[1 - s->cur];
             sa.q_out = s->q[1 - s->cur];
             sa.check = a.check;
+            sa.ticket = s->d_err + 1;
+            sa.ticket_base = s->ticket_base;
             void *args[] = {(void *)&sa};
             CK(cudaLaunchKernel(s->sinfo.func, s->grid, dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
                "launch pf_iter_staged");
+            s->ticket_base += (uint64_t)s->items + (uint64_t)s->grid.x;
         } else {
             a.u_in = s->u[s->cur];
             a.q_in = s->q[s->cur];

@@ -13,15 +13,15 @@
 //     elements are zero-filled by the TMA unit, which is exactly q^k(-1) = 0 (reading R4);
 //   * plane p+2 is in flight while plane p is computed; q(p) and S(p) of the own voxel are kept
 //     in registers (two alternating sets) until the flow step of plane p runs one plane later;
-//   * OSTAGE: the new u and q are staged in shared memory and written by TMA bulk-tensor stores
-//     with an evict-first L2 policy (no per-thread 64-bit address arithmetic, no L2 pollution);
-//     OSTAGE 1 double-buffers the flow staging tile, OSTAGE 2 (many nodes, tight shared memory) has a
-//     single one whose reuse is guarded by an mbarrier that thread 0 arrives on once the previous
-//     store has read it;
-//   * G = 2 (Potts with many labels): the labels of a row of 32 voxels are split over a warp pair;
-//     the only per-voxel couplings of the label update -- m = min_L d_L and a = sum_L u~_L -- are
-//     exchanged through shared memory under a 64-thread named barrier.  The sum is always formed
-//     as (first half) + (second half) (also for G = 1, see label_update), so G does not change a bit.
+//   * OSTAGE: the new u and q are staged in shared memory and written by TMA bulk-tensor stores with an
+//     evict-first L2 policy (no per-thread 64-bit address arithmetic, no L2 pollution).  u always as
+//     one double-buffered tile per plane, issued by thread 0 at the plane barrier.  q: OSTAGE 1
+//     double-buffers the flow tile the same way; OSTAGE 2 (many nodes, tight shared memory) has ONE
+//     flow row per main warp, which the warp hands to the TMA unit itself at the end of its flow step.
+//     Bulk-store groups are per thread, so lane 0 only waits for its own previous row store -- issued a
+//     whole stage-A phase earlier -- and no CTA-wide barrier or single-thread drain sits on the
+//     critical path (a single CTA-wide flow tile stalled every plane on the store's shared-memory read).
+//     OSTAGE 0 stores straight from registers.
 #pragma once
 #include <cuda.h>
 
@@ -48,6 +48,8 @@ struct StagedArgs {
     float inv_c, ctau;
     unsigned int *resid_bits;
     unsigned long long *err_voxel;
+    unsigned long long *ticket;       // monotone work-item ticket counter (never reset)
+    unsigned long long ticket_base;   // its value at the start of this launch
     GraphConst g;
 };
 
@@ -55,6 +57,8 @@ __host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 
 template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
 struct StagedLayout {
+    static_assert(G == 1, "one label group per voxel row");
+    static_assert(OSTAGE >= 0 && OSTAGE <= 2, "OSTAGE: 0 direct, 1 tile stores, 2 tile u + per-warp q rows");
     static constexpr int NV = NI + NL;
     static constexpr int NF = Model<MODEL, NI, NL>::NF;   // flow-carrying nodes
     static constexpr int QW = 40, UW = 36, SW = 32;
@@ -62,11 +66,10 @@ struct StagedLayout {
     static constexpr int QSZ = round32(3 * NF * QROWS * QW);  // floats per stage
     static constexpr int USZ = round32(NL * UROWS * UW);
     static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NF * RPS;
-    static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // output staging (per buffer)
-    static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;
-    static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         // flow staging buffers
-    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // m / a exchange (G = 2)
-    static constexpr int kThreads = 32 * G * (TY + 2);
+    static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // u staging [l][row][32], x2
+    static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;   // q staging: OSTAGE 1 [ch][row][32] x2,
+    static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         //            OSTAGE 2 [row][ch][32] x1
+    static constexpr int kThreads = 32 * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
     __host__ __device__ static constexpr int off_U() { return 2 * QSZ; }
@@ -75,32 +78,26 @@ struct StagedLayout {
     __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + 2 * ssz(s_ch); }
     __host__ __device__ static constexpr int off_Uo(int s_ch) { return off_R(s_ch) + round32(3 * RING); }
     __host__ __device__ static constexpr int off_Qo(int s_ch) { return off_Uo(s_ch) + 2 * UOSZ; }
-    __host__ __device__ static constexpr int off_X(int s_ch) { return off_Qo(s_ch) + QOB * QOSZ; }
-    __host__ __device__ static constexpr int floats(int s_ch) { return off_X(s_ch) + XSZ; }
+    __host__ __device__ static constexpr int floats(int s_ch) { return off_Qo(s_ch) + QOB * QOSZ; }
     __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 32; }
 };
 
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// Flow step + projection of the thread's NFG flow nodes (channels f0 .. f0+NFG-1) at one voxel.
-template <int NFG, int NF, int CAP, int OSTAGE, int TY>
-__device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int f0, int roff, int rps,
-                                                int rs, const float (&Mn)[NFG], bool has_z, int x, int y, int zg,
-                                                const float (&qc)[3][NFG], const float (&svc)[NFG], float *qo,
-                                                int64_t P) {
+// Flow step + projection of the thread's NF flow nodes at one voxel (P:148 / P:298).  qo: the thread's
+// slot in the staging row (channel stride 32) or its global address (channel stride P).
+template <int NF, int CAP, int OSTAGE>
+__device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int roff, int rps, int rs,
+                                                const float (&Mn)[NF], bool has_z, int x, int y, int zg,
+                                                const float (&qc)[3][NF], const float (&svc)[NF], float *qo,
+                                                int Pi /* channel stride: staging, or global (fits 32 bits) */) {
     const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
-    const int Pi = OSTAGE ? TY * 32 : (int)P;  // channel stride: smem staging tile, or global (fits 32 bits)
 #pragma unroll
-    for (int v = 0; v < NFG; ++v) {
-        const int f = f0 + v;
+    for (int f = 0; f < NF; ++f) {
         const float mc = Rz[f * rps + roff];
         const float gx = gxv ? Rz[f * rps + roff + 1] - mc : 0.f;
         const float gy = gyv ? Rz[f * rps + roff + rs] - mc : 0.f;
-        const float gz = gzv ? Mn[v] - mc : 0.f;
-        float hx = qc[0][v], hy = qc[1][v], hz = qc[2][v];
-        flow_step<CAP>(a.ctau, gx, gy, gz, svc[v], hx, hy, hz);
+        const float gz = gzv ? Mn[f] - mc : 0.f;
+        float hx = qc[0][f], hy = qc[1][f], hz = qc[2][f];
+        flow_step<CAP>(a.ctau, gx, gy, gz, svc[f], hx, hy, hz);
         if (OSTAGE) {
             qo[f * Pi] = hx;
             qo[(NF + f) * Pi] = hy;
@@ -113,13 +110,33 @@ __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float
     }
 }
 
+// Per-warp staged output row: lane 0 waits until this warp's previous bulk store from the same row has
+// read it.  `since` = bulk groups this warp committed after that store (the u and q rows alternate, so
+// it is 0 or 1 except across item boundaries); waiting for all but the newest group is enough when
+// since >= 1 and never waits for the other row's just-issued store.
+__device__ __forceinline__ void stage_row_acquire(int lane, int since) {
+    if (lane == 0) {
+        if (since >= 1) bulk_wait_read_but1();
+        else bulk_wait_read_all();
+    }
+    __syncwarp();
+}
+
+// ... and hands the written row (plane coordinate cz of the tensor map) to the TMA unit.
+__device__ __forceinline__ void stage_row_release(int lane, const CUtensorMap *map, const float *row, int x0, int y,
+                                                  int cz, uint64_t pol) {
+    fence_proxy_async();  // this thread's generic-proxy writes -> visible to the async proxy
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_4d(map, row, x0, y, 0, cz, pol);
+        bulk_commit();
+    }
+}
+
 template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
-__global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
+__global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
     constexpr int NF = L::NF;
-    static_assert(G == 1 || (MODEL == 0 && NI == 0 && NL % G == 0), "label split only for Potts");
-    constexpr int NLG = NL / G;   // end labels of this thread's group
-    constexpr int NFG = NF / G;   // flow nodes of this thread's group
     constexpr int QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
     constexpr int QCS = QROWS * QW;   // q channel stride in smem
     constexpr int UCS = UROWS * UW;
@@ -132,36 +149,37 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
     float *R = sm + L::off_R(a.s_ch);
     float *Uo = sm + L::off_Uo(a.s_ch);
     float *Qo = sm + L::off_Qo(a.s_ch);
-    float *X = sm + L::off_X(a.s_ch);
     const int SSZ = L::ssz(a.s_ch);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L::floats(a.s_ch));
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool is_main = warp < G * TY;
-    const int grp = warp % G;
-    int lx, ly, xr;  // tile coordinates of the thread's point; exchange row
+    const bool is_main = warp < TY;
+    int lx, ly;  // tile coordinates of the thread's point
     if (is_main) {
-        lx = lane; ly = warp / G; xr = ly;
-    } else if ((warp - G * TY) / G == 0) {  // bottom halo row
-        lx = lane; ly = TY; xr = TY;
-    } else {                                 // right halo column
-        lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0; xr = TY + 1;
+        lx = lane; ly = warp;
+    } else if (warp == TY) {  // bottom halo row
+        lx = lane; ly = TY;
+    } else {                  // right halo column
+        lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0;
     }
-    const int l0 = grp * NLG, f0 = grp * NFG;  // first label / flow node of the group
     const int64_t P = (int64_t)a.pitch * a.ny;
     const int64_t qps = (int64_t)3 * NF * P;
     const int64_t ups = (int64_t)NL * P;
     const float k2 = kLog2e * a.inv_c;
+    float *qo_row = Qo + ly * 3 * NF * 32 + lane;   // OSTAGE 2, main warps: the thread's flow staging slots
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], 1);  // OSTAGE 2: flow staging tile free
         fence_mbar_init();
         prefetch_tmap(&a.tm_q);
         prefetch_tmap(&a.tm_u);
         prefetch_tmap(&a.tm_D);
         if (a.s_ch) prefetch_tmap(&a.tm_S);
+        if (OSTAGE) {
+            prefetch_tmap(&a.tm_uo);
+            prefetch_tmap(&a.tm_qo);
+        }
     }
     __syncthreads();
 
@@ -175,8 +193,21 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
     const uint64_t pol_out = OSTAGE ? policy_evict_first() : 0;
 
     float resid = 0.f;
+    int since_q = 1 << 20;  // bulk groups this thread committed after its last q row store (OSTAGE 2)
     int kbase = 0;   // planes consumed so far by this CTA (ring position / mbarrier parity)
-    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+    // Dynamic work queue: a CTA takes the next ticket when it starts an item, so the items in flight are
+    // always a window of ~gridDim consecutive tiles and the halo lines one tile loads from HBM are still in
+    // L2 when its neighbours read them (a static round-robin lets CTAs drift apart by whole items on
+    // many-item volumes, which sent ~40 % extra halo traffic to HBM on 768^2 planes).  Every launch
+    // consumes exactly items + gridDim tickets (one failed grab per CTA), so the host knows the base.
+    __shared__ int s_item;
+    auto grab = [&]() -> int {
+        const unsigned long long t = atomicAdd(a.ticket, 1ull) - a.ticket_base;
+        return t < (unsigned long long)a.items ? (int)t : a.items;
+    };
+    if (tid == 0) s_item = grab();
+    __syncthreads();
+    for (int item = s_item; item < a.items; item = s_item) {
         const int chunk = item / a.tiles, tile = item - chunk * a.tiles;
         const int x0 = (tile % a.tiles_x) * 32, y0 = (tile / a.tiles_x) * TY;
         const int zc0 = chunk * a.zchunk, zc1 = min(zc0 + a.zchunk, a.nzl);
@@ -184,31 +215,61 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
         const int pend = has_above ? zc1 : zc1 - 1;
         const int x = x0 + (lx < 0 ? 0 : lx), y = y0 + ly;
         const bool valid = (lx >= 0) && x < a.nx && y < a.ny;
+        const bool row_out = is_main && y < a.ny;   // warp-uniform: this warp owns an output row
         const int pix = valid ? y * a.pitch + x : 0;
         const int qoff = (ly + 1) * QW + (lx < 0 ? 0 : lx) + 4;
         const int uoff = ly * UW + (lx < 0 ? 0 : lx);
         const int roff = ly * RS + (lx < 0 ? 0 : lx);
 
-        __syncthreads();  // previous item's readers of the ring / stage buffers are done
+        __syncthreads();  // previous item's readers of the ring / stage buffers (and of s_item) are done
         if (tid == 0) {
+            s_item = grab();  // next item; read by all threads after this item's plane barriers
             fence_proxy_async();
             issue(zc0, kbase & 1, x0, y0);
             if (zc0 + 1 <= pend) issue(zc0 + 1, (kbase + 1) & 1, x0, y0);
         }
         // q of the plane below the chunk (its z-component enters div of the first plane).  Two register
         // sets alternate between "current plane" and "plane awaiting its flow step" (no copies).
-        float qA[3][NFG], qB[3][NFG];
-        float sA[NFG], sB[NFG];
+        float qA[3][NF], qB[3][NF];
+        float sA[NF], sB[NF];
 #pragma unroll
-        for (int v = 0; v < NFG; ++v) { qA[0][v] = 0.f; qA[1][v] = 0.f; qA[2][v] = 0.f; sA[v] = 0.f; }
+        for (int v = 0; v < NF; ++v) { qA[0][v] = 0.f; qA[1][v] = 0.f; qA[2][v] = 0.f; sA[v] = 0.f; }
         if (valid && (a.zg0 + zc0) > 0) {
-            const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + (2 * NF + f0) * P + pix;
+            const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + (2 * NF) * P + pix;
 #pragma unroll
-            for (int v = 0; v < NFG; ++v) qA[2][v] = __ldg(qb + v * P);
+            for (int v = 0; v < NF; ++v) qA[2][v] = __ldg(qb + v * P);
         }
 
-        auto plane_step = [&](const int p, float (&qc)[3][NFG], float (&svc)[NFG], float (&qn)[3][NFG],
-                              float (&svn)[NFG]) {
+        // flow step + projection of plane z (stage B); Mn = M(z+1) at the voxel (unused when !has_z)
+        auto stage_b = [&](const int z, const float (&Mn)[NF], bool has_z, const float (&qc)[3][NF],
+                           const float (&svc)[NF]) {
+            const float *Rz = R + (z % 3) * RING;
+            if (OSTAGE == 2) {
+                if (row_out) {
+                    stage_row_acquire(lane, since_q);
+                    if (valid) {
+                        if (a.cap == 0)
+                            flow_out_staged<NF, 0, 1>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc,
+                                                      qo_row, 32);
+                        else
+                            flow_out_staged<NF, 1, 1>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc,
+                                                      qo_row, 32);
+                    }
+                    stage_row_release(lane, &a.tm_qo, Qo + ly * 3 * NF * 32, x0, y, z + 1, pol_out);
+                    since_q = 0;
+                }
+            } else if (is_main && valid) {
+                float *qo = OSTAGE ? Qo + (z & 1) * L::QOSZ + ly * 32 + lx : a.q_out + (int64_t)z * qps + pix;
+                const int Pi = OSTAGE ? TY * 32 : (int)P;
+                if (a.cap == 0)
+                    flow_out_staged<NF, 0, OSTAGE>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc, qo, Pi);
+                else
+                    flow_out_staged<NF, 1, OSTAGE>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc, qo, Pi);
+            }
+        };
+
+        auto plane_step = [&](const int p, float (&qc)[3][NF], float (&svc)[NF], float (&qn)[3][NF],
+                              float (&svn)[NF]) {
             const int k = kbase + (p - zc0);
             const int st = k & 1;
             mbar_wait(&bars[st], (k >> 1) & 1);
@@ -216,120 +277,78 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
             const float *Ub = Us + st * L::USZ;
             const float *Db = Ds + st * L::USZ;
             float *Rp = R + (p % 3) * RING;
-            float Mv[NFG];
+            float Mv[NF];
 #pragma unroll
-            for (int v = 0; v < NFG; ++v) svn[v] = 0.f;
+            for (int v = 0; v < NF; ++v) svn[v] = 0.f;
             // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
-            float dq[NFG];
-            float Dv[NLG], uold[NLG], ut[NLG], un[NLG];
-            float dlab[G == 1 ? NI + NL : NLG];   // end-label excesses (G = 1: positions NI..)
+            float dq[NF];
+            float Dv[NL], uold[NL], ut[NL], un[NL];
+            float dlab[NI + NL];   // end-label excesses at positions NI..
+            float sum = 1.f;
             if (lx >= 0) {
 #pragma unroll
-                for (int v = 0; v < NFG; ++v) {
-                    const int f = f0 + v;
+                for (int f = 0; f < NF; ++f) {
                     const float qx = Qb[f * QCS + qoff];
                     const float qxm = Qb[f * QCS + qoff - 1];
                     const float qy = Qb[(NF + f) * QCS + qoff];
                     const float qym = Qb[(NF + f) * QCS + qoff - QW];
                     const float qz = Qb[(2 * NF + f) * QCS + qoff];
-                    dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
-                    qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
+                    dq[f] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][f]);
+                    qn[0][f] = qx; qn[1][f] = qy; qn[2][f] = qz;
                 }
 #pragma unroll
-                for (int l = 0; l < NLG; ++l) {
-                    Dv[l] = Db[(l0 + l) * UCS + uoff];
-                    uold[l] = Ub[(l0 + l) * UCS + uoff];
+                for (int l = 0; l < NL; ++l) {
+                    Dv[l] = Db[l * UCS + uoff];
+                    uold[l] = Ub[l * UCS + uoff];
                 }
-            }
-            float sum = 1.f;
-            if constexpr (G == 1) {
-                if (lx >= 0) {
-                    label_excess<MODEL, NI, NL>(dq, Dv, dlab, a.g.w);
-                    sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
-                }
-            } else {
-                // Potts, labels l0 .. l0+NLG-1: d_L = D_L + div q_L; m and a exchanged with the partner warp
-                float *xm = X + (xr * G) * 32 + lane;
-                float *xa = X + ((TY + 2) * G + xr * G) * 32 + lane;
-                float mpart = 0.f;
-                if (lx >= 0) {
-#pragma unroll
-                    for (int l = 0; l < NLG; ++l) dlab[l] = Dv[l] + dq[l];
-                    mpart = dlab[0];
-#pragma unroll
-                    for (int l = 1; l < NLG; ++l) mpart = fminf(mpart, dlab[l]);
-                }
-                if (a.shift == 0) {
-                    xm[grp * 32] = mpart;
-                    named_bar(1 + xr, 32 * G);
-                    mpart = fminf(xm[0], xm[32]);
-                } else {
-                    mpart = 0.f;
-                }
-                float spart = 0.f;
-                if (lx >= 0) {
-#pragma unroll
-                    for (int l = 0; l < NLG; ++l) {
-                        ut[l] = uold[l] * ex2_approx((mpart - dlab[l]) * k2);
-                        spart += ut[l];
-                    }
-                }
-                xa[grp * 32] = spart;
-                named_bar(1 + xr, 32 * G);
-                sum = xa[0] + xa[32];
-                const float inv = __frcp_rn(sum);
-#pragma unroll
-                for (int l = 0; l < NLG; ++l) {
-                    const float nu = ut[l] * inv;
-                    un[l] = nu < FLT_MIN ? 0.f : nu;
-                }
+                label_excess<MODEL, NI, NL>(dq, Dv, dlab, a.g.w);
+                sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
             }
             if (lx >= 0) {
-                if (is_main && valid && p < zc1) {
-                    if (grp == 0 && (!(sum > 0.f) || !(sum <= FLT_MAX))) {
-                        const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
-                        atomicMin(a.err_voxel, vox);
-                    }
+                if (p < zc1) {
                     if (OSTAGE) {
-                        float *uo = Uo + (p & 1) * L::UOSZ + ly * 32 + lx;
+                        if (is_main && valid) {
+                            float *uo = Uo + (p & 1) * L::UOSZ + ly * 32 + lx;
 #pragma unroll
-                        for (int l = 0; l < NLG; ++l) uo[(l0 + l) * TY * 32] = un[l];
-                    } else {
+                            for (int l = 0; l < NL; ++l) uo[l * TY * 32] = un[l];
+                        }
+                    } else if (is_main && valid) {
                         float *uo = a.u_out + (int64_t)p * ups + pix;
 #pragma unroll
-                        for (int l = 0; l < NLG; ++l) st_stream(uo + (l0 + l) * (int)P, un[l]);
+                        for (int l = 0; l < NL; ++l) st_stream(uo + l * (int)P, un[l]);
                     }
+                    if (is_main && valid) {
+                        if (!(sum > 0.f) || !(sum <= FLT_MAX)) {
+                            const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
+                            atomicMin(a.err_voxel, vox);
+                        }
 #pragma unroll
-                    for (int l = 0; l < NLG; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
+                        for (int l = 0; l < NL; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
+                    }
                 }
-                if constexpr (G == 1) {
-                    node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
-                } else {
+                node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
 #pragma unroll
-                    for (int l = 0; l < NLG; ++l) Mv[l] = ut[l];
-                }
-#pragma unroll
-                for (int v = 0; v < NFG; ++v) Rp[(f0 + v) * RPS + roff] = Mv[v];
+                for (int v = 0; v < NF; ++v) Rp[v * RPS + roff] = Mv[v];
                 if (is_main) {
                     const float *Sb = Ss + st * SSZ + ly * SW + lx;
                     if (a.s_ch == 0) {
 #pragma unroll
-                        for (int v = 0; v < NFG; ++v) svn[v] = a.g.s[f0 + v];
+                        for (int v = 0; v < NF; ++v) svn[v] = a.g.s[v];
                     } else if (a.s_ch == 1) {  // shared field x per-node factor (1 for a plain shared field)
                         const float sv = Sb[0];
 #pragma unroll
-                        for (int v = 0; v < NFG; ++v) svn[v] = sv * a.g.s[f0 + v];
+                        for (int v = 0; v < NF; ++v) svn[v] = sv * a.g.s[v];
                     } else {
 #pragma unroll
-                        for (int v = 0; v < NFG; ++v) svn[v] = Sb[(f0 + v) * TY * SW];
+                        for (int v = 0; v < NF; ++v) svn[v] = Sb[v * TY * SW];
                     }
                 }
             }
             if (OSTAGE) {
-                fence_proxy_async();                // staged outputs -> visible to the TMA (async proxy)
+                fence_proxy_async();                // staged u -> visible to the TMA (async proxy)
                 if (tid == 0) bulk_wait_read_all(); // stores of the buffers about to be rewritten have read them
             }
-            __syncthreads();  // ring slot p complete; stage st fully consumed; staged outputs complete
+            __syncthreads();  // ring slot p complete; stage st fully consumed; staged u complete
             if (tid == 0) {
                 if (p + 2 <= pend) {
                     fence_proxy_async();
@@ -337,29 +356,14 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                 }
                 if (OSTAGE) {
                     if (p < zc1) tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, 0, p + 1, pol_out);
-                    if (p - 2 >= zc0)
-                        tma_store_4d(&a.tm_qo, Qo + (OSTAGE == 1 ? (p & 1) : 0) * L::QOSZ, x0, y0, 0, p - 1, pol_out);
+                    if (OSTAGE == 1 && p - 2 >= zc0)
+                        tma_store_4d(&a.tm_qo, Qo + (p & 1) * L::QOSZ, x0, y0, 0, p - 1, pol_out);
                     bulk_commit();
-                }
-                if (OSTAGE == 2) {  // the single flow staging tile may be rewritten once the store has read it
-                    bulk_wait_read_all();
-                    mbar_arrive(&bars[2]);
+                    ++since_q;
                 }
             }
             // ---------------- stage B(p-1): flow step + projection of plane p-1
-            if (OSTAGE == 2 && is_main && p > zc0) mbar_wait(&bars[2], k & 1);
-            if (is_main && valid && p > zc0) {
-                const int z = p - 1;
-                const float *Rz = R + (z % 3) * RING;
-                float *qo = OSTAGE ? Qo + (OSTAGE == 1 ? (z & 1) : 0) * L::QOSZ + ly * 32 + lx
-                                   : a.q_out + (int64_t)z * qps + pix;
-                if (a.cap == 0)
-                    flow_out_staged<NFG, NF, 0, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc,
-                                                            svc, qo, P);
-                else
-                    flow_out_staged<NFG, NF, 1, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mv, true, x, y, a.zg0 + z, qc,
-                                                            svc, qo, P);
-            }
+            if (p > zc0) stage_b(p - 1, Mv, true, qc, svc);
         };
         int p = zc0;
         for (; p + 1 <= pend; p += 2) {
@@ -369,53 +373,32 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
         const bool last_in_B = p <= pend;
         if (last_in_B) plane_step(p, qA, sA, qB, sB);
         // last plane of the volume: no plane above, nabla_z = 0
-        auto tail_step = [&](const float (&qc)[3][NFG], const float (&svc)[NFG]) {
-            const int z = zc1 - 1;
-            const float *Rz = R + (z % 3) * RING;
-            float *qo = OSTAGE ? Qo + (OSTAGE == 1 ? (z & 1) : 0) * L::QOSZ + ly * 32 + lx
-                               : a.q_out + (int64_t)z * qps + pix;
-            float Mdummy[NFG];
-#pragma unroll
-            for (int v = 0; v < NFG; ++v) Mdummy[v] = 0.f;
-            if (a.cap == 0)
-                flow_out_staged<NFG, NF, 0, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z,
-                                                        qc, svc, qo, P);
-            else
-                flow_out_staged<NFG, NF, 1, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mdummy, false, x, y, a.zg0 + z,
-                                                        qc, svc, qo, P);
-        };
         if (!has_above) {
             if (OSTAGE == 1) {  // the store issued at the last plane step may still be reading the tail's buffer
                 if (tid == 0) bulk_wait_read_all();
                 __syncthreads();
-            } else if (OSTAGE == 2) {  // single tile: store the last stepped plane before the tail rewrites it
-                fence_proxy_async();
-                __syncthreads();
-                if (tid == 0) {
-                    if (pend - 1 >= zc0) tma_store_4d(&a.tm_qo, Qo, x0, y0, 0, pend, pol_out);
-                    bulk_commit();
-                    bulk_wait_read_all();
-                }
-                __syncthreads();
             }
-            if (is_main && valid) {
-                if (last_in_B) tail_step(qB, sB);
-                else tail_step(qA, sA);
-            }
+            float Mdummy[NF];
+#pragma unroll
+            for (int v = 0; v < NF; ++v) Mdummy[v] = 0.f;
+            if (last_in_B) stage_b(zc1 - 1, Mdummy, false, qB, sB);
+            else stage_b(zc1 - 1, Mdummy, false, qA, sA);
         }
-        if (OSTAGE) {  // flush the item's last staged flow planes
+        if (OSTAGE == 1) {  // flush the item's last staged flow planes
             fence_proxy_async();
             __syncthreads();
             if (tid == 0) {
-                for (int z = OSTAGE == 1 ? max(zc0, pend - 1) : zc1 - 1; z < zc1; ++z)
-                    tma_store_4d(&a.tm_qo, Qo + (OSTAGE == 1 ? (z & 1) : 0) * L::QOSZ, x0, y0, 0, z + 1, pol_out);
+                for (int z = max(zc0, pend - 1); z < zc1; ++z)
+                    tma_store_4d(&a.tm_qo, Qo + (z & 1) * L::QOSZ, x0, y0, 0, z + 1, pol_out);
                 bulk_commit();
-                bulk_wait_read_all();
             }
         }
+        // the next item rewrites the u (and OSTAGE 1 flow) tiles: their stores must have read them
+        // (ordered before the other threads by the barrier at the top of the next item)
+        if (OSTAGE && tid == 0) bulk_wait_read_all();
         kbase += pend - zc0 + 1;
     }
-    if (OSTAGE && tid == 0) bulk_wait_all();
+    if (OSTAGE && lane == 0) bulk_wait_all();
     if (a.check) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) resid = fmaxf(resid, __shfl_xor_sync(0xffffffffu, resid, o));
