@@ -17,7 +17,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpf.so")
+# PF_LIB selects another in-tree build of the same library (A/B timing of kernel variants in one run;
+# tools/ab.py).  The default is the library __graft_entry__.build() produces.
+LIB_PATH = os.path.join(_HERE, os.environ.get("PF_LIB", "libpf.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

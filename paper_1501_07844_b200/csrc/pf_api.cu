@@ -507,7 +507,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         if (s->staged) {
             const int s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD)
                                  ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NF : 0);
-            s->staged_smem = s->sinfo.smem_bytes + 8 * ((s_ch * s->sinfo.tile_y * 32 + 31) / 32 * 32);
+            s->staged_smem = s->sinfo.smem_bytes + 16 * ((s_ch * s->sinfo.tile_y * 32 + 31) / 32 * 32);  // 4 S slots
             int maxsm = 0;
             cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device);
             cudaFuncAttributes fa{};
@@ -620,7 +620,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         for (int i = 0; i < 2; ++i) {
             // OSTAGE 2 stores one flow row per warp, OSTAGE 1 the whole tile
             ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 32,
-                                s->sinfo.ostage == 2 ? 1 : ty, 3 * NF);
+                                s->sinfo.ostage == 2 ? 1 : ty, s->sinfo.ostage == 2 ? NF / s->sinfo.groups : 3 * NF);
             ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, NL);
         }
         ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);

@@ -17,6 +17,14 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// 1/sqrt(x) on the SFU (MUFU.RSQ).  Only called on x in [1, 3] (the rescaled squared norm below), where
+// rsqrtf() would return the same value after a denormal-input guard that can never trigger.
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Streaming (evict-first) store: the new state is not re-read in this launch, keep it out of L2's way.
 __device__ __forceinline__ void st_stream(float *p, float v) {
     asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
@@ -128,12 +136,14 @@ __device__ __forceinline__ void node_masses(const float (&ut)[NL], float (&M)[Mo
 
 // Flow step + capacity projection of one node at one voxel (P:148 / P:298; Eq. 8 / Eq. 16; R5, R14):
 //   q^ = q - c tau nabla M;  q' = q^ if |q^| <= S else q^ S/|q^|  (CAP 0, l2)  |  clamp(q^, -S, S) (CAP 1).
+// cx, cy, cz: c tau per axis, 0 where nabla_k M is 0 (last index along k) -- the staged kernel folds the
+// boundary into the coefficient (q - 0 * g == q for the finite g it passes there).
 template <int CAP>
-__device__ __forceinline__ void flow_step(float ctau, float gx, float gy, float gz, float sv, float &hx, float &hy,
-                                          float &hz) {
-    hx = fmaf(-ctau, gx, hx);
-    hy = fmaf(-ctau, gy, hy);
-    hz = fmaf(-ctau, gz, hz);
+__device__ __forceinline__ void flow_step3(float cx, float cy, float cz, float gx, float gy, float gz, float sv,
+                                           float &hx, float &hy, float &hz) {
+    hx = fmaf(-cx, gx, hx);
+    hy = fmaf(-cy, gy, hy);
+    hz = fmaf(-cz, gz, hz);
     if (CAP == 0) {
         // Norm on a power-of-two rescaled copy (exact scaling), so tiny flows next to tiny capacities
         // (S(x) down to 1e-38 in the configs' edge-weighted S) neither under-flow their squares nor
@@ -144,13 +154,19 @@ __device__ __forceinline__ void flow_step(float ctau, float gx, float gy, float 
         const float sx = hx * sc, sy = hy * sc, sz = hz * sc;
         const float n2 = fmaf(sx, sx, fmaf(sy, sy, sz * sz));
         const float ss = sv * sc;
-        const float f = n2 > ss * ss ? ss * rsqrtf(n2) : 1.f;  // S / |q^| when projecting
+        const float f = n2 > ss * ss ? ss * rsqrt_approx(n2) : 1.f;  // S / |q^| when projecting
         hx *= f; hy *= f; hz *= f;
     } else {
         hx = fminf(fmaxf(hx, -sv), sv);
         hy = fminf(fmaxf(hy, -sv), sv);
         hz = fminf(fmaxf(hz, -sv), sv);
     }
+}
+
+template <int CAP>
+__device__ __forceinline__ void flow_step(float ctau, float gx, float gy, float gz, float sv, float &hx, float &hy,
+                                          float &hz) {
+    flow_step3<CAP>(ctau, ctau, ctau, gx, gy, gz, sv, hx, hy, hz);
 }
 
 }  // namespace pf

@@ -3,16 +3,17 @@
 // Same arithmetic and same per-voxel order as pf_iter_kernel (see pf_kernels.cuh for the
 // step-by-step mapping to Alg. 1 / Alg. 2 / Alg. 3; the shared math is in pf_math.cuh), different
 // data movement:
-//   * persistent CTAs (one per SM) walk work items = (32 x TY tile, z-chunk) in a static
-//     round-robin order, so the tiles in flight at any time are spatial neighbours and their
-//     shared halo lines are served from L2;
+//   * persistent CTAs (one per SM) take work items = (32 x TY tile, z-chunk) from a device-side
+//     ticket queue, so the tiles in flight at any time are a window of consecutive (neighbouring)
+//     tiles and their shared halo lines are served from L2;
 //   * every z-plane of the tile is fetched by ONE thread as 3-4 TMA box loads
 //     (cp.async.bulk.tensor.4d) into a 2-deep shared-memory ring guarded by mbarriers: q over
 //     x in [x0-4, x0+36) x y in [y0-1, y0+TY] (the -x/-y neighbours for div and the +1 halo
 //     points), u and D over [x0, x0+36) x [y0, y0+TY], S over the tile.  Out-of-range box
 //     elements are zero-filled by the TMA unit, which is exactly q^k(-1) = 0 (reading R4);
-//   * plane p+2 is in flight while plane p is computed; q(p) and S(p) of the own voxel are kept
-//     in registers (two alternating sets) until the flow step of plane p runs one plane later;
+//   * plane p+2 is in flight while plane p is computed; q(p) of the own voxel is kept in registers
+//     (two alternating sets) until the flow step of plane p runs one plane later; S(p) stays in a
+//     4-slot shared ring (slot p mod 4) until then;
 //   * OSTAGE: the new u and q are staged in shared memory and written by TMA bulk-tensor stores with an
 //     evict-first L2 policy (no per-thread 64-bit address arithmetic, no L2 pollution).  u always as
 //     one double-buffered tile per plane, issued by thread 0 at the plane barrier.  q: OSTAGE 1
@@ -21,7 +22,12 @@
 //     Bulk-store groups are per thread, so lane 0 only waits for its own previous row store -- issued a
 //     whole stage-A phase earlier -- and no CTA-wide barrier or single-thread drain sits on the
 //     critical path (a single CTA-wide flow tile stalled every plane on the store's shared-memory read).
-//     OSTAGE 0 stores straight from registers.
+//     OSTAGE 0 stores straight from registers;
+//   * G = 2 (Potts with many labels): the labels of a row of 32 voxels are split over a warp pair, which
+//     doubles the warps per SM at the same shared-memory footprint and halves the registers per thread;
+//     the only per-voxel couplings of the label update -- m = min_L d_L and a = sum_L u~_L -- are
+//     exchanged through shared memory under a 64-thread named barrier.  The sum is always formed as
+//     (first half) + (second half) (also for G = 1, see label_update), so G does not change a bit.
 #pragma once
 #include <cuda.h>
 
@@ -35,8 +41,8 @@ struct StagedArgs {
     CUtensorMap tm_u;   // input u, 4-D (x, y, l, plane+1)
     CUtensorMap tm_D;   // D, 4-D (x, y, l, plane)
     CUtensorMap tm_S;   // S field, 4-D (x, y, channel, plane); unused when s_ch == 0
-    CUtensorMap tm_uo;  // output u, store box (32, TY, NL)        [OSTAGE]
-    CUtensorMap tm_qo;  // output q, store box (32, TY, 3*NF)      [OSTAGE]
+    CUtensorMap tm_uo;  // output u, store box (32, TY, NL)                                   [OSTAGE]
+    CUtensorMap tm_qo;  // output q, store box (32, TY, 3*NF) [OSTAGE 1] or (32, 1, NF/G)   [OSTAGE 2]
     const float *q_in;  // plane 0 of input q (chunk-start q^z(zc0-1) read)
     float *u_out;
     float *q_out;
@@ -57,7 +63,6 @@ __host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 
 template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
 struct StagedLayout {
-    static_assert(G == 1, "one label group per voxel row");
     static_assert(OSTAGE >= 0 && OSTAGE <= 2, "OSTAGE: 0 direct, 1 tile stores, 2 tile u + per-warp q rows");
     static constexpr int NV = NI + NL;
     static constexpr int NF = Model<MODEL, NI, NL>::NF;   // flow-carrying nodes
@@ -68,52 +73,73 @@ struct StagedLayout {
     static constexpr int RS = 33, RPS = (TY + 1) * RS, RING = NF * RPS;
     static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // u staging [l][row][32], x2
     static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;   // q staging: OSTAGE 1 [ch][row][32] x2,
-    static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         //            OSTAGE 2 [row][ch][32] x1
-    static constexpr int kThreads = 32 * (TY + 2);
+    static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         //   OSTAGE 2 [row][grp][k][f][32] x1
+    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // m / a exchange (G = 2)
+    static constexpr int kThreads = 32 * G * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
     __host__ __device__ static constexpr int off_U() { return 2 * QSZ; }
     __host__ __device__ static constexpr int off_D() { return 2 * QSZ + 2 * USZ; }
     __host__ __device__ static constexpr int off_S() { return 2 * QSZ + 4 * USZ; }
-    __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + 2 * ssz(s_ch); }
+    __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + 4 * ssz(s_ch); }
     __host__ __device__ static constexpr int off_Uo(int s_ch) { return off_R(s_ch) + round32(3 * RING); }
     __host__ __device__ static constexpr int off_Qo(int s_ch) { return off_Uo(s_ch) + 2 * UOSZ; }
-    __host__ __device__ static constexpr int floats(int s_ch) { return off_Qo(s_ch) + QOB * QOSZ; }
+    __host__ __device__ static constexpr int off_X(int s_ch) { return off_Qo(s_ch) + QOB * QOSZ; }
+    __host__ __device__ static constexpr int floats(int s_ch) { return off_X(s_ch) + XSZ; }
     __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 32; }
 };
 
-// Flow step + projection of the thread's NF flow nodes at one voxel (P:148 / P:298).  qo: the thread's
-// slot in the staging row (channel stride 32) or its global address (channel stride P).
-template <int NF, int CAP, int OSTAGE>
-__device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int roff, int rps, int rs,
-                                                const float (&Mn)[NF], bool has_z, int x, int y, int zg,
-                                                const float (&qc)[3][NF], const float (&svc)[NF], float *qo,
-                                                int Pi /* channel stride: staging, or global (fits 32 bits) */) {
-    const bool gxv = x < a.nx - 1, gyv = y < a.ny - 1, gzv = has_z && (zg < a.nzg - 1);
-#pragma unroll
-    for (int f = 0; f < NF; ++f) {
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Flow step + projection of the thread's NFG flow nodes (channels f0 .. f0+NFG-1) at one voxel (P:148,
+// P:298).  qo: the thread's slot for channel (k = 0, node f0) in the staging buffer or in global memory;
+// Pf / Pk: the stride between consecutive nodes / between the k-components there.
+// Sz: the voxel's S slot of plane z (shared field, or node 0 of per-node fields; stride TY*32 per node).
+// Boundaries (nabla_k M = 0 at the last index) are folded into per-axis step coefficients computed once
+// per voxel; M is finite at every point the kernel computes (also outside the volume, from the TMA zero
+// fill), so q - 0 * g == q there.  Capacity: S_f = sb * g.s[f] with sb = 1 (scalars), the shared field
+// (g.s = 1 for a plain shared field, the node factors for a scaled one), or the node's own field.
+template <int NFG, int CAP, int OSTAGE, int TY>
+__device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float *Rz, int f0, int roff, int rps,
+                                                int rs, const float (&Mn)[NFG], bool has_z, int x, int y, int zg,
+                                                const float (&qc)[3][NFG], const float *Sz, float *qo,
+                                                int Pf, int Pk) {
+    const float cx = x < a.nx - 1 ? a.ctau : 0.f, cy = y < a.ny - 1 ? a.ctau : 0.f;
+    const float cz = (has_z && zg < a.nzg - 1) ? a.ctau : 0.f;
+    auto one = [&](int v, float sv) {
+        const int f = f0 + v;
         const float mc = Rz[f * rps + roff];
-        const float gx = gxv ? Rz[f * rps + roff + 1] - mc : 0.f;
-        const float gy = gyv ? Rz[f * rps + roff + rs] - mc : 0.f;
-        const float gz = gzv ? Mn[f] - mc : 0.f;
-        float hx = qc[0][f], hy = qc[1][f], hz = qc[2][f];
-        flow_step<CAP>(a.ctau, gx, gy, gz, svc[f], hx, hy, hz);
+        const float gx = Rz[f * rps + roff + 1] - mc;
+        const float gy = Rz[f * rps + roff + rs] - mc;
+        const float gz = Mn[v] - mc;
+        float hx = qc[0][v], hy = qc[1][v], hz = qc[2][v];
+        flow_step3<CAP>(cx, cy, cz, gx, gy, gz, sv, hx, hy, hz);
         if (OSTAGE) {
-            qo[f * Pi] = hx;
-            qo[(NF + f) * Pi] = hy;
-            qo[(2 * NF + f) * Pi] = hz;
+            qo[v * Pf] = hx;
+            qo[v * Pf + Pk] = hy;
+            qo[v * Pf + 2 * Pk] = hz;
         } else {
-            st_stream(qo + f * Pi, hx);
-            st_stream(qo + (NF + f) * Pi, hy);
-            st_stream(qo + (2 * NF + f) * Pi, hz);
+            st_stream(qo + v * Pf, hx);
+            st_stream(qo + v * Pf + Pk, hy);
+            st_stream(qo + v * Pf + 2 * Pk, hz);
         }
+    };
+    if (a.s_ch <= 1) {
+        const float sb = a.s_ch == 1 ? Sz[0] : 1.f;
+#pragma unroll
+        for (int v = 0; v < NFG; ++v) one(v, sb * a.g.s[f0 + v]);
+    } else {
+#pragma unroll
+        for (int v = 0; v < NFG; ++v) one(v, Sz[(f0 + v) * TY * 32]);
     }
 }
 
-// Per-warp staged output row: lane 0 waits until this warp's previous bulk store from the same row has
-// read it.  `since` = bulk groups this warp committed after that store (the u and q rows alternate, so
-// it is 0 or 1 except across item boundaries); waiting for all but the newest group is enough when
-// since >= 1 and never waits for the other row's just-issued store.
+// Per-warp staged output row (OSTAGE 2): lane 0 waits until this warp's previous bulk store from the
+// row has read it.  `since` = bulk groups lane 0 committed after that store (thread 0 also commits the
+// CTA's u tiles); waiting for all but the newest group is enough when since >= 1 and never waits for
+// a just-issued u store.
 __device__ __forceinline__ void stage_row_acquire(int lane, int since) {
     if (lane == 0) {
         if (since >= 1) bulk_wait_read_but1();
@@ -122,21 +148,13 @@ __device__ __forceinline__ void stage_row_acquire(int lane, int since) {
     __syncwarp();
 }
 
-// ... and hands the written row (plane coordinate cz of the tensor map) to the TMA unit.
-__device__ __forceinline__ void stage_row_release(int lane, const CUtensorMap *map, const float *row, int x0, int y,
-                                                  int cz, uint64_t pol) {
-    fence_proxy_async();  // this thread's generic-proxy writes -> visible to the async proxy
-    __syncwarp();
-    if (lane == 0) {
-        tma_store_4d(map, row, x0, y, 0, cz, pol);
-        bulk_commit();
-    }
-}
-
 template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
-__global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
+__global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
     constexpr int NF = L::NF;
+    static_assert(G == 1 || (MODEL == 0 && NI == 0 && NL % G == 0), "label split only for Potts");
+    constexpr int NLG = NL / G;   // end labels of this thread's group
+    constexpr int NFG = NF / G;   // flow nodes of this thread's group
     constexpr int QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
     constexpr int QCS = QROWS * QW;   // q channel stride in smem
     constexpr int UCS = UROWS * UW;
@@ -149,24 +167,28 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_
     float *R = sm + L::off_R(a.s_ch);
     float *Uo = sm + L::off_Uo(a.s_ch);
     float *Qo = sm + L::off_Qo(a.s_ch);
+    float *X = sm + L::off_X(a.s_ch);
     const int SSZ = L::ssz(a.s_ch);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + L::floats(a.s_ch));
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool is_main = warp < TY;
-    int lx, ly;  // tile coordinates of the thread's point
+    const bool is_main = warp < G * TY;
+    const int grp = warp % G;
+    int lx, ly, xr;  // tile coordinates of the thread's point; exchange row
     if (is_main) {
-        lx = lane; ly = warp;
-    } else if (warp == TY) {  // bottom halo row
-        lx = lane; ly = TY;
-    } else {                  // right halo column
-        lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0;
+        lx = lane; ly = warp / G; xr = ly;
+    } else if ((warp - G * TY) / G == 0) {  // bottom halo row
+        lx = lane; ly = TY; xr = TY;
+    } else {                                 // right halo column
+        lx = (lane < TY) ? 32 : -1; ly = (lane < TY) ? lane : 0; xr = TY + 1;
     }
+    const int l0 = grp * NLG, f0 = grp * NFG;  // first label / flow node of the group
     const int64_t P = (int64_t)a.pitch * a.ny;
     const int64_t qps = (int64_t)3 * NF * P;
     const int64_t ups = (int64_t)NL * P;
     const float k2 = kLog2e * a.inv_c;
-    float *qo_row = Qo + ly * 3 * NF * 32 + lane;   // OSTAGE 2, main warps: the thread's flow staging slots
+    // OSTAGE 2: this warp's flow staging row, [k][v][32] for its NFG nodes
+    float *qo_row = Qo + (ly * G + grp) * 3 * NFG * 32;
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -188,13 +210,13 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_
         tma_load_4d(Qs + stage * L::QSZ, &a.tm_q, &bars[stage], x0 - 4, y0 - 1, 0, plane + 1);
         tma_load_4d(Us + stage * L::USZ, &a.tm_u, &bars[stage], x0, y0, 0, plane + 1);
         tma_load_4d(Ds + stage * L::USZ, &a.tm_D, &bars[stage], x0, y0, 0, plane);
-        if (a.s_ch) tma_load_4d(Ss + stage * SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
+        if (a.s_ch) tma_load_4d(Ss + (plane & 3) * SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
     };
     const uint64_t pol_out = OSTAGE ? policy_evict_first() : 0;
 
     float resid = 0.f;
     int since_q = 1 << 20;  // bulk groups this thread committed after its last q row store (OSTAGE 2)
-    int kbase = 0;   // planes consumed so far by this CTA (ring position / mbarrier parity)
+    int kbase = 0;          // planes consumed so far by this CTA (ring position / mbarrier parity)
     // Dynamic work queue: a CTA takes the next ticket when it starts an item, so the items in flight are
     // always a window of ~gridDim consecutive tiles and the halo lines one tile loads from HBM are still in
     // L2 when its neighbours read them (a static round-robin lets CTAs drift apart by whole items on
@@ -230,46 +252,54 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_
         }
         // q of the plane below the chunk (its z-component enters div of the first plane).  Two register
         // sets alternate between "current plane" and "plane awaiting its flow step" (no copies).
-        float qA[3][NF], qB[3][NF];
-        float sA[NF], sB[NF];
+        float qA[3][NFG], qB[3][NFG];
 #pragma unroll
-        for (int v = 0; v < NF; ++v) { qA[0][v] = 0.f; qA[1][v] = 0.f; qA[2][v] = 0.f; sA[v] = 0.f; }
+        for (int v = 0; v < NFG; ++v) { qA[0][v] = 0.f; qA[1][v] = 0.f; qA[2][v] = 0.f; }
         if (valid && (a.zg0 + zc0) > 0) {
-            const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + (2 * NF) * P + pix;
+            const float *qb = a.q_in + (int64_t)(zc0 - 1) * qps + (2 * NF + f0) * P + pix;
 #pragma unroll
-            for (int v = 0; v < NF; ++v) qA[2][v] = __ldg(qb + v * P);
+            for (int v = 0; v < NFG; ++v) qA[2][v] = __ldg(qb + v * P);
         }
 
         // flow step + projection of plane z (stage B); Mn = M(z+1) at the voxel (unused when !has_z)
-        auto stage_b = [&](const int z, const float (&Mn)[NF], bool has_z, const float (&qc)[3][NF],
-                           const float (&svc)[NF]) {
+        auto stage_b = [&](const int z, const float (&Mn)[NFG], bool has_z, const float (&qc)[3][NFG]) {
             const float *Rz = R + (z % 3) * RING;
+            const float *Sz = Ss + (z & 3) * SSZ + ly * SW + lx;
             if (OSTAGE == 2) {
                 if (row_out) {
                     stage_row_acquire(lane, since_q);
                     if (valid) {
                         if (a.cap == 0)
-                            flow_out_staged<NF, 0, 1>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc,
-                                                      qo_row, 32);
+                            flow_out_staged<NFG, 0, 1, TY>(a, Rz, f0, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc,
+                                                           Sz, qo_row + lx, 32, NFG * 32);
                         else
-                            flow_out_staged<NF, 1, 1>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc,
-                                                      qo_row, 32);
+                            flow_out_staged<NFG, 1, 1, TY>(a, Rz, f0, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc,
+                                                           Sz, qo_row + lx, 32, NFG * 32);
                     }
-                    stage_row_release(lane, &a.tm_qo, Qo + ly * 3 * NF * 32, x0, y, z + 1, pol_out);
+                    fence_proxy_async();  // this thread's staged flows -> visible to the async proxy
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int kk = 0; kk < 3; ++kk)
+                            tma_store_4d(&a.tm_qo, qo_row + kk * NFG * 32, x0, y, kk * NF + f0, z + 1, pol_out);
+                        bulk_commit();
+                    }
                     since_q = 0;
                 }
             } else if (is_main && valid) {
-                float *qo = OSTAGE ? Qo + (z & 1) * L::QOSZ + ly * 32 + lx : a.q_out + (int64_t)z * qps + pix;
-                const int Pi = OSTAGE ? TY * 32 : (int)P;
+                float *qo = OSTAGE ? Qo + (z & 1) * L::QOSZ + f0 * TY * 32 + ly * 32 + lx
+                                   : a.q_out + (int64_t)z * qps + f0 * P + pix;
+                const int Pf = OSTAGE ? TY * 32 : (int)P;
                 if (a.cap == 0)
-                    flow_out_staged<NF, 0, OSTAGE>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc, qo, Pi);
+                    flow_out_staged<NFG, 0, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, Sz,
+                                                        qo, Pf, NF * Pf);
                 else
-                    flow_out_staged<NF, 1, OSTAGE>(a, Rz, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, svc, qo, Pi);
+                    flow_out_staged<NFG, 1, OSTAGE, TY>(a, Rz, f0, roff, RPS, RS, Mn, has_z, x, y, a.zg0 + z, qc, Sz,
+                                                        qo, Pf, NF * Pf);
             }
         };
 
-        auto plane_step = [&](const int p, float (&qc)[3][NF], float (&svc)[NF], float (&qn)[3][NF],
-                              float (&svn)[NF]) {
+        auto plane_step = [&](const int p, float (&qc)[3][NFG], float (&qn)[3][NFG]) {
             const int k = kbase + (p - zc0);
             const int st = k & 1;
             mbar_wait(&bars[st], (k >> 1) & 1);
@@ -277,72 +307,100 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_
             const float *Ub = Us + st * L::USZ;
             const float *Db = Ds + st * L::USZ;
             float *Rp = R + (p % 3) * RING;
-            float Mv[NF];
-#pragma unroll
-            for (int v = 0; v < NF; ++v) svn[v] = 0.f;
+            float Mv[NFG];
             // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
-            float dq[NF];
-            float Dv[NL], uold[NL], ut[NL], un[NL];
-            float dlab[NI + NL];   // end-label excesses at positions NI..
-            float sum = 1.f;
+            float dq[NFG];
+            float Dv[NLG], uold[NLG], ut[NLG], un[NLG];
+            float dlab[G == 1 ? NI + NL : NLG];   // end-label excesses (G = 1: positions NI..)
             if (lx >= 0) {
 #pragma unroll
-                for (int f = 0; f < NF; ++f) {
+                for (int v = 0; v < NFG; ++v) {
+                    const int f = f0 + v;
                     const float qx = Qb[f * QCS + qoff];
                     const float qxm = Qb[f * QCS + qoff - 1];
                     const float qy = Qb[(NF + f) * QCS + qoff];
                     const float qym = Qb[(NF + f) * QCS + qoff - QW];
                     const float qz = Qb[(2 * NF + f) * QCS + qoff];
-                    dq[f] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][f]);
-                    qn[0][f] = qx; qn[1][f] = qy; qn[2][f] = qz;
+                    dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
+                    qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
                 }
 #pragma unroll
-                for (int l = 0; l < NL; ++l) {
-                    Dv[l] = Db[l * UCS + uoff];
-                    uold[l] = Ub[l * UCS + uoff];
+                for (int l = 0; l < NLG; ++l) {
+                    Dv[l] = Db[(l0 + l) * UCS + uoff];
+                    uold[l] = Ub[(l0 + l) * UCS + uoff];
                 }
-                label_excess<MODEL, NI, NL>(dq, Dv, dlab, a.g.w);
-                sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
+            }
+            float sum = 1.f;
+            if constexpr (G == 1) {
+                if (lx >= 0) {
+                    label_excess<MODEL, NI, NL>(dq, Dv, dlab, a.g.w);
+                    sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
+                }
+            } else {
+                // Potts, labels l0 .. l0+NLG-1: d_L = D_L + div q_L; m and a exchanged with the partner warp
+                float *xm = X + (xr * G) * 32 + lane;
+                float *xa = X + ((TY + 2) * G + xr * G) * 32 + lane;
+                float mpart = 0.f;
+                if (lx >= 0) {
+#pragma unroll
+                    for (int l = 0; l < NLG; ++l) dlab[l] = Dv[l] + dq[l];
+                    mpart = dlab[0];
+#pragma unroll
+                    for (int l = 1; l < NLG; ++l) mpart = fminf(mpart, dlab[l]);
+                }
+                if (a.shift == 0) {
+                    xm[grp * 32] = mpart;
+                    named_bar(1 + xr, 32 * G);
+                    mpart = fminf(xm[0], xm[32]);
+                } else {
+                    mpart = 0.f;
+                }
+                float spart = 0.f;
+                if (lx >= 0) {
+#pragma unroll
+                    for (int l = 0; l < NLG; ++l) {
+                        ut[l] = uold[l] * ex2_approx((mpart - dlab[l]) * k2);
+                        spart += ut[l];
+                    }
+                }
+                xa[grp * 32] = spart;
+                named_bar(1 + xr, 32 * G);
+                sum = xa[0] + xa[32];
+                const float inv = __frcp_rn(sum);
+#pragma unroll
+                for (int l = 0; l < NLG; ++l) {
+                    const float nu = ut[l] * inv;
+                    un[l] = nu < FLT_MIN ? 0.f : nu;
+                }
             }
             if (lx >= 0) {
-                if (p < zc1) {
+                if (p < zc1 && is_main && valid) {
+                    if (grp == 0 && (!(sum > 0.f) || !(sum <= FLT_MAX))) {
+                        const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
+                        atomicMin(a.err_voxel, vox);
+                    }
                     if (OSTAGE) {
-                        if (is_main && valid) {
-                            float *uo = Uo + (p & 1) * L::UOSZ + ly * 32 + lx;
+                        float *uo = Uo + (p & 1) * L::UOSZ + l0 * TY * 32 + ly * 32 + lx;
 #pragma unroll
-                            for (int l = 0; l < NL; ++l) uo[l * TY * 32] = un[l];
-                        }
-                    } else if (is_main && valid) {
-                        float *uo = a.u_out + (int64_t)p * ups + pix;
-#pragma unroll
-                        for (int l = 0; l < NL; ++l) st_stream(uo + l * (int)P, un[l]);
-                    }
-                    if (is_main && valid) {
-                        if (!(sum > 0.f) || !(sum <= FLT_MAX)) {
-                            const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
-                            atomicMin(a.err_voxel, vox);
-                        }
-#pragma unroll
-                        for (int l = 0; l < NL; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
-                    }
-                }
-                node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
-#pragma unroll
-                for (int v = 0; v < NF; ++v) Rp[v * RPS + roff] = Mv[v];
-                if (is_main) {
-                    const float *Sb = Ss + st * SSZ + ly * SW + lx;
-                    if (a.s_ch == 0) {
-#pragma unroll
-                        for (int v = 0; v < NF; ++v) svn[v] = a.g.s[v];
-                    } else if (a.s_ch == 1) {  // shared field x per-node factor (1 for a plain shared field)
-                        const float sv = Sb[0];
-#pragma unroll
-                        for (int v = 0; v < NF; ++v) svn[v] = sv * a.g.s[v];
+                        for (int l = 0; l < NLG; ++l) uo[l * TY * 32] = un[l];
                     } else {
+                        float *uo = a.u_out + (int64_t)p * ups + l0 * P + pix;
 #pragma unroll
-                        for (int v = 0; v < NF; ++v) svn[v] = Sb[v * TY * SW];
+                        for (int l = 0; l < NLG; ++l) st_stream(uo + l * (int)P, un[l]);
+                    }
+                    if (a.check) {
+#pragma unroll
+                        for (int l = 0; l < NLG; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
                     }
                 }
+                if constexpr (G == 1) {
+                    node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
+                } else {
+#pragma unroll
+                    for (int l = 0; l < NLG; ++l) Mv[l] = ut[l];
+                }
+#pragma unroll
+                for (int v = 0; v < NFG; ++v) Rp[(f0 + v) * RPS + roff] = Mv[v];
             }
             if (OSTAGE) {
                 fence_proxy_async();                // staged u -> visible to the TMA (async proxy)
@@ -363,26 +421,26 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_
                 }
             }
             // ---------------- stage B(p-1): flow step + projection of plane p-1
-            if (p > zc0) stage_b(p - 1, Mv, true, qc, svc);
+            if (p > zc0) stage_b(p - 1, Mv, true, qc);
         };
         int p = zc0;
         for (; p + 1 <= pend; p += 2) {
-            plane_step(p, qA, sA, qB, sB);
-            plane_step(p + 1, qB, sB, qA, sA);
+            plane_step(p, qA, qB);
+            plane_step(p + 1, qB, qA);
         }
         const bool last_in_B = p <= pend;
-        if (last_in_B) plane_step(p, qA, sA, qB, sB);
+        if (last_in_B) plane_step(p, qA, qB);
         // last plane of the volume: no plane above, nabla_z = 0
         if (!has_above) {
             if (OSTAGE == 1) {  // the store issued at the last plane step may still be reading the tail's buffer
                 if (tid == 0) bulk_wait_read_all();
                 __syncthreads();
             }
-            float Mdummy[NF];
+            float Mdummy[NFG];
 #pragma unroll
-            for (int v = 0; v < NF; ++v) Mdummy[v] = 0.f;
-            if (last_in_B) stage_b(zc1 - 1, Mdummy, false, qB, sB);
-            else stage_b(zc1 - 1, Mdummy, false, qA, sA);
+            for (int v = 0; v < NFG; ++v) Mdummy[v] = 0.f;
+            if (last_in_B) stage_b(zc1 - 1, Mdummy, false, qB);
+            else stage_b(zc1 - 1, Mdummy, false, qA);
         }
         if (OSTAGE == 1) {  // flush the item's last staged flow planes
             fence_proxy_async();
@@ -409,7 +467,7 @@ __global__ void __launch_bounds__(32 * (TY + 2), 1) pf_iter_staged(const __grid_
 struct StagedKernelInfo {
     const void *func;
     int threads;
-    int smem_bytes;  // with s_ch = 0; add 2 * round32(s_ch * tile_y * 32) floats for an S field
+    int smem_bytes;  // with s_ch = 0; add 4 * round32(s_ch * tile_y * 32) floats for an S field
     int tile_y;
     int ostage;      // 1: outputs staged in smem and written by TMA stores
     int groups;      // label groups per row (G)
