@@ -211,7 +211,7 @@ def run_ours(args, rank, world, local_rank):
     info = s.kernel_info()
     vl_total = V * world * NL * iters * args.steps
     value = vl_total / (ms / 1e3) / 1e9
-    # roofline of the dominant kernel (pf_iter_kernel): algorithmic bytes per launch / mean launch time
+    # roofline of the dominant kernel (pf_iter_staged): algorithmic bytes per launch / mean launch time
     per_launch_ms = iter_ms / (iters * args.steps)
     alg_bytes = info["algorithmic_bytes_per_iteration"]
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
@@ -277,7 +277,8 @@ def run_ours(args, rank, world, local_rank):
                                                         "regs_per_thread", "smem_bytes", "ctas_per_sm")}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "pf_iter_kernel", "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel": "pf_iter_staged" if info["staged"] else "pf_iter_kernel",
+                         "algorithmic_bytes_per_launch": alg_bytes,
                          "mean_launch_ms": per_launch_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
