@@ -133,6 +133,19 @@ pf_status pf_reset(pf_solver *s);
  * exchanged between calls (pf_halo_regions / pf_exchange_local); n must then be 1. */
 pf_status pf_iterate(pf_solver *s, int32_t n, float *residual);
 
+/* One iteration split in two launches so that a slab's halo exchange overlaps its interior
+ * compute (BASELINE.json north_star "halo exchange ... overlapped with
+ * interior compute").  phase 0 computes the new state on the boundary planes only -- plane 0 if
+ * there is a neighbour below, plane nz_local-1 if there is one above -- so the send regions of
+ * the new state are final once phase 0 has completed on the stream; phase 1 computes every other
+ * plane and completes the iteration (state swap).  The usual pattern: phase 0, record an event,
+ * phase 1, pf_halo_regions (now describing the new state), exchange on another stream after the
+ * event, and make the solver's stream wait for the exchange before the next phase 0.  Results
+ * are bitwise those of pf_iterate(s, 1, residual).  residual: as pf_iterate, phase 1 only.
+ * Errors: PF_ERR_INVALID (phase not 0/1), PF_ERR_STATE (phases out of order; pf_iterate while a
+ * split iteration is open). */
+pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual);
+
 /* Current labeling of the owned slab: u (may be NULL) as [|L|][V_local] and the
  * thresholded labeling argmax (may be NULL) as uint8 [V_local], ties to the lowest
  * label id ("thresholded"). */

@@ -33,7 +33,7 @@ PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE, PF_S_SCALED_FIELD 
 _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_CUDA", 5: "PF_ERR_UNSUPPORTED",
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
-EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
+EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_iterate_phase", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
@@ -85,6 +85,7 @@ _sig = {
                                  _P(pf_slab), _P(ctypes.c_void_p)]),
     "pf_reset": (ctypes.c_int, [_vp]),
     "pf_iterate": (ctypes.c_int, [_vp, ctypes.c_int32, _P(ctypes.c_float)]),
+    "pf_iterate_phase": (ctypes.c_int, [_vp, ctypes.c_int32, _P(ctypes.c_float)]),
     "pf_get_labeling": (ctypes.c_int, [_vp, _vp, _vp]),
     "pf_get_flows": (ctypes.c_int, [_vp, _vp]),
     "pf_get_energy": (ctypes.c_int, [_vp, _P(ctypes.c_double), _P(ctypes.c_double)]),
@@ -173,6 +174,12 @@ def pf_reset(s: int):
 def pf_iterate(s: int, n: int, want_residual: bool = False) -> Optional[float]:
     r = ctypes.c_float(-1.0)
     _check(_lib.pf_iterate(s, int(n), ctypes.byref(r) if want_residual else None))
+    return float(r.value) if want_residual else None
+
+
+def pf_iterate_phase(s: int, phase: int, want_residual: bool = False) -> Optional[float]:
+    r = ctypes.c_float(-1.0)
+    _check(_lib.pf_iterate_phase(s, int(phase), ctypes.byref(r) if want_residual else None))
     return float(r.value) if want_residual else None
 
 

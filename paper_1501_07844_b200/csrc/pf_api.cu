@@ -236,6 +236,9 @@ struct pf_solver {
     int staged_smem = 0;
     int s_ch = 0;
     int tiles_x = 0, tiles = 0, items = 0, sgrid = 0;
+    // boundary / interior split of the z-chunks (slabs with neighbours; pf_iterate_phase)
+    int nb = 0, bplane[2] = {0, 0}, zlo = 0, zhi = 0, items_b = 0;
+    int phase_pending = 0;  // 1 after pf_iterate_phase(0) until its phase 1
     unsigned int tx_bytes = 0;
 };
 
@@ -336,12 +339,21 @@ void choose_chunking(pf_solver *s) {
     if (s->staged) {
         const int occ = std::max(1, s->ctas_per_sm);
         const int64_t slots = (int64_t)sms * occ;
-        const int n = best_chunks(tiles, nzl, slots);
-        s->zchunk = (nzl + n - 1) / n;
-        const int nch = (nzl + s->zchunk - 1) / s->zchunk;
+        // planes next to a neighbouring slab form their own one-plane chunks, computed first
+        s->nb = 0;
+        const bool below = s->z0 > 0, above = s->z1 < s->nz;
+        if (below) s->bplane[s->nb++] = 0;
+        if (above && !(below && nzl == 1)) s->bplane[s->nb++] = nzl - 1;
+        s->zlo = below ? 1 : 0;
+        s->zhi = std::max(s->zlo, (above ? nzl - 1 : nzl));
+        const int nzi = s->zhi - s->zlo;
+        const int n = nzi > 0 ? best_chunks(tiles, nzi, slots) : 0;
+        s->zchunk = nzi > 0 ? (nzi + n - 1) / n : 1;
+        const int nch = nzi > 0 ? (nzi + s->zchunk - 1) / s->zchunk : 0;
         s->tiles_x = gx;
         s->tiles = (int)tiles;
-        s->items = (int)(tiles * nch);
+        s->items_b = (int)(tiles * s->nb);
+        s->items = (int)(tiles * (s->nb + nch));
         s->sgrid = (int)std::min<int64_t>(slots, s->items);
         s->grid = dim3(s->sgrid, 1, 1);
     } else {
@@ -656,105 +668,153 @@ pf_status pf_set_stream(pf_solver *s, void *stream) {
     return PF_OK;
 }
 
+namespace {
+
+// Launch items [ib, ie) of one iteration reading state `cur` (no swap).  ie == ib launches nothing.
+pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
+    if (s->staged) {
+        if (ie <= ib) return PF_OK;
+        StagedArgs sa;
+        memset(&sa, 0, sizeof(sa));
+        sa.tm_D = s->tm_D;
+        sa.tm_S = s->tm_S;
+        sa.nx = (int)s->nx;
+        sa.ny = (int)s->ny;
+        sa.pitch = (int)s->pitch;
+        sa.nzl = (int)s->nzl;
+        sa.zg0 = (int)s->z0;
+        sa.nzg = (int)s->nz;
+        sa.zchunk = s->zchunk;
+        sa.tiles_x = s->tiles_x;
+        sa.tiles = s->tiles;
+        sa.item_begin = ib;
+        sa.items = ie;
+        sa.nb = s->nb;
+        sa.bplane0 = s->bplane[0];
+        sa.bplane1 = s->bplane[1];
+        sa.zlo = s->zlo;
+        sa.zhi = s->zhi;
+        sa.s_ch = s->s_ch;
+        sa.cap = s->cfg.cap;
+        sa.shift = s->cfg.shift;
+        sa.tx_bytes = s->tx_bytes;
+        sa.inv_c = 1.0f / s->cfg.c;
+        sa.ctau = s->cfg.c * s->cfg.tau;
+        sa.resid_bits = s->d_resid;
+        sa.err_voxel = s->d_err;
+        sa.g = s->gc.g;
+        sa.tm_q = s->tm_q[s->cur];
+        sa.tm_u = s->tm_u[s->cur];
+        sa.tm_qo = s->tm_qo[1 - s->cur];
+        sa.tm_uo = s->tm_uo[1 - s->cur];
+        sa.q_in = s->q[s->cur];
+        sa.u_out = s->u[1 - s->cur];
+        sa.q_out = s->q[1 - s->cur];
+        sa.check = check;
+        sa.ticket = s->d_err + 1;
+        sa.ticket_base = s->ticket_base;
+        const int grid = (int)std::min<int64_t>(s->sgrid, ie - ib);
+        void *args[] = {(void *)&sa};
+        CK(cudaLaunchKernel(s->sinfo.func, dim3(grid), dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
+           "launch pf_iter_staged");
+        s->ticket_base += (uint64_t)(ie - ib) + (uint64_t)grid;  // every launch consumes items + grid tickets
+    } else {
+        IterArgs a;
+        memset(&a, 0, sizeof(a));
+        a.D = s->D_alloc;
+        a.S = s->S_alloc;
+        a.nx = (int)s->nx;
+        a.ny = (int)s->ny;
+        a.pitch = (int)s->pitch;
+        a.nzl = (int)s->nzl;
+        a.zg0 = (int)s->z0;
+        a.nzg = (int)s->nz;
+        a.zchunk = s->zchunk;
+        a.s_kind = s->s_kind == PF_S_SCALED_FIELD ? 1 : s->s_kind;
+        a.cap = s->cfg.cap;
+        a.shift = s->cfg.shift;
+        a.inv_c = 1.0f / s->cfg.c;
+        a.ctau = s->cfg.c * s->cfg.tau;
+        a.resid_bits = s->d_resid;
+        a.err_voxel = s->d_err;
+        a.g = s->gc.g;
+        a.check = check;
+        a.u_in = s->u[s->cur];
+        a.q_in = s->q[s->cur];
+        a.u_out = s->u[1 - s->cur];
+        a.q_out = s->q[1 - s->cur];
+        void *args[] = {(void *)&a};
+        CK(cudaLaunchKernel(s->kinfo.func, s->grid, dim3(s->kinfo.threads), args, s->kinfo.smem_bytes, s->stream),
+           "launch pf_iter_kernel");
+    }
+    s->launches++;
+    return PF_OK;
+}
+
+int check_this_iteration(pf_solver *s) {
+    const int64_t it = s->iters + 1;
+    return (s->cfg.check_every > 0 && it % s->cfg.check_every == 0) ? 1 : 0;
+}
+
+pf_status read_residual(pf_solver *s, bool any_check, float *residual) {
+    if (any_check) s->last_resid_valid = true;
+    if (!residual) return PF_OK;
+    *residual = -1.f;
+    pf_status st;
+    if ((st = check_numeric(s)) != PF_OK) return st;
+    if (any_check) {
+        unsigned int bits = 0;
+        CK(cudaMemcpyAsync(&bits, s->d_resid, sizeof(bits), cudaMemcpyDeviceToHost, s->stream), "read residual");
+        CK(cudaStreamSynchronize(s->stream), "sync");
+        float r;
+        memcpy(&r, &bits, 4);
+        *residual = r;
+    }
+    return PF_OK;
+}
+
+}  // namespace
+
 pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
     if (n < 0) return fail(PF_ERR_INVALID, "n must be >= 0");
+    if (s->phase_pending) return fail(PF_ERR_STATE, "pf_iterate: an iteration split by pf_iterate_phase is open");
     DeviceGuard dg(s->device);
-    IterArgs a;
-    memset(&a, 0, sizeof(a));
-    a.D = s->D_alloc;
-    a.S = s->S_alloc;
-    a.nx = (int)s->nx;
-    a.ny = (int)s->ny;
-    a.pitch = (int)s->pitch;
-    a.nzl = (int)s->nzl;
-    a.zg0 = (int)s->z0;
-    a.nzg = (int)s->nz;
-    a.zchunk = s->zchunk;
-    a.s_kind = s->s_kind == PF_S_SCALED_FIELD ? 1 : s->s_kind;
-    a.cap = s->cfg.cap;
-    a.shift = s->cfg.shift;
-    a.inv_c = 1.0f / s->cfg.c;
-    a.ctau = s->cfg.c * s->cfg.tau;
-    a.resid_bits = s->d_resid;
-    a.err_voxel = s->d_err;
-    a.g = s->gc.g;
-    StagedArgs sa;
-    if (s->staged) {
-        memset(&sa, 0, sizeof(sa));
-        sa.tm_D = s->tm_D;
-        sa.tm_S = s->tm_S;
-        sa.nx = a.nx;
-        sa.ny = a.ny;
-        sa.pitch = a.pitch;
-        sa.nzl = a.nzl;
-        sa.zg0 = a.zg0;
-        sa.nzg = a.nzg;
-        sa.zchunk = s->zchunk;
-        sa.tiles_x = s->tiles_x;
-        sa.tiles = s->tiles;
-        sa.items = s->items;
-        sa.s_ch = s->s_ch;
-        sa.cap = a.cap;
-        sa.shift = a.shift;
-        sa.tx_bytes = s->tx_bytes;
-        sa.inv_c = a.inv_c;
-        sa.ctau = a.ctau;
-        sa.resid_bits = s->d_resid;
-        sa.err_voxel = s->d_err;
-        sa.g = s->gc.g;
-    }
     bool any_check = false;
     for (int t = 0; t < n; ++t) {
-        const int64_t it = s->iters + 1;
-        a.check = (s->cfg.check_every > 0 && it % s->cfg.check_every == 0) ? 1 : 0;
-        if (a.check) {
+        const int check = check_this_iteration(s);
+        if (check) {
             CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
             any_check = true;
         }
-        if (s->staged) {
-            sa.tm_q = s->tm_q[s->cur];
-            sa.tm_u = s->tm_u[s->cur];
-            sa.tm_qo = s->tm_qo[1 - s->cur];
-            sa.tm_uo = s->tm_uo[1 - s->cur];
-            sa.q_in = s->q[s->cur];
-            sa.u_out = s->u[1 - s->cur];
-            sa.q_out = s->q[1 - s->cur];
-            sa.check = a.check;
-            sa.ticket = s->d_err + 1;
-            sa.ticket_base = s->ticket_base;
-            void *args[] = {(void *)&sa};
-            CK(cudaLaunchKernel(s->sinfo.func, s->grid, dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
-               "launch pf_iter_staged");
-            s->ticket_base += (uint64_t)s->items + (uint64_t)s->grid.x;
-        } else {
-            a.u_in = s->u[s->cur];
-            a.q_in = s->q[s->cur];
-            a.u_out = s->u[1 - s->cur];
-            a.q_out = s->q[1 - s->cur];
-            void *args[] = {(void *)&a};
-            CK(cudaLaunchKernel(s->kinfo.func, s->grid, dim3(s->kinfo.threads), args, s->kinfo.smem_bytes, s->stream),
-               "launch pf_iter_kernel");
-        }
-        s->launches++;
+        if ((st = launch_items(s, 0, s->items, check)) != PF_OK) return st;
         s->cur = 1 - s->cur;
-        s->iters = it;
+        s->iters += 1;
     }
-    if (any_check) s->last_resid_valid = true;
-    if (residual) {
-        *residual = -1.f;
-        if ((st = check_numeric(s)) != PF_OK) return st;
-        if (any_check) {
-            unsigned int bits = 0;
-            CK(cudaMemcpyAsync(&bits, s->d_resid, sizeof(bits), cudaMemcpyDeviceToHost, s->stream), "read residual");
-            CK(cudaStreamSynchronize(s->stream), "sync");
-            float r;
-            memcpy(&r, &bits, 4);
-            *residual = r;
-        }
+    return read_residual(s, any_check, residual);
+}
+
+pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (phase != 0 && phase != 1) return fail(PF_ERR_INVALID, "phase must be 0 or 1");
+    if ((phase == 0) == (s->phase_pending != 0))
+        return fail(PF_ERR_STATE, phase == 0 ? "phase 0 issued twice" : "phase 1 without phase 0");
+    DeviceGuard dg(s->device);
+    const int check = check_this_iteration(s);
+    if (phase == 0) {
+        if (check) CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
+        // global-load kernel: no split, the whole iteration runs in phase 0
+        if ((st = launch_items(s, 0, s->staged ? s->items_b : 1, check)) != PF_OK) return st;
+        s->phase_pending = 1;
+        return PF_OK;
     }
-    return PF_OK;
+    if (s->staged && (st = launch_items(s, s->items_b, s->items, check)) != PF_OK) return st;
+    s->phase_pending = 0;
+    s->cur = 1 - s->cur;
+    s->iters += 1;
+    return read_residual(s, check != 0, residual);
 }
 
 pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {

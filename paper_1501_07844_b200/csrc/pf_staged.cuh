@@ -47,7 +47,12 @@ struct StagedArgs {
     float *u_out;
     float *q_out;
     int nx, ny, pitch, nzl, zg0, nzg;
-    int zchunk, tiles_x, tiles, items;
+    int zchunk, tiles_x, tiles;
+    int item_begin, items;  // this launch runs items [item_begin, items)
+    // z-chunks: item / tiles < nb: boundary chunk = the single plane bplane[item / tiles] (planes next to
+    // a neighbouring slab, computed first so their halo exchange overlaps the rest); otherwise interior
+    // chunk c = item / tiles - nb: planes [zlo + c*zchunk, min(zlo + (c+1)*zchunk, zhi))
+    int nb, bplane0, bplane1, zlo, zhi;
     int s_ch;     // 0: scalar capacities, 1: shared field (x g.s[f]), NF: field per flow node
     int cap, shift, check;
     unsigned int tx_bytes;
@@ -225,14 +230,15 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
     __shared__ int s_item;
     auto grab = [&]() -> int {
         const unsigned long long t = atomicAdd(a.ticket, 1ull) - a.ticket_base;
-        return t < (unsigned long long)a.items ? (int)t : a.items;
+        return t < (unsigned long long)(a.items - a.item_begin) ? a.item_begin + (int)t : a.items;
     };
     if (tid == 0) s_item = grab();
     __syncthreads();
     for (int item = s_item; item < a.items; item = s_item) {
         const int chunk = item / a.tiles, tile = item - chunk * a.tiles;
         const int x0 = (tile % a.tiles_x) * 32, y0 = (tile / a.tiles_x) * TY;
-        const int zc0 = chunk * a.zchunk, zc1 = min(zc0 + a.zchunk, a.nzl);
+        const int zc0 = chunk < a.nb ? (chunk == 0 ? a.bplane0 : a.bplane1) : a.zlo + (chunk - a.nb) * a.zchunk;
+        const int zc1 = chunk < a.nb ? zc0 + 1 : min(zc0 + a.zchunk, a.zhi);
         const bool has_above = (a.zg0 + zc1) < a.nzg;
         const int pend = has_above ? zc1 : zc1 - 1;
         const int x = x0 + (lx < 0 ? 0 : lx), y = y0 + ly;

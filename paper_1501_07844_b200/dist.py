@@ -3,8 +3,14 @@
 Row e of the hot-path scope: the volume is split into z-slabs of
 ceil(nz/P) planes; after every iteration rank r sends its first-plane u and q to r-1 and its
 last-plane q^z to r+1 (pf_halo_regions names the device ranges).  The exchange rides on the
-process group (NCCL over NVLink on a GPU box, gloo on CPU for the host-side tests) and is
-ordered on the solver's stream, which is set to torch's current stream.
+process group (NCCL over NVLink on a GPU box, gloo on CPU for the host-side tests).
+
+Overlap (BASELINE.json north_star: "halo exchange ... overlapped with interior compute"): every
+iteration is issued as pf_iterate_phase 0 (the boundary planes only) and phase 1 (the rest) on the
+solver's stream S; the exchange is posted on a communication stream C that waits for an event
+recorded between the two phases, so NCCL moves the boundary planes while phase 1 computes the
+interior.  S waits for the exchange before the next phase 0 (which reads the received halos).
+The received planes land in halo planes of the new state that phase 1 neither reads nor writes.
 """
 from __future__ import annotations
 
@@ -28,10 +34,11 @@ def device_view(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
     return torch.as_tensor(_CudaBuf(ptr, nbytes), device=device)
 
 
-def halo_exchange(regions: Dict[str, Optional[torch.Tensor]], rank: int, world: int, group=None):
+def halo_exchange(regions: Dict[str, Optional[torch.Tensor]], rank: int, world: int, group=None, wait: bool = True):
     """Exchange one iteration's halo planes.  regions: send_down_u, send_down_q, recv_up_u, recv_up_q,
     send_up_qz, recv_down_qz (None where the neighbour does not exist).  Per peer pair the messages
-    are posted in the same order on both sides (u, then q downward; q^z upward)."""
+    are posted in the same order on both sides (u, then q downward; q^z upward).  wait=False returns
+    the work handles (their wait() orders the caller's current stream after the transfer)."""
     ops = []
     if rank > 0:
         ops.append(dist.P2POp(dist.isend, regions["send_down_u"], rank - 1, group))
@@ -43,9 +50,12 @@ def halo_exchange(regions: Dict[str, Optional[torch.Tensor]], rank: int, world: 
         ops.append(dist.P2POp(dist.irecv, regions["recv_up_q"], rank + 1, group))
         if regions.get("send_up_qz") is not None:
             ops.append(dist.P2POp(dist.isend, regions["send_up_qz"], rank + 1, group))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
+    works = dist.batch_isend_irecv(ops) if ops else []
+    if wait:
+        for w in works:
             w.wait()
+        return []
+    return works
 
 
 class DistSolver:
@@ -72,21 +82,41 @@ class DistSolver:
             "recv_down_qz": device_view(h.recv_down_qz, h.bytes_qz, dv) if h.recv_down_qz else None,
         }
 
-    def iterate(self, n: int, residual: bool = False):
+    def iterate(self, n: int, residual: bool = False, overlap: bool = True):
         if self.world == 1:
             return self.solver.iterate(n, residual)
         r = None
+        S = torch.cuda.current_stream(self.device)
+        C = self._comm_stream()
+        works = []
         for t in range(n):
             last = residual and t == n - 1
-            val = self.solver.iterate(1, last)
-            if self.world > 1:
+            for w in works:      # S waits for the previous exchange (the halos phase 0 reads)
+                w.wait()
+            works = []
+            if overlap:
+                self.solver.iterate_phase(0)
+                ev = torch.cuda.Event()
+                ev.record(S)
+                val = self.solver.iterate_phase(1, last)
+                C.wait_event(ev)
+                with torch.cuda.stream(C):
+                    works = halo_exchange(self._regions(), self.rank, self.world, self.group, wait=False)
+            else:
+                val = self.solver.iterate(1, last)
                 halo_exchange(self._regions(), self.rank, self.world, self.group)
             if last:
                 rt = torch.tensor([val], device=self.device)
-                if self.world > 1:
-                    dist.all_reduce(rt, op=dist.ReduceOp.MAX, group=self.group)
+                dist.all_reduce(rt, op=dist.ReduceOp.MAX, group=self.group)
                 r = float(rt.item())
+        for w in works:
+            w.wait()
         return r
+
+    def _comm_stream(self):
+        if getattr(self, "_C", None) is None:
+            self._C = torch.cuda.Stream(self.device)
+        return self._C
 
     def reset(self):
         self.solver.reset()

@@ -8,7 +8,7 @@ import numpy as np
 from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SCALED_FIELD,
                PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_get_energy, pf_get_flows, pf_get_kernel_info,
-               pf_get_labeling, pf_halo_regions, pf_iterate, pf_iterations, pf_reset, pf_set_stream)
+               pf_get_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_set_stream)
 
 
 class Solver:
@@ -55,6 +55,10 @@ class Solver:
 
     def iterate(self, n: int, residual: bool = False):
         return pf_iterate(self.h, n, residual)
+
+    def iterate_phase(self, phase: int, residual: bool = False):
+        """One iteration in two launches (boundary planes, then the rest); see pf_iterate_phase."""
+        return pf_iterate_phase(self.h, phase, residual)
 
     def set_stream(self, stream_ptr: int):
         pf_set_stream(self.h, stream_ptr)
@@ -114,15 +118,21 @@ class SlabSet:
     """A volume split into consecutive z-slab solvers driven from one process (one or several
     devices); halos are exchanged by pf_exchange_local after every iteration."""
 
-    def __init__(self, solvers: Sequence[Solver]):
+    def __init__(self, solvers: Sequence[Solver], phased: bool = False):
         self.solvers = list(solvers)
         self.handles = [s.h for s in self.solvers]
+        self.phased = phased   # run every iteration as pf_iterate_phase 0 + 1 (the multi-GPU schedule)
 
     def iterate(self, n: int, residual: bool = False):
         r = None
         for t in range(n):
             last = residual and t == n - 1
-            vals = [s.iterate(1, last) for s in self.solvers]
+            if self.phased:
+                for s in self.solvers:
+                    s.iterate_phase(0)
+                vals = [s.iterate_phase(1, last) for s in self.solvers]
+            else:
+                vals = [s.iterate(1, last) for s in self.solvers]
             pf_exchange_local(self.handles)
             if last:
                 r = max(vals)

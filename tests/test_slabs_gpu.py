@@ -18,9 +18,13 @@ def kernel_variant(request, monkeypatch):
     return request.param
 
 
+@pytest.mark.parametrize("phased", [False, True])
 @pytest.mark.parametrize("name,dims,parts", [("C2", (48, 40, 36), 2), ("C2", (48, 40, 37), 3), ("C4", (40, 33, 29), 4),
-                                             ("C3", (33, 30, 24), 8), ("C5", (36, 33, 20), 5)])
-def test_slabs_bitwise_equal_single_domain(name, dims, parts):
+                                             ("C3", (33, 30, 24), 8), ("C5", (36, 33, 20), 5),
+                                             ("C2", (40, 33, 9), 9)])   # one-plane slabs
+def test_slabs_bitwise_equal_single_domain(name, dims, parts, phased):
+    """phased: every iteration as pf_iterate_phase 0 (boundary planes) + 1 (interior), the multi-GPU
+    overlap schedule."""
     cfg = P.config(name).resized(*dims)
     inp = P.generate(cfg)
     ref = solver_from_inputs(inp)
@@ -28,7 +32,7 @@ def test_slabs_bitwise_equal_single_domain(name, dims, parts):
     u_ref, a_ref = ref.labeling()
     q_ref = ref.flows()
     e_ref = ref.energy()
-    slabs = pf.SlabSet([solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, parts)])
+    slabs = pf.SlabSet([solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, parts)], phased=phased)
     slabs.iterate(25)
     u, a = slabs.labeling()
     q = slabs.flows()
@@ -37,3 +41,25 @@ def test_slabs_bitwise_equal_single_domain(name, dims, parts):
     assert abs(e[0] - e_ref[0]) <= 1e-9 * abs(e_ref[0]) and abs(e[1] - e_ref[1]) <= 1e-9 * abs(e_ref[0])
     slabs.close()
     ref.close()
+
+
+def test_phase_order_errors():
+    cfg = P.config("C2").resized(40, 33, 12)
+    inp = P.generate(cfg)
+    s = solver_from_inputs(inp, slab=(4, 8))
+    with pytest.raises(pf.PFError) as ei:
+        s.iterate_phase(1)
+    assert ei.value.status == pf.PF_ERR_STATE
+    s.iterate_phase(0)
+    with pytest.raises(pf.PFError) as ei:
+        s.iterate(1)
+    assert ei.value.status == pf.PF_ERR_STATE
+    with pytest.raises(pf.PFError) as ei:
+        s.iterate_phase(0)
+    assert ei.value.status == pf.PF_ERR_STATE
+    with pytest.raises(pf.PFError) as ei:
+        s.iterate_phase(2)
+    assert ei.value.status == pf.PF_ERR_INVALID
+    s.iterate_phase(1)
+    assert s.iterations() == 1
+    s.close()
