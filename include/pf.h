@@ -99,6 +99,10 @@ typedef struct {
     int32_t cap;         /* pf_capacity */
     int32_t shift;       /* pf_shift */
     int32_t check_every; /* residual max|u_new - u_old| every k iterations; 0 = never */
+    int32_t d_bf16;      /* 1: store D_L as bf16 (round-to-nearest-even at create; BASELINE.json
+                          * north_star "optionally bf16-stored D_L"): the solver then
+                          * solves the problem with data terms bf16(D_L) exactly, 2 B fewer per
+                          * voxel-label-iteration.  0: fp32. */
 } pf_config;
 
 /* z-slab of a volume split along z across ranks / devices.
@@ -132,6 +136,14 @@ pf_status pf_reset(pf_solver *s);
  * residual != NULL synchronizes the stream.  Multi-slab: the halo planes must be
  * exchanged between calls (pf_halo_regions / pf_exchange_local); n must then be 1. */
 pf_status pf_iterate(pf_solver *s, int32_t n, float *residual);
+
+/* "while not converged" (Alg. 1, Alg. 2; reading R7): iterate until the residual
+ * max|u_new - u_old| of a check iteration (every check_every-th, fused into the iteration kernel)
+ * is <= tol, or max_iters iterations have run.  Only the check iterations synchronize the
+ * stream (one 4-byte read).  iters_done (may be NULL) receives the iterations run by this call,
+ * residual (may be NULL) the last residual read (-1 if none).  Errors: PF_ERR_INVALID
+ * (max_iters < 0, tol < 0 or NaN, check_every == 0), PF_ERR_NUMERIC as pf_iterate. */
+pf_status pf_run(pf_solver *s, int32_t max_iters, float tol, int32_t *iters_done, float *residual);
 
 /* One iteration split in two launches so that a slab's halo exchange overlaps its interior
  * compute (BASELINE.json north_star "halo exchange ... overlapped with

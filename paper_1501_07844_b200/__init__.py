@@ -33,7 +33,7 @@ PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE, PF_S_SCALED_FIELD 
 _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_CUDA", 5: "PF_ERR_UNSUPPORTED",
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
-EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_iterate_phase", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
+EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
@@ -55,7 +55,7 @@ class pf_smoothness(ctypes.Structure):
 
 class pf_config(ctypes.Structure):
     _fields_ = [("c", ctypes.c_float), ("tau", ctypes.c_float), ("cap", ctypes.c_int32), ("shift", ctypes.c_int32),
-                ("check_every", ctypes.c_int32)]
+                ("check_every", ctypes.c_int32), ("d_bf16", ctypes.c_int32)]
 
 
 class pf_slab(ctypes.Structure):
@@ -86,6 +86,7 @@ _sig = {
     "pf_reset": (ctypes.c_int, [_vp]),
     "pf_iterate": (ctypes.c_int, [_vp, ctypes.c_int32, _P(ctypes.c_float)]),
     "pf_iterate_phase": (ctypes.c_int, [_vp, ctypes.c_int32, _P(ctypes.c_float)]),
+    "pf_run": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_float, _P(ctypes.c_int32), _P(ctypes.c_float)]),
     "pf_get_labeling": (ctypes.c_int, [_vp, _vp, _vp]),
     "pf_get_flows": (ctypes.c_int, [_vp, _vp]),
     "pf_get_energy": (ctypes.c_int, [_vp, _P(ctypes.c_double), _P(ctypes.c_double)]),
@@ -99,6 +100,8 @@ _sig = {
     "pf_version": (ctypes.c_char_p, []),
 }
 for _name, (_res, _args) in _sig.items():
+    if "PF_LIB" in os.environ and not hasattr(_lib, _name):
+        continue   # an older build selected for A/B timing (tools/ab.py) may lack newer entry points
     _f = getattr(_lib, _name)
     _f.restype = _res
     _f.argtypes = _args
@@ -136,7 +139,8 @@ def pf_last_error() -> str:
 
 def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, weight, D: Sequence, s_kind: int, s_scalars=None,
               s_fields: Optional[Sequence] = None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2,
-              shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None) -> int:
+              shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None,
+              d_bf16: bool = False) -> int:
     """pf_create.  dims = (nx, ny, nz) global.  D: one float32 volume per end label (node-id order)
     covering the slab plus the plane above it.  Returns the opaque solver handle."""
     nx, ny, nz = [int(v) for v in dims]
@@ -159,7 +163,7 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
         keep.append(fp)
     sm = pf_smoothness(s_kind, sc.ctypes.data_as(_P(ctypes.c_float)) if sc is not None else None,
                        ctypes.cast(fp, _P(ctypes.c_void_p)) if fp is not None else None)
-    cfg = pf_config(c, tau, cap, shift, check_every)
+    cfg = pf_config(c, tau, cap, shift, check_every, 1 if d_bf16 else 0)
     sl = pf_slab(int(slab[0]), int(slab[1])) if slab is not None else None
     out = ctypes.c_void_p()
     _check(_lib.pf_create(ctypes.byref(d), ctypes.byref(g), ctypes.cast(Dp, _P(ctypes.c_void_p)), ctypes.byref(sm),
@@ -175,6 +179,14 @@ def pf_iterate(s: int, n: int, want_residual: bool = False) -> Optional[float]:
     r = ctypes.c_float(-1.0)
     _check(_lib.pf_iterate(s, int(n), ctypes.byref(r) if want_residual else None))
     return float(r.value) if want_residual else None
+
+
+def pf_run(s: int, max_iters: int, tol: float):
+    """Iterate until the check-iteration residual <= tol or max_iters; returns (iterations, residual)."""
+    n = ctypes.c_int32(0)
+    r = ctypes.c_float(-1.0)
+    _check(_lib.pf_run(s, int(max_iters), float(tol), ctypes.byref(n), ctypes.byref(r)))
+    return int(n.value), float(r.value)
 
 
 def pf_iterate_phase(s: int, phase: int, want_residual: bool = False) -> Optional[float]:

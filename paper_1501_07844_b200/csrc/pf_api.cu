@@ -212,7 +212,9 @@ struct pf_solver {
     int s_kind = 0;
     // allocations (base pointers) and plane-0 pointers
     float *u_alloc[2] = {nullptr, nullptr}, *q_alloc[2] = {nullptr, nullptr};
-    float *D_alloc = nullptr, *S_alloc = nullptr;
+    float *D_alloc = nullptr, *S_alloc = nullptr;   // D_alloc: fp32 D (nullptr when D is stored as bf16)
+    uint16_t *D16 = nullptr;                          // bf16 D (cfg.d_bf16), same [z][l][y][pitch] layout
+    const void *Dptr() const { return D16 ? (const void *)D16 : (const void *)D_alloc; }
     float *u[2] = {nullptr, nullptr}, *q[2] = {nullptr, nullptr};
     int cur = 0;
     int64_t iters = 0;
@@ -278,13 +280,14 @@ void pool_setup(int dev) {
 }
 
 void free_all(pf_solver *s) {
-    void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc,
+    void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc, s->D16,
                     s->d_resid, s->d_err, s->d_flag, s->d_energy};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, s->stream);
     cudaGetLastError();
     for (int i = 0; i < 2; ++i) s->u_alloc[i] = s->q_alloc[i] = nullptr;
     s->D_alloc = s->S_alloc = nullptr;
+    s->D16 = nullptr;
     s->d_resid = nullptr;
     s->d_err = nullptr;
     s->d_flag = nullptr;
@@ -381,15 +384,18 @@ EncodeTiledFn encode_fn() {
 
 // 4-D fp32 tensor map over an internal array [plane][channel][y][pitch] (x fastest); elements with
 // x >= nx, y outside [0, ny) or plane outside [0, nplanes) read as 0 (TMA out-of-bounds fill).
-bool encode4d(CUtensorMap *m, const float *base, int64_t nx, int64_t ny, int64_t pitch, int64_t nch, int64_t nplanes,
-              int bx, int by, int bc) {
+bool encode4d(CUtensorMap *m, const void *base, int64_t nx, int64_t ny, int64_t pitch, int64_t nch, int64_t nplanes,
+              int bx, int by, int bc, bool bf16 = false) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
+    const int64_t es_b = bf16 ? 2 : 4;
     cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nch, (cuuint64_t)nplanes};
-    cuuint64_t strides[3] = {(cuuint64_t)(pitch * 4), (cuuint64_t)(pitch * ny * 4), (cuuint64_t)(pitch * ny * nch * 4)};
+    cuuint64_t strides[3] = {(cuuint64_t)(pitch * es_b), (cuuint64_t)(pitch * ny * es_b),
+                             (cuuint64_t)(pitch * ny * nch * es_b)};
     cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bc, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    return fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)base, dims,
+              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -503,7 +509,8 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     s->z0 = z0;
     s->z1 = z1;
     s->nzl = z1 - z0;
-    s->pitch = (dims->nx + 3) / 4 * 4;
+    // row pitch: 16-byte TMA strides for fp32 (multiple of 4) and, with bf16 D, for bf16 rows (of 8)
+    s->pitch = cfg->d_bf16 ? (dims->nx + 7) / 8 * 8 : (dims->nx + 3) / 4 * 4;
     s->P = s->pitch * dims->ny;
     s->gc = gc;
     s->cfg = *cfg;
@@ -515,7 +522,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     {
         const char *env = getenv("PF_ITER_KERNEL");
         const bool want_global = env && strcmp(env, "global") == 0;
-        s->staged = !want_global && staged_kernel_lookup(gc.NI, gc.NL, gc.model, &s->sinfo) && encode_fn() != nullptr;
+        s->staged = !want_global && staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, &s->sinfo) && encode_fn() != nullptr;
         if (s->staged) {
             const int s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD)
                                  ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NF : 0);
@@ -576,6 +583,16 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         e = copy_volume(true, s->D_alloc + l * P, NL, (float *)D[l], s->nx, s->ny, s->pitch, nzD, s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "upload D"); return bail(PF_ERR_CUDA); }
     }
+    if (cfg->d_bf16) {  // bf16 storage: round once on the device, drop the fp32 copy
+        const int64_t nD = (nzl + 1) * NL * P;
+        if ((st = alloc(s, (void **)&s->D16, (size_t)nD * sizeof(uint16_t), "D (bf16)")) != PF_OK) return bail(st);
+        e = launch_f32_to_bf16(s->D_alloc, s->D16, nD, s->stream);
+        if (e != cudaSuccess) { cuda_fail(s, e, "D -> bf16"); return bail(PF_ERR_CUDA); }
+        s->launches++;
+        cudaFreeAsync(s->D_alloc, s->stream);
+        s->D_alloc = nullptr;
+        s->device_bytes -= nD * (int64_t)sizeof(float);
+    }
     if (nS > 0) {
         e = cudaMemsetAsync(s->S_alloc, 0, (size_t)(nzl * nS * P) * sizeof(float), s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "zero S"); return bail(PF_ERR_CUDA); }
@@ -635,11 +652,15 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
                                 s->sinfo.ostage == 2 ? 1 : ty, s->sinfo.ostage == 2 ? NF / s->sinfo.groups : 3 * NF);
             ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, NL);
         }
-        ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
+        if (s->D16)  // bf16 rows: a 40-element (80-byte) box keeps the 16-byte box-width rule
+            ok = ok && encode4d(&s->tm_D, s->D16, s->nx, s->ny, s->pitch, NL, nzl + 1, 40, ty + 1, NL, true);
+        else
+            ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
         if (s->s_ch) ok = ok && encode4d(&s->tm_S, s->S_alloc, s->nx, s->ny, s->pitch, s->s_ch, nzl, 32, ty, s->s_ch);
         else memset(&s->tm_S, 0, sizeof(s->tm_S));
         if (!ok) return bail(fail(PF_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
-        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * NF + 2 * 36 * (ty + 1) * NL + 32 * ty * s->s_ch));
+        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * NF + 36 * (ty + 1) * NL + 32 * ty * s->s_ch) +
+                                 (s->D16 ? 2 * 40 : 4 * 36) * (ty + 1) * NL);
     }
     choose_chunking(s);
     e = cudaStreamSynchronize(s->stream);
@@ -721,7 +742,8 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
     } else {
         IterArgs a;
         memset(&a, 0, sizeof(a));
-        a.D = s->D_alloc;
+        a.D = s->Dptr();
+        a.d_bf16 = s->D16 ? 1 : 0;
         a.S = s->S_alloc;
         a.nx = (int)s->nx;
         a.ny = (int)s->ny;
@@ -793,6 +815,31 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
         s->iters += 1;
     }
     return read_residual(s, any_check, residual);
+}
+
+pf_status pf_run(pf_solver *s, int32_t max_iters, float tol, int32_t *iters_done, float *residual) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (max_iters < 0 || !(tol >= 0.f)) return fail(PF_ERR_INVALID, "max_iters must be >= 0 and tol >= 0");
+    if (s->cfg.check_every <= 0) return fail(PF_ERR_INVALID, "pf_run needs check_every > 0 (the residual cadence)");
+    int32_t done = 0;
+    float r = -1.f;
+    while (done < max_iters) {
+        // run up to and including the next check iteration; the residual read is the only host sync
+        const int64_t k = s->cfg.check_every;
+        const int32_t to_check = (int32_t)(k - (s->iters % k));
+        const int32_t n = std::min<int32_t>(to_check, max_iters - done);
+        float rr = -1.f;
+        if ((st = pf_iterate(s, n, &rr)) != PF_OK) return st;
+        done += n;
+        if (rr >= 0.f) {
+            r = rr;
+            if (r <= tol) break;
+        }
+    }
+    if (iters_done) *iters_done = done;
+    if (residual) *residual = r;
+    return PF_OK;
 }
 
 pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual) {
@@ -879,7 +926,8 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
     memset(&a, 0, sizeof(a));
     a.u = s->u[s->cur];
     a.q = s->q[s->cur];
-    a.D = s->D_alloc;
+    a.D = s->Dptr();
+    a.d_bf16 = s->D16 ? 1 : 0;
     a.S = s->S_alloc;
     a.nx = (int)s->nx;
     a.ny = (int)s->ny;
@@ -1011,7 +1059,7 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     const int64_t V = s->nx * s->ny * s->nzl;
     // per end label: u r/w + D r (+ its flow r/w unless it carries none); per flow-carrying internal node:
     // its flow r/w
-    const int64_t per_leaf = 4 + 4 + 4, per_flow = 8 * s->ndim;
+    const int64_t per_leaf = 4 + 4 + (s->D16 ? 2 : 4), per_flow = 8 * s->ndim;
     int64_t b = V * (per_leaf * s->gc.NL + per_flow * s->gc.NF);
     if (s->s_kind == PF_S_SHARED_FIELD || s->s_kind == PF_S_SCALED_FIELD) b += 4 * V;
     if (s->s_kind == PF_S_FIELD_PER_NODE) b += 4 * V * s->gc.NF;

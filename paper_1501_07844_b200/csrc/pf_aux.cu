@@ -69,6 +69,11 @@ __device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, 
     }
 }
 
+__global__ void f32_to_bf16_kernel(const float *__restrict__ src, uint16_t *__restrict__ dst, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = f32_to_bf16_rn(src[i]);
+}
+
 __global__ void energy_kernel(const EnergyArgs a, double *partial) {
     const int64_t P = (int64_t)a.pitch * a.ny;
     const int64_t V = (int64_t)a.nx * a.ny * a.nzl;
@@ -84,7 +89,7 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
         // ---- primal: sum_L D_L u_L + sum_v S_v |nabla u_v|
         float uc[2 * kMaxNodes], un[2 * kMaxNodes];
         labels_at(a, a.u + z * ups + pix, P, uc);
-        for (int l = 0; l < NL; ++l) e_acc += (double)a.D[z * ups + l * P + pix] * (double)uc[NI + l];
+        for (int l = 0; l < NL; ++l) e_acc += (double)load_D(a.D, z * ups + l * P + pix, a.d_bf16) * (double)uc[NI + l];
         double g2[2 * kMaxNodes], g1[2 * kMaxNodes];
         for (int v = 0; v < NV; ++v) { g2[v] = 0.0; g1[v] = 0.0; }
         if (x < a.nx - 1) {
@@ -119,7 +124,7 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
             }
             d[v] = dv;
         }
-        for (int l = 0; l < NL; ++l) d[NI + l] += (double)a.D[z * ups + l * P + pix];
+        for (int l = 0; l < NL; ++l) d[NI + l] += (double)load_D(a.D, z * ups + l * P + pix, a.d_bf16);
         if (a.model == 1) {  // prefix: d_{L_i} += sum_{j <= i} div q_j
             double run = 0.0;
             for (int i = 1; i < NL; ++i) {
@@ -162,6 +167,11 @@ cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st) {
 cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz,
                           cudaStream_t st) {
     argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_f32_to_bf16(const float *src, uint16_t *dst, int64_t n, cudaStream_t st) {
+    f32_to_bf16_kernel<<<1184, 256, 0, st>>>(src, dst, n);
     return cudaGetLastError();
 }
 

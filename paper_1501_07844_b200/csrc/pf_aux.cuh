@@ -10,8 +10,9 @@ namespace pf {
 struct EnergyArgs {
     const float *u;   // current u, plane 0 (the plane above the slab must be current for the primal)
     const float *q;   // current q, plane 0 (the plane below must be current for the dual)
-    const float *D;
+    const void *D;    // fp32, or bf16 when d_bf16
     const float *S;
+    int d_bf16;
     int nx, ny, pitch, nzl, zg0, nzg, ndim;
     int NI, NL, NV;
     int NF;      // flow-carrying nodes (positions 0..NF-1)
@@ -25,6 +26,7 @@ constexpr int kEnergyBlocks = 592;
 cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st);
 cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz,
                           cudaStream_t st);
+cudaError_t launch_f32_to_bf16(const float *src, uint16_t *dst, int64_t n, cudaStream_t st);
 cudaError_t launch_check_nonneg(const float *p, int64_t n, unsigned int *flag, cudaStream_t st);
 cudaError_t launch_energy(const EnergyArgs &a, double *partial, int nblocks, double *out, cudaStream_t st);
 

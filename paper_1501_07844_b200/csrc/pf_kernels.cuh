@@ -50,7 +50,8 @@ struct IterArgs {
     float *u_out;
     const float *q_in;
     float *q_out;
-    const float *D;
+    const void *D;    // fp32, or bf16 when d_bf16
+    int d_bf16;
     const float *S;   // null when capacities are scalars
     int nx, ny, nzl;  // local extents
     int pitch;        // row pitch in elements (>= nx, multiple of 4 for TMA)
@@ -156,10 +157,10 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
                 dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qzp[v]);
                 qzp[v] = qz;
             }
-            const float *Db = a.D + (int64_t)p * ups + pix;
+            const int64_t Db = (int64_t)p * ups + pix;
             float Dv[NL], d[NI + NL];
 #pragma unroll
-            for (int l = 0; l < NL; ++l) Dv[l] = ldg(Db + l * P);
+            for (int l = 0; l < NL; ++l) Dv[l] = load_D(a.D, Db + l * P, a.d_bf16);
             label_excess<MODEL, NI, NL>(dq, Dv, d, a.g.w);
             const float *ub = a.u_in + (int64_t)p * ups + pix;
             float uold[NL], ut[NL], un[NL];

@@ -4,6 +4,7 @@
 #pragma once
 #include <cfloat>
 #include <cstdint>
+#include <cstring>
 
 namespace pf {
 
@@ -23,6 +24,20 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
     float y;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// bf16 storage of D (pf_config.d_bf16): round-to-nearest-even on upload, exact widening on load.
+// (D is finite and >= 0 by validation, so no NaN handling is needed.)
+__host__ __device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
+    uint32_t b;
+    memcpy(&b, &f, 4);
+    b += 0x7fffu + ((b >> 16) & 1u);
+    return (uint16_t)(b >> 16);
+}
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }
+__device__ __forceinline__ float load_D(const void *D, int64_t i, int bf16) {
+    return bf16 ? bf16_to_f32(__ldg(reinterpret_cast<const unsigned short *>(D) + i))
+                : __ldg(reinterpret_cast<const float *>(D) + i);
 }
 
 // Streaming (evict-first) store: the new state is not re-read in this launch, keep it out of L2's way.

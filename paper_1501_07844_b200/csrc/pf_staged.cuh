@@ -153,7 +153,8 @@ __device__ __forceinline__ void stage_row_acquire(int lane, int since) {
     __syncwarp();
 }
 
-template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
+// DBF: D stored as bf16 (pf_config.d_bf16; the D stage then holds rows of 40 bf16)
+template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF>
 __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
     constexpr int NF = L::NF;
@@ -330,11 +331,17 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                     dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
                     qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
                 }
+                if constexpr (DBF) {
+                    const uint16_t *Dh = reinterpret_cast<const uint16_t *>(Db);
+                    const int doff = ly * 40 + (lx < 0 ? 0 : lx);
 #pragma unroll
-                for (int l = 0; l < NLG; ++l) {
-                    Dv[l] = Db[(l0 + l) * UCS + uoff];
-                    uold[l] = Ub[(l0 + l) * UCS + uoff];
+                    for (int l = 0; l < NLG; ++l) Dv[l] = bf16_to_f32(Dh[(l0 + l) * (UROWS * 40) + doff]);
+                } else {
+#pragma unroll
+                    for (int l = 0; l < NLG; ++l) Dv[l] = Db[(l0 + l) * UCS + uoff];
                 }
+#pragma unroll
+                for (int l = 0; l < NLG; ++l) uold[l] = Ub[(l0 + l) * UCS + uoff];
             }
             float sum = 1.f;
             if constexpr (G == 1) {
@@ -479,6 +486,6 @@ struct StagedKernelInfo {
     int groups;      // label groups per row (G)
 };
 
-bool staged_kernel_lookup(int NI, int NL, int MODEL, StagedKernelInfo *info);
+bool staged_kernel_lookup(int NI, int NL, int MODEL, int DBF, StagedKernelInfo *info);
 
 }  // namespace pf

@@ -8,7 +8,8 @@ import numpy as np
 from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SCALED_FIELD,
                PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_get_energy, pf_get_flows, pf_get_kernel_info,
-               pf_get_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_set_stream)
+               pf_get_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
+               pf_set_stream)
 
 
 class Solver:
@@ -23,7 +24,8 @@ class Solver:
 
     def __init__(self, dims: Sequence[int], ndim: int, graph, D: Sequence, *, s_scalars=None, s_shared=None,
                  s_fields=None, s_scaled=None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2,
-                 shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None):
+                 shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None,
+                 d_bf16: bool = False):
         num_nodes, parent, child, weight = graph
         self.dims = tuple(int(v) for v in dims)
         self.ndim = ndim
@@ -39,7 +41,7 @@ class Solver:
         else:
             kind, fields = PF_S_FIELD_PER_NODE, list(s_fields)
         self.h = pf_create(self.dims, ndim, num_nodes, parent, child, weight, list(D), kind, s_scalars, fields, c, tau, cap,
-                           shift, check_every, slab)
+                           shift, check_every, slab, d_bf16)
 
     # ---------------------------------------------------------------- C-ABI calls
     @property
@@ -55,6 +57,10 @@ class Solver:
 
     def iterate(self, n: int, residual: bool = False):
         return pf_iterate(self.h, n, residual)
+
+    def run(self, max_iters: int, tol: float):
+        """Iterate until converged (residual <= tol at a check iteration) or max_iters: (iterations, residual)."""
+        return pf_run(self.h, max_iters, tol)
 
     def iterate_phase(self, phase: int, residual: bool = False):
         """One iteration in two launches (boundary planes, then the rest); see pf_iterate_phase."""

@@ -6,7 +6,8 @@ import phantoms as P
 CAP = {"l2": 0, "linf": 1}
 
 
-def solver_from_inputs(inp, shift=0, cap=None, check_every=10, slab=None, c=None, tau=None, device_inputs=False):
+def solver_from_inputs(inp, shift=0, cap=None, check_every=10, slab=None, c=None, tau=None, device_inputs=False,
+                       d_bf16=False):
     import paper_1501_07844_b200 as pf
 
     cfg, g = inp.cfg, inp.graph
@@ -37,7 +38,17 @@ def solver_from_inputs(inp, shift=0, cap=None, check_every=10, slab=None, c=None
     cap = CAP[cfg.cap] if cap is None else cap
     return pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.child, g.weight), D,
                      c=cfg.c if c is None else c, tau=cfg.tau if tau is None else tau, cap=cap, shift=shift,
-                     check_every=check_every, slab=None if slab is None else (z0, z1), **kw)
+                     check_every=check_every, slab=None if slab is None else (z0, z1), d_bf16=d_bf16, **kw)
+
+
+def bf16_rounded(inp):
+    """`inp` with its data terms rounded to bf16 (round-to-nearest-even) -- the problem a solver created
+    with d_bf16 solves (pf_config.d_bf16).  Input preprocessing only: the oracle then runs unchanged."""
+    b = np.ascontiguousarray(inp.D, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    D = b.astype(np.uint32).view(np.float32)
+    out = P.Inputs(inp.cfg, inp.graph, inp.window, D, inp.s_kind, inp.s_scalars, inp.s_field, inp.intensity)
+    return out
 
 
 def compare(u_gpu, q_gpu, u_ref, q_ref, tol=1e-4, argmax_frac=0.9999):

@@ -8,7 +8,7 @@ import pytest
 
 import oracle as O
 import phantoms as P
-from helpers import compare, solver_from_inputs, with_field_per_node
+from helpers import bf16_rounded, compare, solver_from_inputs, with_field_per_node
 
 pytestmark = pytest.mark.gpu
 
@@ -135,6 +135,29 @@ def test_deterministic_and_reset():
     assert np.array_equal(u1, u2) and np.array_equal(a1, a2) and np.array_equal(q1, s.flows())
 
 
+@pytest.mark.parametrize("name,dims,n", [("C1", (64, 64, 1), 200), ("C2", (67, 45, 37), 300), ("C4", (40, 40, 40), 300),
+                                         ("C5", (40, 36, 24), 200), ("I2", (37, 29, 19), 300)])
+def test_bf16_data_terms(name, dims, n):
+    """pf_config.d_bf16: the solver solves the problem with bf16(D) -- same parity bar
+    against the oracle run on the bf16-rounded data terms."""
+    inp = bf16_rounded(P.generate(P.config(name).resized(*dims)))
+    assert not np.array_equal(inp.D, P.generate(P.config(name).resized(*dims)).D)   # rounding did something
+    s = solver_from_inputs(inp, d_bf16=True)
+    s.iterate(n)
+    u, _ = s.labeling()
+    q = s.flows()
+    e = s.energy()
+    s.close()
+    ur, qr = O.run_inputs(inp, n)
+    compare(u, q, ur, qr)
+    # the fp32 solver on the rounded inputs is the same computation
+    t = solver_from_inputs(inp)
+    t.iterate(n)
+    assert np.array_equal(t.labeling()[0], u) and np.array_equal(t.flows(), q)
+    assert t.energy() == e
+    t.close()
+
+
 def test_split_calls_equal_one_call():
     """iterate(a) + iterate(b) == iterate(a + b), bitwise (ping-pong bookkeeping)."""
     inp = P.generate(P.config("C2").resized(33, 30, 27))
@@ -153,6 +176,24 @@ def test_residual_matches_state_difference():
     u10, _ = s.labeling()
     assert r == float(np.max(np.abs(u10 - u9)))
     assert s.iterate(3, residual=True) == -1.0   # 11..13: no check
+
+
+def test_run_until_converged():
+    """pf_run ("while not converged"): stops at the first check iteration whose residual <= tol,
+    and its state is bitwise that of iterate(iterations run)."""
+    inp = P.generate(P.config("C1"))
+    s = solver_from_inputs(inp, check_every=10)
+    n, r = s.run(5000, 1e-5)
+    assert 0 < n < 5000 and n % 10 == 0 and 0.0 <= r <= 1e-5
+    t = solver_from_inputs(inp, check_every=10)
+    rs = [t.iterate(10, residual=True) for _ in range(n // 10)]
+    assert all(x > 1e-5 for x in rs[:-1]) and rs[-1] == r
+    assert np.array_equal(s.labeling()[0], t.labeling()[0]) and np.array_equal(s.flows(), t.flows())
+    # budget-limited: max_iters not a multiple of check_every, tol never met
+    n2, r2 = s.run(13, 0.0)
+    assert (n2 == 13 or r2 == 0.0) and r2 >= 0.0 and s.iterations() == n + n2
+    s.close()
+    t.close()
 
 
 def test_energies_match_oracle_and_weak_duality():
