@@ -103,7 +103,14 @@ typedef struct {
                           * north_star "optionally bf16-stored D_L"): the solver then
                           * solves the problem with data terms bf16(D_L) exactly, 2 B fewer per
                           * voxel-label-iteration.  0: fp32. */
+    int32_t method;      /* PF_METHOD_PSEUDO_FLOW (default): Alg. 1 / 2 / 3.  PF_METHOD_EXPLICIT_ALM: the
+                          * explicit-flow ("full-flow") augmented-Lagrangian solver of the Potts
+                          * model Eq. 3 that stores p_S and p_L, the comparison arm of SURVEY 8(f2):
+                          * c = the ALM penalty, tau = its flow step; Potts graphs, whole volumes, l2 or
+                          * box capacities only (else PF_ERR_UNSUPPORTED); no split iterations. */
 } pf_config;
+
+enum { PF_METHOD_PSEUDO_FLOW = 0, PF_METHOD_EXPLICIT_ALM = 1 };
 
 /* z-slab of a volume split along z across ranks / devices.
  * The solver owns global planes [z_begin, z_end).  Inputs D_L cover

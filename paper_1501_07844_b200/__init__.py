@@ -28,6 +28,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 PF_OK, PF_ERR_INVALID, PF_ERR_GRAPH, PF_ERR_OOM, PF_ERR_CUDA, PF_ERR_UNSUPPORTED, PF_ERR_NUMERIC, PF_ERR_STATE = range(8)
 PF_CAP_L2, PF_CAP_LINF = 0, 1
+PF_METHOD_PSEUDO_FLOW, PF_METHOD_EXPLICIT_ALM = 0, 1
 PF_SHIFT_MIN, PF_SHIFT_NONE = 0, 1
 PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE, PF_S_SCALED_FIELD = 0, 1, 2, 3
 _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_CUDA", 5: "PF_ERR_UNSUPPORTED",
@@ -55,7 +56,7 @@ class pf_smoothness(ctypes.Structure):
 
 class pf_config(ctypes.Structure):
     _fields_ = [("c", ctypes.c_float), ("tau", ctypes.c_float), ("cap", ctypes.c_int32), ("shift", ctypes.c_int32),
-                ("check_every", ctypes.c_int32), ("d_bf16", ctypes.c_int32)]
+                ("check_every", ctypes.c_int32), ("d_bf16", ctypes.c_int32), ("method", ctypes.c_int32)]
 
 
 class pf_slab(ctypes.Structure):
@@ -140,7 +141,7 @@ def pf_last_error() -> str:
 def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, weight, D: Sequence, s_kind: int, s_scalars=None,
               s_fields: Optional[Sequence] = None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2,
               shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None,
-              d_bf16: bool = False) -> int:
+              d_bf16: bool = False, method: int = 0) -> int:
     """pf_create.  dims = (nx, ny, nz) global.  D: one float32 volume per end label (node-id order)
     covering the slab plus the plane above it.  Returns the opaque solver handle."""
     nx, ny, nz = [int(v) for v in dims]
@@ -163,7 +164,7 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
         keep.append(fp)
     sm = pf_smoothness(s_kind, sc.ctypes.data_as(_P(ctypes.c_float)) if sc is not None else None,
                        ctypes.cast(fp, _P(ctypes.c_void_p)) if fp is not None else None)
-    cfg = pf_config(c, tau, cap, shift, check_every, 1 if d_bf16 else 0)
+    cfg = pf_config(c, tau, cap, shift, check_every, 1 if d_bf16 else 0, int(method))
     sl = pf_slab(int(slab[0]), int(slab[1])) if slab is not None else None
     out = ctypes.c_void_p()
     _check(_lib.pf_create(ctypes.byref(d), ctypes.byref(g), ctypes.cast(Dp, _P(ctypes.c_void_p)), ctypes.byref(sm),

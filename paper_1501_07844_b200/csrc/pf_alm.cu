@@ -1,0 +1,235 @@
+// pf_alm.cu -- explicit-flow (full-flow) augmented-Lagrangian max-flow for the Potts model on sm_100a:
+// the comparison arm of SURVEY 8(f2) (pf_config.method = PF_METHOD_EXPLICIT_ALM).
+//
+// The paper's point (P:5) is that the pseudo-flow iteration (Alg. 1) keeps the source
+// and sink flows p_S, p_L implicit.  This is the classic alternative that stores them: block-coordinate
+// ascent on the augmented Lagrangian of Eq. 3 with u as the multipliers,
+//   L_c = p_S + sum_L u_L r_L - c/2 sum_L r_L^2,   r_L = div q_L - p_S + p_L,   p_L <= D_L, |q_L| <= S_L,
+// one sweep per iteration in the order of oracle/alm.py potts_alm (the labels are independent given p_S):
+//   q_L  <- Proj_{|q| <= S_L}( q_L + tau grad(div q_L - p_S + p_L - u_L / c) )     [alm_flow_kernel]
+//   p_L  <- min(D_L, p_S - div q_L + u_L / c)              (new q)                  [alm_potential_kernel]
+//   p_S  <- (sum_L (p_L + div q_L - u_L / c)) / K + 1 / (K c)
+//   u_L  <- u_L - c (div q_L - p_S + p_L)
+// The p / p_S / u update needs the divergence of the NEW flows at every voxel, so one iteration is two
+// dependent HBM passes (the pseudo-flow iteration is one): that, and the extra p_L, p_S buffers, are what
+// the comparison measures.  Discretisation as everywhere (reading R4): forward grad with 0 at the last
+// index, div = -grad^T with q^k(-1) = 0.
+//
+// Layouts (pf_api.cu): q ping-pong [z][k][L][y][pitch] with planes -1..nz (as the pseudo-flow solver),
+// u, p [z][L][y][pitch] updated in place, p_S [z][y][pitch] in place, D, S as the pseudo-flow solver.
+#include <cfloat>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pf_alm.cuh"
+#include "pf_kernels.cuh"   // constants + pf_math.cuh (flow_step3, load_D)
+
+namespace pf {
+
+namespace {
+
+constexpr int kAlmTY = 8;   // flow kernel tile height (32 x 8 voxels, +1 halo row / column for the gradient)
+
+__device__ __forceinline__ float ld(const float *p) { return __ldg(p); }
+
+// capacity S_L(z, pixel): scalar per label, shared field x per-label factor, or a field per label
+__device__ __forceinline__ float cap_at(const AlmArgs &a, int L, int z, int pix, int64_t P) {
+    if (!a.S) return a.s[L];
+    if (a.s_per_node) return ld(a.S + ((int64_t)z * a.NL + L) * P + pix);
+    return ld(a.S + (int64_t)z * P + pix) * a.s[L];
+}
+
+// Proj_{|q| <= S} (l2: the pseudo-flow solver's exactly-rescaled projection; box: clamp)
+__device__ __forceinline__ void project(int cap, float sv, float &hx, float &hy, float &hz) {
+    if (cap == 0) flow_step3<0>(0.f, 0.f, 0.f, 0.f, 0.f, 0.f, sv, hx, hy, hz);
+    else flow_step3<1>(0.f, 0.f, 0.f, 0.f, 0.f, 0.f, sv, hx, hy, hz);
+}
+
+// Pass 1, one label per CTA z-slice of the grid: f = div q - p_S + p_L - u_L / c on the tile and its +x/+y
+// halo, then q' = Proj(q + tau grad f) on the tile.  z-march with a 3-slot shared ring of f planes.
+__global__ void __launch_bounds__(32 * kAlmTY + 64) alm_flow_kernel(const AlmArgs a) {
+    constexpr int TY = kAlmTY, RS = 33, PS = (TY + 1) * RS;
+    __shared__ float F[3 * PS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool is_main = warp < TY;
+    int lx, ly;
+    if (is_main) {
+        lx = lane; ly = warp;
+    } else {
+        const int h = (warp - TY) * 32 + lane;
+        if (h < 32) { lx = h; ly = TY; }
+        else if (h < 32 + TY) { lx = 32; ly = h - 32; }
+        else { lx = -1; ly = 0; }
+    }
+    const int nch = (a.nz + a.zchunk - 1) / a.zchunk;
+    const int L = blockIdx.z / nch, chunk = blockIdx.z - L * nch;
+    const int x = blockIdx.x * 32 + lx, y = blockIdx.y * TY + ly;
+    const bool active = lx >= 0 && x < a.nx && y < a.ny;
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int64_t qps = (int64_t)3 * a.NL * P, ups = (int64_t)a.NL * P;
+    const int pix = active ? y * a.pitch + x : 0;
+    const int sme = ly * RS + (lx < 0 ? 0 : lx);
+    const int zc0 = chunk * a.zchunk, zc1 = min(zc0 + a.zchunk, a.nz);
+    const bool has_above = zc1 < a.nz;
+    const float cx = x < a.nx - 1 ? a.tau : 0.f, cy = y < a.ny - 1 ? a.tau : 0.f;
+
+    // q of the plane below the chunk (z-component enters div of the first plane)
+    float qzp = 0.f;
+    if (active && zc0 > 0) qzp = ld(a.q_in + (int64_t)(zc0 - 1) * qps + (2 * a.NL + L) * P + pix);
+    float qcx = 0.f, qcy = 0.f, qcz = 0.f;   // q(p-1) at the voxel, for its flow step one plane later
+    for (int p = zc0; p <= zc1; ++p) {
+        if (p == zc1 && !has_above) break;   // block-uniform
+        float *Fp = F + (p % 3) * PS;
+        float f = 0.f, qx = 0.f, qy = 0.f, qz = 0.f;
+        if (active) {
+            const float *qb = a.q_in + (int64_t)p * qps + pix;
+            qx = ld(qb + L * P);
+            qy = ld(qb + (a.NL + L) * P);
+            qz = ld(qb + (2 * a.NL + L) * P);
+            const float qxm = x > 0 ? ld(qb + L * P - 1) : 0.f;
+            const float qym = y > 0 ? ld(qb + (a.NL + L) * P - a.pitch) : 0.f;
+            const float dq = ((qx - qxm) + (qy - qym)) + (qz - qzp);
+            const int64_t o = (int64_t)p * ups + L * P + pix;
+            f = ((dq - ld(a.pS + (int64_t)p * P + pix)) + ld(a.p + o)) - ld(a.u + o) * a.inv_c;
+            qzp = qz;
+        }
+        if (lx >= 0) Fp[sme] = f;   // (idle halo lanes have lx < 0 and no slot)
+        __syncthreads();
+        if (is_main && active && p > zc0) {
+            const int z = p - 1;
+            const float *Fz = F + (z % 3) * PS;
+            const float fc = Fz[sme];
+            const float gx = Fz[sme + 1] - fc, gy = Fz[sme + RS] - fc;
+            const float gz = f - fc;   // f(z+1) at the voxel; z + 1 <= nz - 1 here
+            const float sv = cap_at(a, L, z, pix, P);
+            float hx = fmaf(cx, gx, qcx), hy = fmaf(cy, gy, qcy), hz = fmaf(a.tau, gz, qcz);   // ascent step
+            project(a.cap, sv, hx, hy, hz);
+            float *qo = a.q_out + (int64_t)z * qps + pix;
+            qo[L * P] = hx;
+            qo[(a.NL + L) * P] = hy;
+            qo[(2 * a.NL + L) * P] = hz;
+        }
+        qcx = qx; qcy = qy; qcz = qz;
+    }
+    if (!has_above && is_main && active) {   // last plane of the volume: grad_z f = 0
+        const int z = zc1 - 1;
+        const float *Fz = F + (z % 3) * PS;
+        const float fc = Fz[sme];
+        const float gx = Fz[sme + 1] - fc, gy = Fz[sme + RS] - fc;
+        const float sv = cap_at(a, L, z, pix, P);
+        float hx = fmaf(cx, gx, qcx), hy = fmaf(cy, gy, qcy), hz = qcz;
+        project(a.cap, sv, hx, hy, hz);
+        float *qo = a.q_out + (int64_t)z * qps + pix;
+        qo[L * P] = hx;
+        qo[(a.NL + L) * P] = hy;
+        qo[(2 * a.NL + L) * P] = hz;
+    }
+}
+
+// Pass 2, every label of a voxel column per thread, z-march: div of the NEW flows, then p_L, p_S, u_L
+// in the oracle's order (p_L uses the old p_S; u uses the new p_S).  Residual max|u' - u| fused.
+template <int NL>
+__global__ void __launch_bounds__(128) alm_potential_kernel(const AlmArgs a) {
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * 4 + (threadIdx.x >> 5);
+    const bool valid = x < a.nx && y < a.ny;   // no early return: the residual reduction is warp-wide
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int64_t qps = (int64_t)3 * NL * P, ups = (int64_t)NL * P;
+    const int pix = valid ? y * a.pitch + x : 0;
+    const int zc0 = blockIdx.z * a.zchunk, zc1 = valid ? min(zc0 + a.zchunk, a.nz) : zc0;
+    const float invK = 1.0f / NL;
+    float qzp[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) qzp[l] = zc0 > 0 ? ld(a.q_out + (int64_t)(zc0 - 1) * qps + (2 * NL + l) * P + pix) : 0.f;
+    float resid = 0.f;
+    for (int z = zc0; z < zc1; ++z) {
+        const float *qb = a.q_out + (int64_t)z * qps + pix;
+        const int64_t o = (int64_t)z * ups + pix;
+        const float ps_old = ld(a.pS + (int64_t)z * P + pix);
+        float dq[NL], pn[NL], uo[NL];
+        float acc = 0.f;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+            const float qx = ld(qb + l * P), qy = ld(qb + (NL + l) * P), qz = ld(qb + (2 * NL + l) * P);
+            const float qxm = x > 0 ? ld(qb + l * P - 1) : 0.f;
+            const float qym = y > 0 ? ld(qb + (NL + l) * P - a.pitch) : 0.f;
+            dq[l] = ((qx - qxm) + (qy - qym)) + (qz - qzp[l]);
+            qzp[l] = qz;
+            uo[l] = ld(a.u + o + l * P);
+            pn[l] = fminf(load_D(a.D, o + l * P, a.d_bf16), (ps_old - dq[l]) + uo[l] * a.inv_c);
+            acc += (pn[l] + dq[l]) - uo[l] * a.inv_c;
+        }
+        const float ps = acc * invK + invK * a.inv_c;
+        a.pS[(int64_t)z * P + pix] = ps;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+            const float un = uo[l] - a.c * ((dq[l] - ps) + pn[l]);
+            a.p[o + l * P] = pn[l];
+            a.u[o + l * P] = un;
+            resid = fmaxf(resid, fabsf(un - uo[l]));
+        }
+    }
+    if (a.check) {
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) resid = fmaxf(resid, __shfl_xor_sync(0xffffffffu, resid, s));
+        if ((threadIdx.x & 31) == 0 && resid > 0.f) atomicMax(a.resid_bits, __float_as_uint(resid));
+    }
+}
+
+// p_S = min_L D_L, p_L = p_S (the oracle's start; u = 1/K and q = 0 are set by the caller).
+__global__ void alm_init_kernel(const AlmArgs a) {
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int64_t V = (int64_t)a.nx * a.ny * a.nz;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / ((int64_t)a.nx * a.ny);
+        const int r = (int)(i - z * (int64_t)a.nx * a.ny);
+        const int y = r / a.nx, x = r - y * a.nx;
+        const int64_t o = z * a.NL * P + (int64_t)y * a.pitch + x;
+        float m = FLT_MAX;
+        for (int l = 0; l < a.NL; ++l) m = fminf(m, load_D(a.D, o + l * P, a.d_bf16));
+        a.pS[z * P + (int64_t)y * a.pitch + x] = m;
+        for (int l = 0; l < a.NL; ++l) a.p[o + l * P] = m;
+    }
+}
+
+template <int NL>
+cudaError_t launch_pot(const AlmArgs &a, cudaStream_t st) {
+    dim3 grid((a.nx + 31) / 32, (a.ny + 3) / 4, (a.nz + a.zchunk - 1) / a.zchunk);
+    alm_potential_kernel<NL><<<grid, 128, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_alm_init(const AlmArgs &a, cudaStream_t st) {
+    alm_init_kernel<<<1184, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_alm_iteration(const AlmArgs &a, cudaStream_t st) {
+    const int nch = (a.nz + a.zchunk - 1) / a.zchunk;
+    dim3 g1((a.nx + 31) / 32, (a.ny + kAlmTY - 1) / kAlmTY, nch * a.NL);
+    alm_flow_kernel<<<g1, 32 * kAlmTY + 64, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    switch (a.NL) {
+        case 2: return launch_pot<2>(a, st);
+        case 3: return launch_pot<3>(a, st);
+        case 4: return launch_pot<4>(a, st);
+        case 5: return launch_pot<5>(a, st);
+        case 6: return launch_pot<6>(a, st);
+        case 7: return launch_pot<7>(a, st);
+        case 8: return launch_pot<8>(a, st);
+        case 9: return launch_pot<9>(a, st);
+        case 10: return launch_pot<10>(a, st);
+        case 11: return launch_pot<11>(a, st);
+        case 12: return launch_pot<12>(a, st);
+        case 13: return launch_pot<13>(a, st);
+        case 14: return launch_pot<14>(a, st);
+        case 15: return launch_pot<15>(a, st);
+        case 16: return launch_pot<16>(a, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace pf

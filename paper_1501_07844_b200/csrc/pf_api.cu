@@ -14,6 +14,7 @@
 #include <cuda.h>
 
 #include "pf.h"
+#include "pf_alm.cuh"
 #include "pf_aux.cuh"
 #include "pf_kernels.cuh"
 #include "pf_staged.cuh"
@@ -214,6 +215,8 @@ struct pf_solver {
     float *u_alloc[2] = {nullptr, nullptr}, *q_alloc[2] = {nullptr, nullptr};
     float *D_alloc = nullptr, *S_alloc = nullptr;   // D_alloc: fp32 D (nullptr when D is stored as bf16)
     uint16_t *D16 = nullptr;                          // bf16 D (cfg.d_bf16), same [z][l][y][pitch] layout
+    bool alm = false;                                 // PF_METHOD_EXPLICIT_ALM (pf_alm.cu)
+    float *p_alloc = nullptr, *pS_alloc = nullptr;    // ALM sink flows [z][l][y][pitch], source flow [z][y][pitch]
     const void *Dptr() const { return D16 ? (const void *)D16 : (const void *)D_alloc; }
     float *u[2] = {nullptr, nullptr}, *q[2] = {nullptr, nullptr};
     int cur = 0;
@@ -281,6 +284,7 @@ void pool_setup(int dev) {
 
 void free_all(pf_solver *s) {
     void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc, s->D16,
+                    s->p_alloc, s->pS_alloc,
                     s->d_resid, s->d_err, s->d_flag, s->d_energy};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, s->stream);
@@ -288,6 +292,7 @@ void free_all(pf_solver *s) {
     for (int i = 0; i < 2; ++i) s->u_alloc[i] = s->q_alloc[i] = nullptr;
     s->D_alloc = s->S_alloc = nullptr;
     s->D16 = nullptr;
+    s->p_alloc = s->pS_alloc = nullptr;
     s->d_resid = nullptr;
     s->d_err = nullptr;
     s->d_flag = nullptr;
@@ -304,8 +309,47 @@ pf_status alloc(pf_solver *s, void **p, size_t bytes, const char *what) {
     return PF_OK;
 }
 
+AlmArgs alm_args(pf_solver *s, int check) {
+    AlmArgs a;
+    memset(&a, 0, sizeof(a));
+    a.q_in = s->q[s->cur];
+    a.q_out = s->q[1 - s->cur];
+    a.u = s->u[0];
+    a.p = s->p_alloc;
+    a.pS = s->pS_alloc;
+    a.D = s->Dptr();
+    a.d_bf16 = s->D16 ? 1 : 0;
+    a.S = s->S_alloc;
+    a.s_per_node = s->s_kind == PF_S_FIELD_PER_NODE ? 1 : 0;
+    a.cap = s->cfg.cap;
+    a.check = check;
+    a.nx = (int)s->nx;
+    a.ny = (int)s->ny;
+    a.nz = (int)s->nzl;
+    a.pitch = (int)s->pitch;
+    a.NL = s->gc.NL;
+    a.zchunk = 32;
+    a.c = s->cfg.c;
+    a.inv_c = 1.0f / s->cfg.c;
+    a.tau = s->cfg.tau;
+    for (int l = 0; l < s->gc.NL && l < 16; ++l) a.s[l] = s->gc.g.s[l];
+    a.resid_bits = s->d_resid;
+    return a;
+}
+
+
 pf_status init_state(pf_solver *s) {
     const int64_t nu = (s->nzl + 2) * ups(s), nq = (s->nzl + 2) * qps(s);
+    if (s->alm) {  // u = 1/K, q = 0, p_S = min_L D_L, p_L = p_S (oracle/alm.py potts_alm)
+        CK(launch_fill(s->u_alloc[0], nu, 1.0f / (float)s->gc.NL, s->stream), "init u");
+        for (int i = 0; i < 2; ++i) CK(cudaMemsetAsync(s->q_alloc[i], 0, nq * sizeof(float), s->stream), "init q");
+        CK(launch_alm_init(alm_args(s, 0), s->stream), "ALM init");
+        s->launches += 2;
+        CK(cudaMemsetAsync(s->d_err, 0xff, sizeof(unsigned long long), s->stream), "init err");
+        s->cur = 0;
+        s->iters = 0;
+        return PF_OK;
+    }
     for (int i = 0; i < 2; ++i) {
         CK(launch_fill(s->u_alloc[i], nu, 1.0f / (float)s->gc.NL, s->stream), "init u");
         s->launches++;
@@ -499,8 +543,15 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
                                         "(<= %d internal, <= %d non-source nodes)", gc.NI, gc.NL, kMaxInternal,
                     kMaxNodes);
     gc.NF = gc.model == 1 ? gc.NI : gc.NV;
+    if (cfg->method != PF_METHOD_PSEUDO_FLOW && cfg->method != PF_METHOD_EXPLICIT_ALM)
+        return fail(PF_ERR_INVALID, "config: bad method");
+    const bool alm = cfg->method == PF_METHOD_EXPLICIT_ALM;
+    if (alm && (gc.model != 0 || gc.NI != 0 || gc.NL > 16 || slab || S->kind == PF_S_SCALED_FIELD))
+        return fail(PF_ERR_UNSUPPORTED, "explicit-flow ALM: Potts graphs (<= 16 labels), whole volumes, scalar, "
+                                        "shared or per-label capacities only");
 
     pf_solver *s = new pf_solver();
+    s->alm = alm;
     cudaGetDevice(&s->device);
     s->ndim = dims->ndim;
     s->nx = dims->nx;
@@ -522,7 +573,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     {
         const char *env = getenv("PF_ITER_KERNEL");
         const bool want_global = env && strcmp(env, "global") == 0;
-        s->staged = !want_global && staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, &s->sinfo) && encode_fn() != nullptr;
+        s->staged = !alm && !want_global && staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, &s->sinfo) && encode_fn() != nullptr;
         if (s->staged) {
             const int s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD)
                                  ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NF : 0);
@@ -552,14 +603,23 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         g_last_error = msg;
         return st2;
     };
-    // state: planes -1 .. nzl (halo below / above)
+    // state: planes -1 .. nzl (halo below / above); the ALM updates u in place (one buffer) and stores p, p_S
     for (int i = 0; i < 2; ++i) {
-        if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u")) != PF_OK)
+        if (alm && i == 1) {
+            s->u_alloc[1] = nullptr;
+        } else if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u")) != PF_OK) {
             return bail(st);
+        }
         if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * 3 * NF * P) * sizeof(float), "q")) != PF_OK)
             return bail(st);
-        s->u[i] = s->u_alloc[i] + NL * P;
+        s->u[i] = (alm ? s->u_alloc[0] : s->u_alloc[i]) + NL * P;
         s->q[i] = s->q_alloc[i] + (int64_t)3 * NF * P;
+    }
+    if (alm) {
+        if ((st = alloc(s, (void **)&s->p_alloc, (size_t)(nzl * NL * P) * sizeof(float), "ALM p")) != PF_OK)
+            return bail(st);
+        if ((st = alloc(s, (void **)&s->pS_alloc, (size_t)(nzl * P) * sizeof(float), "ALM p_S")) != PF_OK)
+            return bail(st);
     }
     const int64_t nzD = std::min(z1 + 1, dims->nz) - z0;  // owned + static halo plane above
     if ((st = alloc(s, (void **)&s->D_alloc, (size_t)((nzl + 1) * NL * P) * sizeof(float), "D")) != PF_OK)
@@ -810,7 +870,12 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
             CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
             any_check = true;
         }
-        if ((st = launch_items(s, 0, s->items, check)) != PF_OK) return st;
+        if (s->alm) {
+            CK(launch_alm_iteration(alm_args(s, check), s->stream), "ALM iteration");
+            s->launches += 2;
+        } else if ((st = launch_items(s, 0, s->items, check)) != PF_OK) {
+            return st;
+        }
         s->cur = 1 - s->cur;
         s->iters += 1;
     }
@@ -846,6 +911,7 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
     if (phase != 0 && phase != 1) return fail(PF_ERR_INVALID, "phase must be 0 or 1");
+    if (s->alm) return fail(PF_ERR_UNSUPPORTED, "pf_iterate_phase: not for the explicit-flow ALM");
     if ((phase == 0) == (s->phase_pending != 0))
         return fail(PF_ERR_STATE, phase == 0 ? "phase 0 issued twice" : "phase 1 without phase 0");
     DeviceGuard dg(s->device);
@@ -1061,6 +1127,8 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     // its flow r/w
     const int64_t per_leaf = 4 + 4 + (s->D16 ? 2 : 4), per_flow = 8 * s->ndim;
     int64_t b = V * (per_leaf * s->gc.NL + per_flow * s->gc.NF);
+    if (s->alm)  // pass 1: q r/w, p r, u r (+ p_S r); pass 2: q r, D r, p w, u r/w (+ p_S r/w)  (pf_alm.cu)
+        b = V * ((int64_t)s->gc.NL * (8 * s->ndim + 4 + 4 + 4 * s->ndim + (s->D16 ? 2 : 4) + 4 + 8) + 12);
     if (s->s_kind == PF_S_SHARED_FIELD || s->s_kind == PF_S_SCALED_FIELD) b += 4 * V;
     if (s->s_kind == PF_S_FIELD_PER_NODE) b += 4 * V * s->gc.NF;
     info->algorithmic_bytes_per_iteration = b;

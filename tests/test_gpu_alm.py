@@ -1,0 +1,75 @@
+"""Explicit-flow ALM comparison arm (pf_config.method = PF_METHOD_EXPLICIT_ALM) against
+the independent oracle oracle/alm.py potts_alm (fp64), same seeded inputs, same iteration count."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1501_07844_b200 as pf
+import phantoms as P
+from helpers import compare, solver_from_inputs
+from oracle import alm as A
+
+pytestmark = pytest.mark.gpu
+
+CA, TA = 0.3, 0.11
+
+
+def _oracle(inp, n, cap):
+    K = inp.D.shape[0]
+    if inp.s_kind == "shared_field":
+        S = np.repeat(inp.s_field[None].astype(np.float64), K, axis=0)
+    else:
+        S = np.stack([np.full(inp.shape, float(inp.s_scalars[1 + l])) for l in range(K)])
+    return A.potts_alm(inp.D, S, inp.cfg.ndim, n, ca=CA, ta=TA, cap=cap)
+
+
+@pytest.mark.parametrize("name,dims,n,cap", [
+    ("C1", (64, 64, 1), 150, "l2"),
+    ("C2", (37, 29, 21), 100, "l2"),       # ragged tiles / z-chunks, edge-weighted shared S field
+    ("C5", (24, 20, 40), 60, "l2"),        # K = 16, two z-chunks
+    ("C1", (40, 33, 1), 120, "linf"),
+])
+def test_alm_matches_oracle(name, dims, n, cap):
+    inp = P.generate(P.config(name).resized(*dims))
+    s = solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM, c=CA, tau=TA, cap=0 if cap == "l2" else 1)
+    s.iterate(n)
+    u, am = s.labeling()
+    q = s.flows()
+    s.close()
+    ur, qr, _ = _oracle(inp, n, cap)
+    compare(u, q, ur, qr)
+    assert np.array_equal(am, O.argmax(u))
+
+
+def test_alm_and_pseudo_flow_reach_the_same_labeling():
+    """Both methods solve the same convex relaxation (Eq. 1 / Eq. 3): at convergence the thresholded
+    labelings agree and the energies match (the paper's claim that the pseudo-flow needs less memory
+    is only meaningful because of this)."""
+    inp = P.generate(P.config("C1").resized(48, 40, 1))
+    a = solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM, c=CA, tau=TA)
+    b = solver_from_inputs(inp)
+    a.iterate(6000)
+    b.iterate(6000)
+    ua, ama = a.labeling()
+    ub, amb = b.labeling()
+    ea, eb = a.energy(), b.energy()
+    assert float(np.mean(ama == amb)) >= 0.999
+    assert abs(ea[0] - eb[0]) <= 1e-3 * abs(eb[0])
+    a.close()
+    b.close()
+
+
+def test_alm_rejects_unsupported():
+    inp = P.generate(P.config("C3").resized(20, 20, 8))   # HMF tree: not a Potts graph
+    with pytest.raises(pf.PFError) as ei:
+        solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM)
+    assert ei.value.status == pf.PF_ERR_UNSUPPORTED
+    inp = P.generate(P.config("C2").resized(20, 20, 8))
+    with pytest.raises(pf.PFError) as ei:
+        solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM, slab=(0, 4))
+    assert ei.value.status == pf.PF_ERR_UNSUPPORTED
+    s = solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM)
+    with pytest.raises(pf.PFError) as ei:
+        s.iterate_phase(0)
+    assert ei.value.status == pf.PF_ERR_UNSUPPORTED
+    s.close()

@@ -31,6 +31,8 @@ def main():
     ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5slab", "I2"])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--oracle", action="store_true")
+    ap.add_argument("--d-bf16", action="store_true", help="store D as bf16 (pf_config.d_bf16)")
+    ap.add_argument("--alm", action="store_true", help="explicit-flow ALM comparison arm (Potts configs)")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -48,8 +50,13 @@ def main():
             kw = {"s_shared": torch.from_numpy(inp.s_field).to(dev)}
         else:
             kw = {"s_scalars": inp.s_scalars}
-        s = pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.child, g.weight), D, c=cfg.c,
-                      tau=cfg.tau, check_every=10, **kw)
+        extra = {"d_bf16": args.d_bf16}
+        c, tau = cfg.c, cfg.tau
+        if args.alm:
+            extra["method"] = pf.PF_METHOD_EXPLICIT_ALM
+            c, tau = 0.3, 0.11   # oracle/alm.py potts_alm defaults
+        s = pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.child, g.weight), D, c=c,
+                      tau=tau, check_every=10, **extra, **kw)
         stream = torch.cuda.current_stream(dev)
         s.set_stream(stream.cuda_stream)
         labels = torch.empty((cfg.nz, cfg.ny, cfg.nx), dtype=torch.uint8, device=dev)
@@ -81,7 +88,9 @@ def main():
         r = s.iterate(0, True)
         e, f = s.energy()
         s.close()
-        line = {"config": name, "dims": [cfg.nx, cfg.ny, cfg.nz], "end_labels": NL, "nodes": g.num_nodes - 1,
+        line = {"config": name, "method": "explicit-flow ALM" if args.alm else "pseudo-flow",
+                "d_dtype": "bf16" if args.d_bf16 else "f32",
+                "dims": [cfg.nx, cfg.ny, cfg.nz], "end_labels": NL, "nodes": g.num_nodes - 1,
                 "iterations": n, "ms_per_solve": ms, "ms_per_iteration": it_ms,
                 "gvl_it_per_s": V * NL * n / (ms / 1e3) / 1e9,
                 "gvnode_it_per_s": V * (g.num_nodes - 1) * n / (ms / 1e3) / 1e9,
