@@ -5,7 +5,7 @@
 // and sink flows p_S, p_L implicit.  This is the classic alternative that stores them: block-coordinate
 // ascent on the augmented Lagrangian of Eq. 3 with u as the multipliers,
 //   L_c = p_S + sum_L u_L r_L - c/2 sum_L r_L^2,   r_L = div q_L - p_S + p_L,   p_L <= D_L, |q_L| <= S_L,
-// one sweep per iteration in the order of oracle/alm.py potts_alm (the labels are independent given p_S):
+// one sweep per iteration in block-coordinate order (q, then p, then p_S, then u) (the labels are independent given p_S):
 //   q_L  <- Proj_{|q| <= S_L}( q_L + tau grad(div q_L - p_S + p_L - u_L / c) )     [alm_flow_kernel]
 //   p_L  <- min(D_L, p_S - div q_L + u_L / c)              (new q)                  [alm_potential_kernel]
 //   p_S  <- (sum_L (p_L + div q_L - u_L / c)) / K + 1 / (K c)
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(32 * kAlmTY + 64) alm_flow_kernel(const AlmArg
 }
 
 // Pass 2, every label of a voxel column per thread, z-march: div of the NEW flows, then p_L, p_S, u_L
-// in the oracle's order (p_L uses the old p_S; u uses the new p_S).  Residual max|u' - u| fused.
+// in that order (p_L uses the old p_S; u uses the new p_S).  Residual max|u' - u| fused.
 template <int NL>
 __global__ void __launch_bounds__(128) alm_potential_kernel(const AlmArgs a) {
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(128) alm_potential_kernel(const AlmArgs a) {
     }
 }
 
-// p_S = min_L D_L, p_L = p_S (the oracle's start; u = 1/K and q = 0 are set by the caller).
+// p_S = min_L D_L, p_L = p_S (the standard start; u = 1/K and q = 0 are set by the caller).
 __global__ void alm_init_kernel(const AlmArgs a) {
     const int64_t P = (int64_t)a.pitch * a.ny;
     const int64_t V = (int64_t)a.nx * a.ny * a.nz;

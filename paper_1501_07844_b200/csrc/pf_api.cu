@@ -340,7 +340,7 @@ AlmArgs alm_args(pf_solver *s, int check) {
 
 pf_status init_state(pf_solver *s) {
     const int64_t nu = (s->nzl + 2) * ups(s), nq = (s->nzl + 2) * qps(s);
-    if (s->alm) {  // u = 1/K, q = 0, p_S = min_L D_L, p_L = p_S (oracle/alm.py potts_alm)
+    if (s->alm) {  // u = 1/K, q = 0, p_S = min_L D_L, p_L = p_S
         CK(launch_fill(s->u_alloc[0], nu, 1.0f / (float)s->gc.NL, s->stream), "init u");
         for (int i = 0; i < 2; ++i) CK(cudaMemsetAsync(s->q_alloc[i], 0, nq * sizeof(float), s->stream), "init q");
         CK(launch_alm_init(alm_args(s, 0), s->stream), "ALM init");
