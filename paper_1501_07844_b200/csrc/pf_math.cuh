@@ -59,17 +59,20 @@ __device__ __forceinline__ float label_update(const float (&d)[NI + NL], const f
 #pragma unroll
         for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
     }
-    // a = (sum of the first NL/2 masses) + (sum of the rest): the order a label-split kernel (two warps per
-    // voxel row, pf_staged.cuh G = 2) also uses, so every variant rounds identically
-    constexpr int H = NL / 2;
-    float s0 = 0.f, s1 = 0.f;
+    // a = (q0 + q1) + (q2 + q3), q_i = sequential sum of the i-th quarter of the labels (quarters = halves
+    // of halves): the order the label-split kernels (2 or 4 warps per voxel row, pf_staged.cuh G = 2, 4)
+    // also use, so every variant rounds identically
+    constexpr int H = NL / 2, Q1 = H / 2, Q3 = H + (NL - H) / 2;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
         ut[l] = uold[l] * ex2_approx((m - d[NI + l]) * k2);
-        if (l < H) s0 += ut[l];
-        else s1 += ut[l];
+        if (l < Q1) s0 += ut[l];
+        else if (l < H) s1 += ut[l];
+        else if (l < Q3) s2 += ut[l];
+        else s3 += ut[l];
     }
-    const float sum = s0 + s1;
+    const float sum = (s0 + s1) + (s2 + s3);
     const float inv = __frcp_rn(sum);
 #pragma unroll
     for (int l = 0; l < NL; ++l) {

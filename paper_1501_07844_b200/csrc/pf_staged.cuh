@@ -79,7 +79,7 @@ struct StagedLayout {
     static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // u staging [l][row][32], x2
     static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;   // q staging: OSTAGE 1 [ch][row][32] x2,
     static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         //   OSTAGE 2 [row][grp][k][f][32] x1
-    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // m / a exchange (G = 2)
+    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // m / a exchange (G = 2, 4)
     static constexpr int kThreads = 32 * G * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
@@ -158,7 +158,7 @@ template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF>
 __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
     constexpr int NF = L::NF;
-    static_assert(G == 1 || (MODEL == 0 && NI == 0 && NL % G == 0), "label split only for Potts");
+    static_assert(G == 1 || ((G == 2 || G == 4) && MODEL == 0 && NI == 0 && NL % G == 0), "label split: Potts");
     constexpr int NLG = NL / G;   // end labels of this thread's group
     constexpr int NFG = NF / G;   // flow nodes of this thread's group
     constexpr int QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
@@ -364,21 +364,26 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                 if (a.shift == 0) {
                     xm[grp * 32] = mpart;
                     named_bar(1 + xr, 32 * G);
-                    mpart = fminf(xm[0], xm[32]);
+                    mpart = xm[0];
+#pragma unroll
+                    for (int g = 1; g < G; ++g) mpart = fminf(mpart, xm[g * 32]);
                 } else {
                     mpart = 0.f;
                 }
-                float spart = 0.f;
+                // partial sums in label_update's quarter order: G = 2 forms (quarter + quarter) per group
+                float sa = 0.f, sb = 0.f;
                 if (lx >= 0) {
 #pragma unroll
                     for (int l = 0; l < NLG; ++l) {
                         ut[l] = uold[l] * ex2_approx((mpart - dlab[l]) * k2);
-                        spart += ut[l];
+                        if (G == 2 && l >= NLG / 2) sb += ut[l];
+                        else sa += ut[l];
                     }
                 }
-                xa[grp * 32] = spart;
+                xa[grp * 32] = G == 2 ? sa + sb : sa;
                 named_bar(1 + xr, 32 * G);
-                sum = xa[0] + xa[32];
+                if constexpr (G == 2) sum = xa[0] + xa[32];
+                else sum = (xa[0] + xa[32]) + (xa[64] + xa[96]);
                 const float inv = __frcp_rn(sum);
 #pragma unroll
                 for (int l = 0; l < NLG; ++l) {

@@ -17,7 +17,7 @@ import numpy as np  # noqa: E402
 
 import oracle as O  # noqa: E402
 import phantoms as P  # noqa: E402
-from helpers import solver_from_inputs, window_oracle  # noqa: E402
+from helpers import bf16_rounded, solver_from_inputs, window_oracle  # noqa: E402
 
 
 def full_case(name, dims, n, shift):
@@ -36,6 +36,37 @@ def full_case(name, dims, n, shift):
             "max_abs_du": float(np.max(np.abs(u - ur))), "max_abs_dq": float(np.max(np.abs(q - qr))),
             "argmax_agree": float(np.mean(am == O.argmax(ur))), "voxels": int(cfg.V),
             "kernel_staged": info["staged"], "oracle_s": round(dt, 2)}
+
+
+def bf16_case(name, dims, n):
+    inp = bf16_rounded(P.generate(P.config(name).resized(*dims)))
+    s = solver_from_inputs(inp, d_bf16=True)
+    s.iterate(n)
+    u, am = s.labeling()
+    q = s.flows()
+    s.close()
+    ur, qr = O.run_inputs(inp, n)
+    return {"case": f"{name} {dims[0]}x{dims[1]}x{dims[2]} D stored as bf16 (oracle on bf16-rounded D)",
+            "iterations": n, "max_abs_du": float(np.max(np.abs(u - ur))), "max_abs_dq": float(np.max(np.abs(q - qr))),
+            "argmax_agree": float(np.mean(am == O.argmax(ur)))}
+
+
+def alm_case(name, dims, n):
+    import paper_1501_07844_b200 as pf
+    from oracle import alm as A
+    inp = P.generate(P.config(name).resized(*dims))
+    s = solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM, c=0.3, tau=0.11)
+    s.iterate(n)
+    u, am = s.labeling()
+    q = s.flows()
+    s.close()
+    K = inp.D.shape[0]
+    S = (np.repeat(inp.s_field[None].astype(np.float64), K, axis=0) if inp.s_kind == "shared_field" else
+         np.stack([np.full(inp.shape, float(inp.s_scalars[1 + l])) for l in range(K)]))
+    ur, qr, _ = A.potts_alm(inp.D, S, inp.cfg.ndim, n, ca=0.3, ta=0.11)
+    return {"case": f"{name} {dims[0]}x{dims[1]}x{dims[2]} explicit-flow ALM vs oracle/alm.py", "iterations": n,
+            "max_abs_du": float(np.max(np.abs(u - ur))), "max_abs_dq": float(np.max(np.abs(q - qr))),
+            "argmax_agree": float(np.mean(am == np.argmax(ur, axis=0)))}
 
 
 def sampled_case(name, n=6):
@@ -71,5 +102,9 @@ if __name__ == "__main__":
              ("C5", (40, 36, 24), 200, 0), ("I2", (48, 40, 36), 300, 0), ("I2", (37, 29, 19), 300, 1)]
     for c in cases:
         print(json.dumps(full_case(*c)), flush=True)
+    for c in [("C2", (67, 45, 37), 300), ("C5", (40, 36, 24), 200)]:
+        print(json.dumps(bf16_case(*c)), flush=True)
+    for c in [("C1", (64, 64, 1), 200), ("C2", (37, 29, 21), 100)]:
+        print(json.dumps(alm_case(*c)), flush=True)
     for name in ("C2", "C3", "C4", "C5slab", "I2"):
         print(json.dumps(sampled_case(name)), flush=True)
