@@ -18,6 +18,7 @@
 #include "pf_aux.cuh"
 #include "pf_kernels.cuh"
 #include "pf_staged.cuh"
+#include "pf_cluster.cuh"
 
 using namespace pf;
 
@@ -236,6 +237,7 @@ struct pf_solver {
     int64_t launches = 0;
     // TMA-staged persistent kernel (default) -- see pf_staged.cuh
     bool staged = false;
+    bool cluster = false;   // staged work split over a 2-CTA cluster (pf_cluster.cuh; Potts, many labels)
     StagedKernelInfo sinfo{};
     CUtensorMap tm_q[2], tm_u[2], tm_D, tm_S, tm_qo[2], tm_uo[2];
     int staged_smem = 0;
@@ -394,14 +396,15 @@ void choose_chunking(pf_solver *s) {
         s->zlo = below ? 1 : 0;
         s->zhi = std::max(s->zlo, (above ? nzl - 1 : nzl));
         const int nzi = s->zhi - s->zlo;
-        const int n = nzi > 0 ? best_chunks(tiles, nzi, slots) : 0;
+        const int64_t wslots = s->cluster ? slots / 2 : slots;   // concurrent work items
+        const int n = nzi > 0 ? best_chunks(tiles, nzi, wslots) : 0;
         s->zchunk = nzi > 0 ? (nzi + n - 1) / n : 1;
         const int nch = nzi > 0 ? (nzi + s->zchunk - 1) / s->zchunk : 0;
         s->tiles_x = gx;
         s->tiles = (int)tiles;
         s->items_b = (int)(tiles * s->nb);
         s->items = (int)(tiles * (s->nb + nch));
-        s->sgrid = (int)std::min<int64_t>(slots, s->items);
+        s->sgrid = (int)std::min<int64_t>(slots, (int64_t)s->items * (s->cluster ? 2 : 1));
         s->grid = dim3(s->sgrid, 1, 1);
     } else {
         const int n = best_chunks(tiles, nzl, sms);
@@ -574,6 +577,16 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         const char *env = getenv("PF_ITER_KERNEL");
         const bool want_global = env && strcmp(env, "global") == 0;
         s->staged = !alm && !want_global && staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, &s->sinfo) && encode_fn() != nullptr;
+        // Potts with many labels: the 2-CTA cluster split (scalar / shared capacities; PF_CLUSTER=0 disables)
+        const char *cenv = getenv("PF_CLUSTER");
+        if (s->staged && gc.model == 0 && gc.NI == 0 && S->kind != PF_S_FIELD_PER_NODE &&
+            !(cenv && strcmp(cenv, "0") == 0)) {
+            StagedKernelInfo ci{};
+            if (cluster_kernel_lookup(gc.NL, cfg->d_bf16 ? 1 : 0, &ci)) {
+                s->sinfo = ci;
+                s->cluster = true;
+            }
+        }
         if (s->staged) {
             const int s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD)
                                  ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NF : 0);
@@ -701,26 +714,30 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         s->s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD) ? 1
                                                                                    : (S->kind == PF_S_FIELD_PER_NODE ? NF : 0);
         bool ok = true;
+        // boxes: the cluster kernel's CTAs stage half of the labels (channel boxes of NL/2, three q loads)
+        const int cq = s->cluster ? NL / 2 : 3 * NF, cl = s->cluster ? NL / 2 : NL;
         for (int i = 0; i < 2; ++i) {
             ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 40,
-                                ty + 2, 3 * NF);
-            ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, NL);
+                                ty + 2, cq);
+            ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, cl);
         }
         for (int i = 0; i < 2; ++i) {
             // OSTAGE 2 stores one flow row per warp, OSTAGE 1 the whole tile
             ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 32,
-                                s->sinfo.ostage == 2 ? 1 : ty, s->sinfo.ostage == 2 ? NF / s->sinfo.groups : 3 * NF);
-            ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, NL);
+                                s->sinfo.ostage == 2 ? 1 : ty,
+                                s->sinfo.ostage == 2 ? NF / s->sinfo.groups : (s->cluster ? NL / 2 : 3 * NF));
+            ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, cl);
         }
         if (s->D16)  // bf16 rows: a 40-element (80-byte) box keeps the 16-byte box-width rule
-            ok = ok && encode4d(&s->tm_D, s->D16, s->nx, s->ny, s->pitch, NL, nzl + 1, 40, ty + 1, NL, true);
+            ok = ok && encode4d(&s->tm_D, s->D16, s->nx, s->ny, s->pitch, NL, nzl + 1, 40, ty + 1, cl, true);
         else
-            ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, NL);
+            ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, cl);
         if (s->s_ch) ok = ok && encode4d(&s->tm_S, s->S_alloc, s->nx, s->ny, s->pitch, s->s_ch, nzl, 32, ty, s->s_ch);
         else memset(&s->tm_S, 0, sizeof(s->tm_S));
         if (!ok) return bail(fail(PF_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
-        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * NF + 36 * (ty + 1) * NL + 32 * ty * s->s_ch) +
-                                 (s->D16 ? 2 * 40 : 4 * 36) * (ty + 1) * NL);
+        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * (s->cluster ? NL / 2 : NF) + 36 * (ty + 1) * cl +
+                                      32 * ty * s->s_ch) +
+                                 (s->D16 ? 2 * 40 : 4 * 36) * (ty + 1) * cl);
     }
     choose_chunking(s);
     e = cudaStreamSynchronize(s->stream);
@@ -794,11 +811,13 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
         sa.check = check;
         sa.ticket = s->d_err + 1;
         sa.ticket_base = s->ticket_base;
-        const int grid = (int)std::min<int64_t>(s->sgrid, ie - ib);
+        // cluster kernel: 2 CTAs per item and one ticket grab per cluster
+        const int per = s->cluster ? 2 : 1;
+        const int grid = (int)std::min<int64_t>(s->sgrid / per, ie - ib) * per;
         void *args[] = {(void *)&sa};
         CK(cudaLaunchKernel(s->sinfo.func, dim3(grid), dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
-           "launch pf_iter_staged");
-        s->ticket_base += (uint64_t)(ie - ib) + (uint64_t)grid;  // every launch consumes items + grid tickets
+           s->cluster ? "launch pf_iter_cluster" : "launch pf_iter_staged");
+        s->ticket_base += (uint64_t)(ie - ib) + (uint64_t)(grid / per);  // items + one failed grab per launcher
     } else {
         IterArgs a;
         memset(&a, 0, sizeof(a));

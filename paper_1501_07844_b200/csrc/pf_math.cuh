@@ -50,29 +50,69 @@ __device__ __forceinline__ void st_stream(float *p, float v) {
 // with u' below the fp32 normal range flushed to 0 (reading R18: u is stored in fp32).
 // d[NI..NI+NL) holds the end-label excesses on entry; ut receives u~ (the unnormalised masses).
 // Returns a; writes u' to unew.
+//
+// Summation order: a = (q0 + q1) + (q2 + q3), q_i the sequential sum of the i-th quarter of the labels
+// (quarters = halves of halves).  With many labels (NL >= kHalfSplitNL) the two halves are shifted
+// separately and rescaled (the "online softmax" identity exp(-(d-m)/c) = exp(-(d-m_h)/c) exp(-(m_h-m)/c)):
+//   m_h = min over half h, u~^h_L = u_L exp(-(d_L - m_h)/c), a_h = quarter + quarter,
+//   f_h = exp(-(m_h - m)/c), a = a_1 f_1 + a_0 f_0 (one fma), u~_L = u~^h_L f_h,
+// which is the arithmetic of the label-split kernels (two warps or two CTAs per voxel row exchange only
+// (m_h, a_h), once), so every variant rounds identically.
+constexpr int kHalfSplitNL = 10;
+
+__device__ __forceinline__ float halves_sum(float a0, float f0, float a1, float f1) { return fmaf(a1, f1, a0 * f0); }
+
 template <int NI, int NL>
 __device__ __forceinline__ float label_update(const float (&d)[NI + NL], const float (&uold)[NL], float (&ut)[NL],
                                               float (&unew)[NL], int shift, float k2 /* log2(e)/c */) {
-    float m = 0.f;
-    if (shift == 0) {
-        m = d[NI];
-#pragma unroll
-        for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
-    }
-    // a = (q0 + q1) + (q2 + q3), q_i = sequential sum of the i-th quarter of the labels (quarters = halves
-    // of halves): the order the label-split kernels (2 or 4 warps per voxel row, pf_staged.cuh G = 2, 4)
-    // also use, so every variant rounds identically
     constexpr int H = NL / 2, Q1 = H / 2, Q3 = H + (NL - H) / 2;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    float sum;
+    if constexpr (NL >= kHalfSplitNL) {
+        float m0 = 0.f, m1 = 0.f;
+        if (shift == 0) {
+            m0 = d[NI];
 #pragma unroll
-    for (int l = 0; l < NL; ++l) {
-        ut[l] = uold[l] * ex2_approx((m - d[NI + l]) * k2);
-        if (l < Q1) s0 += ut[l];
-        else if (l < H) s1 += ut[l];
-        else if (l < Q3) s2 += ut[l];
-        else s3 += ut[l];
+            for (int l = 1; l < H; ++l) m0 = fminf(m0, d[NI + l]);
+            m1 = d[NI + H];
+#pragma unroll
+            for (int l = H + 1; l < NL; ++l) m1 = fminf(m1, d[NI + l]);
+        }
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+            ut[l] = uold[l] * ex2_approx(((l < H ? m0 : m1) - d[NI + l]) * k2);
+            if (l < Q1) s0 += ut[l];
+            else if (l < H) s1 += ut[l];
+            else if (l < Q3) s2 += ut[l];
+            else s3 += ut[l];
+        }
+        float f0 = 1.f, f1 = 1.f;
+        if (shift == 0) {
+            const float m = fminf(m0, m1);
+            f0 = ex2_approx((m - m0) * k2);
+            f1 = ex2_approx((m - m1) * k2);
+        }
+        sum = halves_sum(s0 + s1, f0, s2 + s3, f1);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) ut[l] *= (l < H ? f0 : f1);
+    } else {
+        float m = 0.f;
+        if (shift == 0) {
+            m = d[NI];
+#pragma unroll
+            for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
+        }
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+            ut[l] = uold[l] * ex2_approx((m - d[NI + l]) * k2);
+            if (l < Q1) s0 += ut[l];
+            else if (l < H) s1 += ut[l];
+            else if (l < Q3) s2 += ut[l];
+            else s3 += ut[l];
+        }
+        sum = (s0 + s1) + (s2 + s3);
     }
-    const float sum = (s0 + s1) + (s2 + s3);
     const float inv = __frcp_rn(sum);
 #pragma unroll
     for (int l = 0; l < NL; ++l) {

@@ -26,8 +26,8 @@
 //   * G = 2 (Potts with many labels): the labels of a row of 32 voxels are split over a warp pair, which
 //     doubles the warps per SM at the same shared-memory footprint and halves the registers per thread;
 //     the only per-voxel couplings of the label update -- m = min_L d_L and a = sum_L u~_L -- are
-//     exchanged through shared memory under a 64-thread named barrier.  The sum is always formed as
-//     (first half) + (second half) (also for G = 1, see label_update), so G does not change a bit.
+//     combined from per-half (shift, sum) pairs exchanged once through shared memory under a 64-thread named
+//     barrier -- label_update's split form (pf_math.cuh), so G does not change a bit.
 #pragma once
 #include <cuda.h>
 
@@ -79,7 +79,7 @@ struct StagedLayout {
     static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // u staging [l][row][32], x2
     static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;   // q staging: OSTAGE 1 [ch][row][32] x2,
     static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         //   OSTAGE 2 [row][grp][k][f][32] x1
-    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // m / a exchange (G = 2, 4)
+    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // (m_h, a_h) exchange (G = 2)
     static constexpr int kThreads = 32 * G * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
@@ -158,7 +158,7 @@ template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF>
 __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
     constexpr int NF = L::NF;
-    static_assert(G == 1 || ((G == 2 || G == 4) && MODEL == 0 && NI == 0 && NL % G == 0), "label split: Potts");
+    static_assert(G == 1 || (G == 2 && MODEL == 0 && NI == 0 && NL % 2 == 0), "label split: Potts, two halves");
     constexpr int NLG = NL / G;   // end labels of this thread's group
     constexpr int NFG = NF / G;   // flow nodes of this thread's group
     constexpr int QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
@@ -350,43 +350,44 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                     sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
                 }
             } else {
-                // Potts, labels l0 .. l0+NLG-1: d_L = D_L + div q_L; m and a exchanged with the partner warp
+                // Potts, labels l0 .. l0+NLG-1 = half `grp` of the labels (NL >= kHalfSplitNL): local shift
+                // m_h, local masses and a_h = quarter + quarter, then ONE exchange of (m_h, a_h) with the
+                // partner warp and the rescale of label_update's split form (pf_math.cuh)
+                static_assert(G == 2 && NL >= kHalfSplitNL, "label split = label_update's two halves");
                 float *xm = X + (xr * G) * 32 + lane;
                 float *xa = X + ((TY + 2) * G + xr * G) * 32 + lane;
-                float mpart = 0.f;
+                float mh = 0.f, sa = 0.f, sb = 0.f;
                 if (lx >= 0) {
 #pragma unroll
                     for (int l = 0; l < NLG; ++l) dlab[l] = Dv[l] + dq[l];
-                    mpart = dlab[0];
+                    if (a.shift == 0) {
+                        mh = dlab[0];
 #pragma unroll
-                    for (int l = 1; l < NLG; ++l) mpart = fminf(mpart, dlab[l]);
-                }
-                if (a.shift == 0) {
-                    xm[grp * 32] = mpart;
-                    named_bar(1 + xr, 32 * G);
-                    mpart = xm[0];
-#pragma unroll
-                    for (int g = 1; g < G; ++g) mpart = fminf(mpart, xm[g * 32]);
-                } else {
-                    mpart = 0.f;
-                }
-                // partial sums in label_update's quarter order: G = 2 forms (quarter + quarter) per group
-                float sa = 0.f, sb = 0.f;
-                if (lx >= 0) {
+                        for (int l = 1; l < NLG; ++l) mh = fminf(mh, dlab[l]);
+                    }
 #pragma unroll
                     for (int l = 0; l < NLG; ++l) {
-                        ut[l] = uold[l] * ex2_approx((mpart - dlab[l]) * k2);
-                        if (G == 2 && l >= NLG / 2) sb += ut[l];
-                        else sa += ut[l];
+                        ut[l] = uold[l] * ex2_approx((mh - dlab[l]) * k2);
+                        if (l < NLG / 2) sa += ut[l];
+                        else sb += ut[l];
                     }
                 }
-                xa[grp * 32] = G == 2 ? sa + sb : sa;
+                xm[grp * 32] = mh;
+                xa[grp * 32] = sa + sb;
                 named_bar(1 + xr, 32 * G);
-                if constexpr (G == 2) sum = xa[0] + xa[32];
-                else sum = (xa[0] + xa[32]) + (xa[64] + xa[96]);
+                const float m0 = xm[0], m1 = xm[32];
+                float f0 = 1.f, f1 = 1.f;
+                if (a.shift == 0) {
+                    const float m = fminf(m0, m1);
+                    f0 = ex2_approx((m - m0) * k2);
+                    f1 = ex2_approx((m - m1) * k2);
+                }
+                sum = halves_sum(xa[0], f0, xa[32], f1);
+                const float fo = grp == 0 ? f0 : f1;
                 const float inv = __frcp_rn(sum);
 #pragma unroll
                 for (int l = 0; l < NLG; ++l) {
+                    ut[l] *= fo;
                     const float nu = ut[l] * inv;
                     un[l] = nu < FLT_MIN ? 0.f : nu;
                 }

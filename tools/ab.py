@@ -1,6 +1,6 @@
 """A/B timing of library builds in ONE GPU session (boxes differ from call to call, so only
 interleaved runs on the same GPU compare kernel variants).
-usage: python tools/ab.py --libs libpf_ref.so libpf.so --configs C2 C5slab [--rounds 3] [--steps 2]
+usage: python tools/ab.py --libs libpf_ref.so libpf.so libpf.so:PF_CLUSTER=0 --configs C2 C5slab [--rounds 3]
 Each (round, config, lib) runs tools/bench_configs.py in a fresh process with PF_LIB=<lib>."""
 import argparse
 import json
@@ -20,9 +20,18 @@ res = {}
 for r in range(args.rounds):
     for c in args.configs:
         for lib in args.libs:
-            env = dict(os.environ, PF_LIB=lib)
-            out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_configs.py"), c, "--steps",
-                                  str(args.steps)], env=env, capture_output=True, text=True).stdout
+            # "libname.so[:VAR=value,...]": extra environment for that arm (e.g. PF_CLUSTER=0)
+            name, _, extra = lib.partition(":")
+            env = dict(os.environ, PF_LIB=name)
+            for kv in filter(None, extra.split(",")):
+                k, _, v = kv.partition("=")
+                env[k] = v
+            pr = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_configs.py"), c, "--steps",
+                                 str(args.steps)], env=env, capture_output=True, text=True)
+            out = pr.stdout
+            if pr.returncode != 0:
+                print(json.dumps({"round": r, "config": c, "lib": lib, "failed": pr.returncode,
+                                  "stderr": pr.stderr[-600:]}), flush=True)
             for line in out.splitlines():
                 try:
                     d = json.loads(line)
