@@ -55,7 +55,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 template <int NL, int TY, int DBF>
 struct ClusterLayout {
     static constexpr int NLC = NL / 2;     // labels (= flow nodes, Potts) of one CTA
-    using L = StagedLayout<0, NLC, TY, 1, 0, 1>;
+    static constexpr int NLCP = (NLC + 1) & ~1;   // q-stage k-block stride in channels: 128-byte aligned TMA dst
+    using L = StagedLayout<0, NLCP, TY, 1, 0, 1>;
     static constexpr int XPTS = round32((TY + 1) * 33);   // exchange slots: tile + halo points
     __host__ __device__ static constexpr int off_X(int s_ch) { return L::floats(s_ch); }
     __host__ __device__ static constexpr int floats(int s_ch) { return off_X(s_ch) + 4 * XPTS; }   // (m, a) x 2
@@ -68,7 +69,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     pf_iter_cluster(const __grid_constant__ StagedArgs a) {
     using CL = ClusterLayout<NL, TY, DBF>;
     using L = typename CL::L;
-    constexpr int NLC = CL::NLC, NF = NL;
+    constexpr int NLC = CL::NLC, NLCP = CL::NLCP, NF = NL;
     constexpr int QW = L::QW, UW = L::UW, SW = L::SW, QROWS = L::QROWS, UROWS = L::UROWS;
     constexpr int QCS = QROWS * QW, UCS = UROWS * UW;
     constexpr int RS = L::RS, RPS = L::RPS, RING = L::RING;
@@ -129,7 +130,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
         mbar_arrive_expect_tx(&bars[stage], a.tx_bytes);
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-            tma_load_4d(Qs + stage * L::QSZ + k * NLC * QCS, &a.tm_q, &bars[stage], x0 - 4, y0 - 1, k * NF + lb,
+            tma_load_4d(Qs + stage * L::QSZ + k * NLCP * QCS, &a.tm_q, &bars[stage], x0 - 4, y0 - 1, k * NF + lb,
                         plane + 1);
         tma_load_4d(Us + stage * L::USZ, &a.tm_u, &bars[stage], x0, y0, lb, plane + 1);
         tma_load_4d(Ds + stage * L::USZ, &a.tm_D, &bars[stage], x0, y0, lb, plane);
@@ -228,9 +229,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                 for (int v = 0; v < NLC; ++v) {
                     const float qx = Qb[v * QCS + qoff];
                     const float qxm = Qb[v * QCS + qoff - 1];
-                    const float qy = Qb[(NLC + v) * QCS + qoff];
-                    const float qym = Qb[(NLC + v) * QCS + qoff - QW];
-                    const float qz = Qb[(2 * NLC + v) * QCS + qoff];
+                    const float qy = Qb[(NLCP + v) * QCS + qoff];
+                    const float qym = Qb[(NLCP + v) * QCS + qoff - QW];
+                    const float qz = Qb[(2 * NLCP + v) * QCS + qoff];
                     const float dq = ((qx - qxm) + (qy - qym)) + (qz - qc[2][v]);
                     qn[0][v] = qx; qn[1][v] = qy; qn[2][v] = qz;
                     float Dv;

@@ -158,6 +158,23 @@ def test_bf16_data_terms(name, dims, n):
     t.close()
 
 
+@pytest.mark.parametrize("K,dims,shift", [(10, (45, 37, 21), O.SHIFT_MIN), (12, (33, 40, 17), O.SHIFT_NONE),
+                                           (14, (40, 25, 19), O.SHIFT_MIN), (16, (70, 17, 9), O.SHIFT_NONE)])
+def test_many_label_potts_cluster_kernel(K, dims, shift, monkeypatch):
+    """Potts K = 10..16 runs the 2-CTA cluster kernel (pf_cluster.cuh): parity with the oracle, and bitwise
+    equal to the one-CTA kernels (PF_CLUSTER=0) -- the split-half label update is shared arithmetic."""
+    import dataclasses
+    cfg = dataclasses.replace(P.config("C5"), classes=K).resized(*dims)
+    inp = P.generate(cfg)
+    u, q, ur, qr = _run_both(inp, 120, shift)
+    compare(u, q, ur, qr)
+    monkeypatch.setenv("PF_CLUSTER", "0")
+    s = solver_from_inputs(inp, shift=shift)
+    s.iterate(120)
+    assert np.array_equal(s.labeling()[0], u) and np.array_equal(s.flows(), q)
+    s.close()
+
+
 def test_split_calls_equal_one_call():
     """iterate(a) + iterate(b) == iterate(a + b), bitwise (ping-pong bookkeeping)."""
     inp = P.generate(P.config("C2").resized(33, 30, 27))
