@@ -397,7 +397,11 @@ void choose_chunking(pf_solver *s) {
         s->zhi = std::max(s->zlo, (above ? nzl - 1 : nzl));
         const int nzi = s->zhi - s->zlo;
         const int64_t wslots = s->cluster ? slots / 2 : slots;   // concurrent work items
-        const int n = nzi > 0 ? best_chunks(tiles, nzi, wslots) : 0;
+        int n = nzi > 0 ? best_chunks(tiles, nzi, wslots) : 0;
+        if (const char *zc = getenv("PF_ZCHUNK")) {   // experiments (tools/): force the z-chunk length
+            const int want = atoi(zc);
+            if (want > 0 && nzi > 0) n = (nzi + want - 1) / want;
+        }
         s->zchunk = nzi > 0 ? (nzi + n - 1) / n : 1;
         const int nch = nzi > 0 ? (nzi + s->zchunk - 1) / s->zchunk : 0;
         s->tiles_x = gx;
