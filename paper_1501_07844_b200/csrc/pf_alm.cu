@@ -35,7 +35,7 @@ __device__ __forceinline__ float ld(const float *p) { return __ldg(p); }
 // capacity S_L(z, pixel): scalar per label, shared field x per-label factor, or a field per label
 __device__ __forceinline__ float cap_at(const AlmArgs &a, int L, int z, int pix, int64_t P) {
     if (!a.S) return a.s[L];
-    if (a.s_per_node) return ld(a.S + ((int64_t)z * a.NL + L) * P + pix);
+    if (a.s_per_node) return ld(a.S + ((int64_t)z * (a.dag ? a.NV : a.NL) + L) * P + pix);
     return ld(a.S + (int64_t)z * P + pix) * a.s[L];
 }
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(128) alm_potential_kernel(const AlmArgs a) {
     const int64_t P = (int64_t)a.pitch * a.ny;
     const int64_t qps = (int64_t)3 * NL * P, ups = (int64_t)NL * P;
     const int pix = valid ? y * a.pitch + x : 0;
-    const int zc0 = blockIdx.z * a.zchunk, zc1 = valid ? min(zc0 + a.zchunk, a.nz) : zc0;
+    const int zc0 = blockIdx.z * a.zchunk2, zc1 = valid ? min(zc0 + a.zchunk2, a.nz) : zc0;
     const float invK = 1.0f / NL;
     float qzp[NL];
 #pragma unroll
@@ -176,6 +176,224 @@ __global__ void __launch_bounds__(128) alm_potential_kernel(const AlmArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// DAG / HMF explicit-flow ALM (Eq. 11): every node v != S has u_v, p_v, q_v; residuals
+//   r_v = div q_v + p_v - sum_{P in parents(v)} w_(P,v) p_P        (source row: p_S)
+// pass 1 (per node): q_v <- Proj(q_v + tau grad(r_v - u_v / c))                       [alm_dag_flow_kernel]
+// pass 2 (per voxel, nodes in topological order, the block-coordinate maxima of L_c):  [alm_dag_potential]
+//   p_S  = ((1 - sum_c w u_c) / c + sum_c w (r_c + w p_S)) / sum_c w^2        (c: children of S)
+//   p_v  = ((u_v - sum_c w u_c) / c - (div q_v - sum_P w p_P) + sum_c w (r_c + w p_v)) / (1 + sum_c w^2)
+//   p_L  = min(D_L, u_L / c - div q_L + sum_P w p_P)                            (end labels)
+//   u_v -= c r_v                                                                 (all v, new p)
+
+// pass 1: one node per CTA z-slice; f = r_v - u_v / c on the tile + halo, q' = Proj(q + tau grad f)
+__global__ void __launch_bounds__(32 * kAlmTY + 64) alm_dag_flow_kernel(const AlmArgs a) {
+    constexpr int TY = kAlmTY, RS = 33, PS = (TY + 1) * RS;
+    __shared__ float F[3 * PS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool is_main = warp < TY;
+    int lx, ly;
+    if (is_main) {
+        lx = lane; ly = warp;
+    } else {
+        const int h = (warp - TY) * 32 + lane;
+        if (h < 32) { lx = h; ly = TY; }
+        else if (h < 32 + TY) { lx = 32; ly = h - 32; }
+        else { lx = -1; ly = 0; }
+    }
+    const int nch = (a.nz + a.zchunk - 1) / a.zchunk;
+    const int v = blockIdx.z / nch, chunk = blockIdx.z - v * nch;
+    const int x = blockIdx.x * 32 + lx, y = blockIdx.y * TY + ly;
+    const bool active = lx >= 0 && x < a.nx && y < a.ny;
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int NV = a.NV, NLab = a.NL;
+    const int64_t qps = (int64_t)3 * NV * P;
+    const int pix = active ? y * a.pitch + x : 0;
+    const int sme = ly * RS + (lx < 0 ? 0 : lx);
+    const int zc0 = chunk * a.zchunk, zc1 = min(zc0 + a.zchunk, a.nz);
+    const bool has_above = zc1 < a.nz;
+    const float cx = x < a.nx - 1 ? a.tau : 0.f, cy = y < a.ny - 1 ? a.tau : 0.f;
+    float qzp = 0.f;
+    if (active && zc0 > 0) qzp = ld(a.q_in + (int64_t)(zc0 - 1) * qps + (2 * NV + v) * P + pix);
+    float qcx = 0.f, qcy = 0.f, qcz = 0.f;
+    for (int p = zc0; p <= zc1; ++p) {
+        if (p == zc1 && !has_above) break;
+        float *Fp = F + (p % 3) * PS;
+        float f = 0.f, qx = 0.f, qy = 0.f, qz = 0.f;
+        if (active) {
+            const float *qb = a.q_in + (int64_t)p * qps + pix;
+            qx = ld(qb + v * P);
+            qy = ld(qb + (NV + v) * P);
+            qz = ld(qb + (2 * NV + v) * P);
+            const float qxm = x > 0 ? ld(qb + v * P - 1) : 0.f;
+            const float qym = y > 0 ? ld(qb + (NV + v) * P - a.pitch) : 0.f;
+            const float dq = ((qx - qxm) + (qy - qym)) + (qz - qzp);
+            const float *pb = a.p + (int64_t)p * NV * P + pix;
+            float inflow = a.W[0][v] * ld(a.pS + (int64_t)p * P + pix);
+            for (int i = 0; i < a.NI; ++i)
+                if (a.W[1 + i][v] != 0.f) inflow = fmaf(a.W[1 + i][v], ld(pb + i * P), inflow);
+            const float uv = v < a.NI ? ld(a.u_int + ((int64_t)p * a.NI + v) * P + pix)
+                                      : ld(a.u + ((int64_t)p * NLab + (v - a.NI)) * P + pix);
+            f = ((dq + ld(pb + v * P)) - inflow) - uv * a.inv_c;
+            qzp = qz;
+        }
+        if (lx >= 0) Fp[sme] = f;
+        __syncthreads();
+        if (is_main && active && p > zc0) {
+            const int z = p - 1;
+            const float *Fz = F + (z % 3) * PS;
+            const float fc = Fz[sme];
+            const float gx = Fz[sme + 1] - fc, gy = Fz[sme + RS] - fc, gz = f - fc;
+            const float sv = cap_at(a, v, z, pix, P);
+            float hx = fmaf(cx, gx, qcx), hy = fmaf(cy, gy, qcy), hz = fmaf(a.tau, gz, qcz);
+            project(a.cap, sv, hx, hy, hz);
+            float *qo = a.q_out + (int64_t)z * qps + pix;
+            qo[v * P] = hx;
+            qo[(NV + v) * P] = hy;
+            qo[(2 * NV + v) * P] = hz;
+        }
+        qcx = qx; qcy = qy; qcz = qz;
+    }
+    if (!has_above && is_main && active) {
+        const int z = zc1 - 1;
+        const float *Fz = F + (z % 3) * PS;
+        const float fc = Fz[sme];
+        const float gx = Fz[sme + 1] - fc, gy = Fz[sme + RS] - fc;
+        const float sv = cap_at(a, v, z, pix, P);
+        float hx = fmaf(cx, gx, qcx), hy = fmaf(cy, gy, qcy), hz = qcz;
+        project(a.cap, sv, hx, hy, hz);
+        float *qo = a.q_out + (int64_t)z * qps + pix;
+        qo[v * P] = hx;
+        qo[(NV + v) * P] = hy;
+        qo[(2 * NV + v) * P] = hz;
+    }
+}
+
+// pass 2: per voxel column over a short z-chunk (a.zchunk2 planes: parallelism over the whole volume),
+// node arrays in registers (NVT = NV non-source nodes, fully unrolled)
+template <int NVT>
+__global__ void __launch_bounds__(128) alm_dag_potential_kernel(const AlmArgs a) {
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * 4 + (threadIdx.x >> 5);
+    const bool valid = x < a.nx && y < a.ny;
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    constexpr int NV = NVT;
+    const int NI = a.NI, NLab = a.NL;
+    const int64_t qps = (int64_t)3 * NV * P;
+    const int pix = valid ? y * a.pitch + x : 0;
+    const int zc0 = blockIdx.z * a.zchunk2, zc1 = valid ? min(zc0 + a.zchunk2, a.nz) : zc0;
+    float qzp[NVT];
+#pragma unroll
+    for (int v = 0; v < NVT; ++v)
+        qzp[v] = (v < NV && zc0 > 0) ? ld(a.q_out + (int64_t)(zc0 - 1) * qps + (2 * NV + v) * P + pix) : 0.f;
+    float resid = 0.f;
+    for (int z = zc0; z < zc1; ++z) {
+        const float *qb = a.q_out + (int64_t)z * qps + pix;
+        float dq[NVT], pv[NVT], uv[NVT];
+#pragma unroll
+        for (int v = 0; v < NVT; ++v) {
+            if (v >= NV) { dq[v] = pv[v] = uv[v] = 0.f; continue; }
+            const float qx = ld(qb + v * P), qy = ld(qb + (NV + v) * P), qz = ld(qb + (2 * NV + v) * P);
+            const float qxm = x > 0 ? ld(qb + v * P - 1) : 0.f;
+            const float qym = y > 0 ? ld(qb + (NV + v) * P - a.pitch) : 0.f;
+            dq[v] = ((qx - qxm) + (qy - qym)) + (qz - qzp[v]);
+            qzp[v] = qz;
+            pv[v] = ld(a.p + ((int64_t)z * NV + v) * P + pix);
+            uv[v] = v < NI ? ld(a.u_int + ((int64_t)z * NI + v) * P + pix)
+                           : ld(a.u + ((int64_t)z * NLab + (v - NI)) * P + pix);
+        }
+        float ps = ld(a.pS + (int64_t)z * P + pix);
+        // inflow of position c with the current p: sum_P w_(P,c) p_P
+        auto inflow = [&](int c) {
+            float acc = a.W[0][c] * ps;
+#pragma unroll
+            for (int i = 0; i < NVT; ++i)
+                if (i < NI && a.W[1 + i][c] != 0.f) acc = fmaf(a.W[1 + i][c], pv[i], acc);
+            return acc;
+        };
+        auto r_of = [&](int c) { return (dq[c] + pv[c]) - inflow(c); };
+        // source
+        {
+            float sw2 = 0.f, wu = 0.f, acc = 0.f;
+#pragma unroll
+            for (int c = 0; c < NVT; ++c) {
+                const float w = c < NV ? a.W[0][c] : 0.f;
+                if (w != 0.f) {
+                    sw2 = fmaf(w, w, sw2);
+                    wu = fmaf(w, uv[c], wu);
+                    acc = fmaf(w, fmaf(w, ps, r_of(c)), acc);
+                }
+            }
+            ps = ((1.f - wu) * a.inv_c + acc) / sw2;
+        }
+        // internal nodes (topological), then end labels
+#pragma unroll
+        for (int v = 0; v < NVT; ++v) {
+            if (v >= NV) continue;
+            if (v < NI) {
+                float sw2 = 0.f, wu = 0.f, acc = 0.f;
+#pragma unroll
+                for (int c = 0; c < NVT; ++c) {
+                    const float w = c < NV ? a.W[1 + v][c] : 0.f;
+                    if (w != 0.f) {
+                        sw2 = fmaf(w, w, sw2);
+                        wu = fmaf(w, uv[c], wu);
+                        acc = fmaf(w, fmaf(w, pv[v], r_of(c)), acc);
+                    }
+                }
+                pv[v] = (((uv[v] - wu) * a.inv_c - (dq[v] - inflow(v))) + acc) / (1.f + sw2);
+            } else {
+                pv[v] = fminf(load_D(a.D, ((int64_t)z * NLab + (v - NI)) * P + pix, a.d_bf16),
+                              (uv[v] * a.inv_c - dq[v]) + inflow(v));
+            }
+        }
+        a.pS[(int64_t)z * P + pix] = ps;
+        float res[NVT];
+#pragma unroll
+        for (int v = 0; v < NVT; ++v) res[v] = v < NV ? r_of(v) : 0.f;
+#pragma unroll
+        for (int v = 0; v < NVT; ++v) {
+            if (v >= NV) continue;
+            const float un = uv[v] - a.c * res[v];
+            a.p[((int64_t)z * NV + v) * P + pix] = pv[v];
+            if (v < NI) a.u_int[((int64_t)z * NI + v) * P + pix] = un;
+            else a.u[((int64_t)z * NLab + (v - NI)) * P + pix] = un;
+            if (v >= NI) resid = fmaxf(resid, fabsf(un - uv[v]));
+        }
+    }
+    if (a.check) {
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) resid = fmaxf(resid, __shfl_xor_sync(0xffffffffu, resid, s));
+        if ((threadIdx.x & 31) == 0 && resid > 0.f) atomicMax(a.resid_bits, __float_as_uint(resid));
+    }
+}
+
+// DAG start: u_L = 1/|L|, u_v = sum_c w u_c (reverse topological), p = 0, p_S = min_L D_L
+__global__ void alm_dag_init_kernel(const AlmArgs a) {
+    const int64_t P = (int64_t)a.pitch * a.ny;
+    const int64_t V = (int64_t)a.nx * a.ny * a.nz;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / ((int64_t)a.nx * a.ny);
+        const int r = (int)(i - z * (int64_t)a.nx * a.ny);
+        const int y = r / a.nx, x = r - y * a.nx;
+        const int64_t pix = (int64_t)y * a.pitch + x;
+        float m = FLT_MAX;
+        for (int l = 0; l < a.NL; ++l) m = fminf(m, load_D(a.D, (z * a.NL + l) * P + pix, a.d_bf16));
+        a.pS[z * P + pix] = m;
+        float uv[16];
+        for (int v = 0; v < a.NV; ++v) uv[v] = v >= a.NI ? 1.0f / (float)a.NL : 0.f;
+        for (int v = a.NI - 1; v >= 0; --v) {
+            float acc = 0.f;
+            for (int c = 0; c < a.NV; ++c) acc = fmaf(a.W[1 + v][c], uv[c], acc);
+            uv[v] = acc;
+        }
+        for (int v = 0; v < a.NV; ++v) {
+            a.p[(z * a.NV + v) * P + pix] = 0.f;
+            if (v < a.NI) a.u_int[(z * a.NI + v) * P + pix] = uv[v];
+        }
+    }
+}
+
 // p_S = min_L D_L, p_L = p_S (the standard start; u = 1/K and q = 0 are set by the caller).
 __global__ void alm_init_kernel(const AlmArgs a) {
     const int64_t P = (int64_t)a.pitch * a.ny;
@@ -194,7 +412,7 @@ __global__ void alm_init_kernel(const AlmArgs a) {
 
 template <int NL>
 cudaError_t launch_pot(const AlmArgs &a, cudaStream_t st) {
-    dim3 grid((a.nx + 31) / 32, (a.ny + 3) / 4, (a.nz + a.zchunk - 1) / a.zchunk);
+    dim3 grid((a.nx + 31) / 32, (a.ny + 3) / 4, (a.nz + a.zchunk2 - 1) / a.zchunk2);
     alm_potential_kernel<NL><<<grid, 128, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -202,12 +420,28 @@ cudaError_t launch_pot(const AlmArgs &a, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_alm_init(const AlmArgs &a, cudaStream_t st) {
-    alm_init_kernel<<<1184, 256, 0, st>>>(a);
+    if (a.dag) alm_dag_init_kernel<<<1184, 256, 0, st>>>(a);
+    else alm_init_kernel<<<1184, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_alm_iteration(const AlmArgs &a, cudaStream_t st) {
     const int nch = (a.nz + a.zchunk - 1) / a.zchunk;
+    if (a.dag) {
+        dim3 g1((a.nx + 31) / 32, (a.ny + kAlmTY - 1) / kAlmTY, nch * a.NV);
+        alm_dag_flow_kernel<<<g1, 32 * kAlmTY + 64, 0, st>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        dim3 g2((a.nx + 31) / 32, (a.ny + 3) / 4, (a.nz + a.zchunk2 - 1) / a.zchunk2);
+        switch (a.NV) {
+#define PF_DAGPOT(n) case n: alm_dag_potential_kernel<n><<<g2, 128, 0, st>>>(a); break;
+            PF_DAGPOT(3) PF_DAGPOT(4) PF_DAGPOT(5) PF_DAGPOT(6) PF_DAGPOT(7) PF_DAGPOT(8) PF_DAGPOT(9)
+            PF_DAGPOT(10) PF_DAGPOT(11) PF_DAGPOT(12) PF_DAGPOT(13) PF_DAGPOT(14) PF_DAGPOT(15) PF_DAGPOT(16)
+#undef PF_DAGPOT
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    }
     dim3 g1((a.nx + 31) / 32, (a.ny + kAlmTY - 1) / kAlmTY, nch * a.NL);
     alm_flow_kernel<<<g1, 32 * kAlmTY + 64, 0, st>>>(a);
     cudaError_t e = cudaGetLastError();

@@ -70,6 +70,7 @@ struct Compiled {
     std::vector<int> node_of_pos;
     GraphConst g;
     std::vector<std::vector<float>> W;  // W[pos][leaf slot] path weights
+    std::vector<float> w_src;           // weight of the edge S -> position (0: none)
 };
 
 pf_status compile_graph(const pf_graph *gr, Compiled *out) {
@@ -191,6 +192,8 @@ pf_status compile_graph(const pf_graph *gr, Compiled *out) {
         const int i = out->pos_of_node[v];
         for (auto &c : kids[v]) out->g.w[i][out->pos_of_node[c.first]] += c.second;
     }
+    out->w_src.assign(out->NV, 0.f);
+    for (auto &c : kids[0]) out->w_src[out->pos_of_node[c.first]] += c.second;
     out->W.assign(out->NV, std::vector<float>(NL, 0.f));  // W_(v, B), for reports
     for (int p = 0; p < out->NV; ++p)
         for (int l = 0; l < NL; ++l) out->W[p][l] = (float)Wd[out->node_of_pos[p]][l];
@@ -218,6 +221,7 @@ struct pf_solver {
     uint16_t *D16 = nullptr;                          // bf16 D (cfg.d_bf16), same [z][l][y][pitch] layout
     bool alm = false;                                 // PF_METHOD_EXPLICIT_ALM (pf_alm.cu)
     float *p_alloc = nullptr, *pS_alloc = nullptr;    // ALM sink flows [z][l][y][pitch], source flow [z][y][pitch]
+    float *uint_alloc = nullptr;                      // ALM on a DAG: u of the internal nodes [z][NI][y][pitch]
     const void *Dptr() const { return D16 ? (const void *)D16 : (const void *)D_alloc; }
     float *u[2] = {nullptr, nullptr}, *q[2] = {nullptr, nullptr};
     int cur = 0;
@@ -286,7 +290,7 @@ void pool_setup(int dev) {
 
 void free_all(pf_solver *s) {
     void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc, s->D16,
-                    s->p_alloc, s->pS_alloc,
+                    s->p_alloc, s->pS_alloc, s->uint_alloc,
                     s->d_resid, s->d_err, s->d_flag, s->d_energy};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, s->stream);
@@ -294,7 +298,7 @@ void free_all(pf_solver *s) {
     for (int i = 0; i < 2; ++i) s->u_alloc[i] = s->q_alloc[i] = nullptr;
     s->D_alloc = s->S_alloc = nullptr;
     s->D16 = nullptr;
-    s->p_alloc = s->pS_alloc = nullptr;
+    s->p_alloc = s->pS_alloc = s->uint_alloc = nullptr;
     s->d_resid = nullptr;
     s->d_err = nullptr;
     s->d_flag = nullptr;
@@ -331,11 +335,22 @@ AlmArgs alm_args(pf_solver *s, int check) {
     a.pitch = (int)s->pitch;
     a.NL = s->gc.NL;
     a.zchunk = 32;
+    a.zchunk2 = s->gc.NI > 0 ? 2 : 8;   // pass-2 chunk: parallelism vs the chunk-start q^z re-read
     a.c = s->cfg.c;
     a.inv_c = 1.0f / s->cfg.c;
     a.tau = s->cfg.tau;
-    for (int l = 0; l < s->gc.NL && l < 16; ++l) a.s[l] = s->gc.g.s[l];
+    for (int l = 0; l < s->gc.NV && l < 16; ++l) a.s[l] = s->gc.g.s[l];
     a.resid_bits = s->d_resid;
+    if (s->gc.NI > 0) {   // DAG / HMF (Eq. 11)
+        a.dag = 1;
+        a.NI = s->gc.NI;
+        a.NV = s->gc.NV;
+        a.u_int = s->uint_alloc;
+        const Compiled &g = s->gc;
+        for (int j = 0; j < g.NV; ++j) a.W[0][j] = g.w_src[j];
+        for (int i = 0; i < g.NI; ++i)
+            for (int j = 0; j < g.NV; ++j) a.W[1 + i][j] = g.g.w[i][j];
+    }
     return a;
 }
 
@@ -553,9 +568,9 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     if (cfg->method != PF_METHOD_PSEUDO_FLOW && cfg->method != PF_METHOD_EXPLICIT_ALM)
         return fail(PF_ERR_INVALID, "config: bad method");
     const bool alm = cfg->method == PF_METHOD_EXPLICIT_ALM;
-    if (alm && (gc.model != 0 || gc.NI != 0 || gc.NL > 16 || slab || S->kind == PF_S_SCALED_FIELD))
-        return fail(PF_ERR_UNSUPPORTED, "explicit-flow ALM: Potts graphs (<= 16 labels), whole volumes, scalar, "
-                                        "shared or per-label capacities only");
+    if (alm && (gc.model != 0 || gc.NV > 16 || slab || S->kind == PF_S_SCALED_FIELD))
+        return fail(PF_ERR_UNSUPPORTED, "explicit-flow ALM: Potts / HMF / DAG graphs (<= 16 non-source nodes), whole "
+                                        "volumes, scalar, shared or per-node capacities only");
 
     pf_solver *s = new pf_solver();
     s->alm = alm;
@@ -633,7 +648,11 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         s->q[i] = s->q_alloc[i] + (int64_t)3 * NF * P;
     }
     if (alm) {
-        if ((st = alloc(s, (void **)&s->p_alloc, (size_t)(nzl * NL * P) * sizeof(float), "ALM p")) != PF_OK)
+        const int np = gc.NI > 0 ? gc.NV : NL;   // p of every non-source node (DAG) or of the labels (Potts)
+        if ((st = alloc(s, (void **)&s->p_alloc, (size_t)(nzl * np * P) * sizeof(float), "ALM p")) != PF_OK)
+            return bail(st);
+        if (gc.NI > 0 &&
+            (st = alloc(s, (void **)&s->uint_alloc, (size_t)(nzl * gc.NI * P) * sizeof(float), "ALM u_int")) != PF_OK)
             return bail(st);
         if ((st = alloc(s, (void **)&s->pS_alloc, (size_t)(nzl * P) * sizeof(float), "ALM p_S")) != PF_OK)
             return bail(st);
@@ -1150,8 +1169,11 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     // its flow r/w
     const int64_t per_leaf = 4 + 4 + (s->D16 ? 2 : 4), per_flow = 8 * s->ndim;
     int64_t b = V * (per_leaf * s->gc.NL + per_flow * s->gc.NF);
-    if (s->alm)  // pass 1: q r/w, p r, u r (+ p_S r); pass 2: q r, D r, p w, u r/w (+ p_S r/w)  (pf_alm.cu)
+    if (s->alm && s->gc.NI == 0)  // pass 1: q r/w, p r, u r (+ p_S r); pass 2: q r, D r, p w, u r/w (+ p_S r/w)
         b = V * ((int64_t)s->gc.NL * (8 * s->ndim + 4 + 4 + 4 * s->ndim + (s->D16 ? 2 : 4) + 4 + 8) + 12);
+    else if (s->alm)  // DAG: per node pass 1 q r/w, p r, u r; pass 2 q r, p r/w, u r/w; D per label; p_S r, r/w
+        b = V * ((int64_t)s->gc.NV * (8 * s->ndim + 4 + 4 + 4 * s->ndim + 8 + 8) +
+                 (int64_t)s->gc.NL * (s->D16 ? 2 : 4) + 12);
     if (s->s_kind == PF_S_SHARED_FIELD || s->s_kind == PF_S_SCALED_FIELD) b += 4 * V;
     if (s->s_kind == PF_S_FIELD_PER_NODE) b += 4 * V * s->gc.NF;
     info->algorithmic_bytes_per_iteration = b;

@@ -59,8 +59,23 @@ def test_alm_and_pseudo_flow_reach_the_same_labeling():
     b.close()
 
 
+@pytest.mark.parametrize("name,dims,n", [("C3", (33, 29, 17), 80), ("C4", (30, 26, 21), 80), ("C3", (40, 40, 12), 60)])
+def test_dag_alm_matches_oracle(name, dims, n):
+    """Explicit-flow ALM on HMF / DAGMF (Eq. 11): every node stores u_v, p_v and q_v."""
+    inp = P.generate(P.config(name).resized(*dims))
+    g = inp.graph
+    s = solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM, c=CA, tau=0.05)
+    s.iterate(n)
+    u, am = s.labeling()
+    q = s.flows()
+    s.close()
+    S = np.stack([np.full(inp.shape, float(inp.s_scalars[v])) for v in range(g.num_nodes)])
+    ur, qr, _ = A.dag_alm(inp.D, S, g.num_nodes, g.parent, g.child, g.weight, inp.cfg.ndim, n, ca=CA, ta=0.05)
+    compare(u, q, ur, qr)
+
+
 def test_alm_rejects_unsupported():
-    inp = P.generate(P.config("C3").resized(20, 20, 8))   # HMF tree: not a Potts graph
+    inp = P.generate(P.config("I2").resized(20, 20, 8))   # Ishikawa chain (Alg. 3): not an Eq. 3 / Eq. 11 arm
     with pytest.raises(pf.PFError) as ei:
         solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM)
     assert ei.value.status == pf.PF_ERR_UNSUPPORTED
