@@ -237,6 +237,12 @@ def run_ours(args, rank, world, local_rank):
             def mk(slab_):
                 return pf.Solver((cfg.nx, cfg.ny, cfg.nz), 3, (gH.num_nodes, gH.parent, gH.child, gH.weight), DH,
                                  s_shared=SH, c=cfg.c, tau=cfg.tau, check_every=10, slab=slab_)
+            if world == 1:   # the single-GPU user path: one Solver on its own stream
+                sv = mk(None)
+                sv.iterate(iters)
+                sv.labeling(u_host, lab_host)
+                sv.close()
+                return
             d = DistSolver(mk, cfg.nz, rank, world, dev)
             d.iterate(iters)
             d.solver.labeling(u_host, lab_host)
@@ -244,7 +250,7 @@ def run_ours(args, rank, world, local_rank):
 
         e2e_step()
         torch.cuda.synchronize()
-        ne = max(1, min(args.steps, 3))
+        ne = max(1, min(args.steps, 5))
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()

@@ -987,13 +987,14 @@ pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {
     if (argmax) {
         const bool dev = is_device_ptr(argmax);
         uint8_t *dst = argmax;
-        if (!dev) CK(cudaMalloc((void **)&dst, (size_t)V), "argmax scratch");
+        // stream-ordered scratch from the (retained) pool: cudaMalloc / cudaFree would synchronize the device
+        if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V, s->stream), "argmax scratch");
         CK(launch_argmax(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, s->stream), "argmax kernel");
         s->launches++;
         if (!dev) {
             CK(cudaMemcpyAsync(argmax, dst, (size_t)V, cudaMemcpyDeviceToHost, s->stream), "download argmax");
             CK(cudaStreamSynchronize(s->stream), "sync");
-            cudaFree(dst);
+            cudaFreeAsync(dst, s->stream);
         }
     }
     return check_numeric(s);
