@@ -6,7 +6,7 @@ import pytest
 import oracle as O
 import paper_1501_07844_b200 as pf
 import phantoms as P
-from helpers import compare, solver_from_inputs
+from helpers import bf16_rounded, compare, solver_from_inputs
 from oracle import alm as A
 
 pytestmark = pytest.mark.gpu
@@ -28,10 +28,15 @@ def _oracle(inp, n, cap):
     ("C2", (37, 29, 21), 100, "l2"),       # ragged tiles / z-chunks, edge-weighted shared S field
     ("C5", (24, 20, 40), 60, "l2"),        # K = 16, two z-chunks
     ("C1", (40, 33, 1), 120, "linf"),
+    ("C2bf16", (30, 22, 17), 80, "l2"),    # D stored as bf16: the ALM solves the problem with bf16(D) too
 ])
 def test_alm_matches_oracle(name, dims, n, cap):
-    inp = P.generate(P.config(name).resized(*dims))
-    s = solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM, c=CA, tau=TA, cap=0 if cap == "l2" else 1)
+    bf16 = name.endswith("bf16")
+    inp = P.generate(P.config(name.replace("bf16", "")).resized(*dims))
+    if bf16:
+        inp = bf16_rounded(inp)
+    s = solver_from_inputs(inp, method=pf.PF_METHOD_EXPLICIT_ALM, c=CA, tau=TA, cap=0 if cap == "l2" else 1,
+                           d_bf16=bf16)
     s.iterate(n)
     u, am = s.labeling()
     q = s.flows()
