@@ -68,7 +68,9 @@ class DistSolver:
         assert len(self.bounds) == world, "every rank needs at least one plane"
         self.slab = self.bounds[rank]
         self.solver: Solver = make_solver(self.slab)
-        self.solver.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        self.cuda = torch.device(device).type == "cuda"
+        if self.cuda:
+            self.solver.set_stream(torch.cuda.current_stream(device).cuda_stream)
 
     def _regions(self):
         h = self.solver.halo()
@@ -83,11 +85,14 @@ class DistSolver:
         }
 
     def iterate(self, n: int, residual: bool = False, overlap: bool = True):
+        """n iterations with the halo exchange after each; residual=True: max over ranks of the last
+        iteration's residual (-1 if it was not a check iteration)."""
         if self.world == 1:
             return self.solver.iterate(n, residual)
+        overlap = overlap and self.cuda
         r = None
-        S = torch.cuda.current_stream(self.device)
-        C = self._comm_stream()
+        S = torch.cuda.current_stream(self.device) if self.cuda else None
+        C = self._comm_stream() if overlap else None
         works = []
         for t in range(n):
             last = residual and t == n - 1
@@ -106,12 +111,40 @@ class DistSolver:
                 val = self.solver.iterate(1, last)
                 halo_exchange(self._regions(), self.rank, self.world, self.group)
             if last:
-                rt = torch.tensor([val], device=self.device)
+                rt = torch.tensor([val], dtype=torch.float64, device=self.device)
                 dist.all_reduce(rt, op=dist.ReduceOp.MAX, group=self.group)
                 r = float(rt.item())
         for w in works:
             w.wait()
         return r
+
+    def run(self, max_iters: int, tol: float):
+        """"while not converged" across the slabs: iterate until the residual of a check iteration, max
+        over ranks (all-reduce MAX), is <= tol or max_iters.  Returns (iterations, residual)."""
+        k = self.solver.check_every
+        if k <= 0:
+            raise ValueError("run() needs check_every > 0")
+        done, r = 0, -1.0
+        while done < max_iters:
+            it = self.solver.iterations()
+            n = min(k - it % k, max_iters - done)
+            rr = self.iterate(n, residual=True)
+            done += n
+            if (it + n) % k == 0:
+                r = rr
+                if r <= tol:
+                    break
+        return done, r
+
+    def energy(self):
+        """(primal, dual) of the whole volume: the slabs' fp64 energies summed over ranks (all-reduce SUM).
+        The halos must be current (they are after iterate())."""
+        e, f = self.solver.energy()
+        if self.world == 1:
+            return e, f
+        t = torch.tensor([e, f], dtype=torch.float64, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return float(t[0]), float(t[1])
 
     def _comm_stream(self):
         if getattr(self, "_C", None) is None:

@@ -32,6 +32,7 @@ class Solver:
         self.num_nodes = int(num_nodes)
         self.NL = len(D)
         self.slab = (0, self.dims[2]) if slab is None else (int(slab[0]), int(slab[1]))
+        self.check_every = int(check_every)
         if s_scaled is not None:
             kind, s_scalars, fields = PF_S_SCALED_FIELD, s_scaled[0], [s_scaled[1]]
         elif s_scalars is not None:

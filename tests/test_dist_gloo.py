@@ -109,3 +109,66 @@ def test_slab_bounds():
     assert slab_bounds(10, 3) == [(0, 4), (4, 8), (8, 10)]
     b = slab_bounds(768, 8)
     assert all(z1 - z0 == 96 for z0, z1 in b)
+
+
+# ---------------------------------------------------------------------------------------------------
+# DistSolver host logic (run / energy / iterate on the non-overlapped path) with stub slab solvers:
+# the convergence decision uses the residual MAX over ranks, energies are SUMMED over ranks.
+
+class _StubSolver:
+    check_every = 5
+
+    def __init__(self, rank):
+        self.rank, self.it = rank, 0
+
+    def iterate(self, n, residual=False):
+        self.it += n
+        if not residual:
+            return None
+        return (self.rank + 1.0) / self.it if self.it % self.check_every == 0 else -1.0
+
+    def iterations(self):
+        return self.it
+
+    def energy(self):
+        return 1.5 * (self.rank + 1), 0.5 * (self.rank + 1)
+
+
+def _dist_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1501_07844_b200.dist import DistSolver
+
+    class CpuDist(DistSolver):
+        def _regions(self):   # tiny CPU halo buffers instead of the library's device ranges
+            r = {k: None for k in ("send_down_u", "send_down_q", "recv_up_u", "recv_up_q", "send_up_qz",
+                                   "recv_down_qz")}
+            if self.rank > 0:
+                r["send_down_u"] = torch.full((3,), float(self.rank))
+                r["send_down_q"] = torch.full((3,), float(self.rank))
+                r["recv_down_qz"] = torch.zeros(3)
+            if self.rank < self.world - 1:
+                r["recv_up_u"] = torch.zeros(3)
+                r["recv_up_q"] = torch.zeros(3)
+                r["send_up_qz"] = torch.full((3,), float(self.rank))
+            return r
+
+    ds = CpuDist(lambda slab: _StubSolver(rank), 16, rank, world, torch.device("cpu"))
+    n, r = ds.run(1000, 0.05)            # rank r reports (r+1)/it: the max over ranks is world/it
+    e = ds.energy()
+    out[rank] = (n, r, e)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_run_uses_global_residual_and_sums_energies(world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_dist_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    want_it = 5 * int(np.ceil(world / 0.05 / 5))            # first check iteration with world / it <= 0.05
+    for rank in range(world):
+        n, r, (e, f) = out[rank]
+        assert n == want_it and abs(r - world / want_it) < 1e-6
+        assert e == 1.5 * world * (world + 1) / 2 and f == 0.5 * world * (world + 1) / 2
