@@ -227,8 +227,13 @@ struct pf_solver {
     int cur = 0;
     int64_t iters = 0;
     unsigned int *d_resid = nullptr;
-    unsigned long long *d_err = nullptr;   // [0] error voxel, [1] work-item ticket counter
-    uint64_t ticket_base = 0;              // ticket counter value at the start of the next launch
+    unsigned long long *d_err = nullptr;   // [0] error voxel, [1], [2] work-item ticket counters
+    int launch_parity = 0;                 // which ticket counter the next staged launch uses
+    // CUDA graph of `graph_iters` whole iterations (pf_iterate), replayed when the state matches the
+    // capture: same ping-pong buffer, same counter parity, check iterations at the same positions
+    cudaGraphExec_t graph = nullptr;
+    int graph_iters = 0, graph_cur = 0, graph_parity = 0;
+    bool graph_failed = false;
     unsigned int *d_flag = nullptr;
     double *d_energy = nullptr;  // partials + result
     IterKernelInfo kinfo{};
@@ -289,6 +294,10 @@ void pool_setup(int dev) {
 }
 
 void free_all(pf_solver *s) {
+    if (s->graph) {
+        cudaGraphExecDestroy(s->graph);
+        s->graph = nullptr;
+    }
     void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc, s->D16,
                     s->p_alloc, s->pS_alloc, s->uint_alloc,
                     s->d_resid, s->d_err, s->d_flag, s->d_energy};
@@ -668,7 +677,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     if ((st = alloc(s, (void **)&s->d_err, 64, "err")) != PF_OK) return bail(st);
     e = cudaMemsetAsync(s->d_err, 0, 64, s->stream);
     if (e != cudaSuccess) { cuda_fail(s, e, "zero ticket"); return bail(PF_ERR_CUDA); }
-    s->ticket_base = 0;
+    s->launch_parity = 0;
     if ((st = alloc(s, (void **)&s->d_flag, 64, "flag")) != PF_OK) return bail(st);
     if ((st = alloc(s, (void **)&s->d_energy, (size_t)(2 * kEnergyBlocks + 2) * sizeof(double), "energy")) != PF_OK)
         return bail(st);
@@ -832,15 +841,15 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
         sa.u_out = s->u[1 - s->cur];
         sa.q_out = s->q[1 - s->cur];
         sa.check = check;
-        sa.ticket = s->d_err + 1;
-        sa.ticket_base = s->ticket_base;
+        sa.ticket = s->d_err + 1 + s->launch_parity;
+        sa.ticket_next = s->d_err + 2 - s->launch_parity;
         // cluster kernel: 2 CTAs per item and one ticket grab per cluster
         const int per = s->cluster ? 2 : 1;
         const int grid = (int)std::min<int64_t>(s->sgrid / per, ie - ib) * per;
         void *args[] = {(void *)&sa};
         CK(cudaLaunchKernel(s->sinfo.func, dim3(grid), dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
            s->cluster ? "launch pf_iter_cluster" : "launch pf_iter_staged");
-        s->ticket_base += (uint64_t)(ie - ib) + (uint64_t)(grid / per);  // items + one failed grab per launcher
+        s->launch_parity ^= 1;
     } else {
         IterArgs a;
         memset(&a, 0, sizeof(a));
@@ -897,20 +906,14 @@ pf_status read_residual(pf_solver *s, bool any_check, float *residual) {
     return PF_OK;
 }
 
-}  // namespace
-
-pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
-    pf_status st = check_usable(s);
-    if (st != PF_OK) return st;
-    if (n < 0) return fail(PF_ERR_INVALID, "n must be >= 0");
-    if (s->phase_pending) return fail(PF_ERR_STATE, "pf_iterate: an iteration split by pf_iterate_phase is open");
-    DeviceGuard dg(s->device);
-    bool any_check = false;
+// Plain launch loop of n iterations (bookkeeping advanced as if executed).
+pf_status launch_iterations(pf_solver *s, int32_t n, bool *any_check) {
+    pf_status st;
     for (int t = 0; t < n; ++t) {
         const int check = check_this_iteration(s);
         if (check) {
             CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
-            any_check = true;
+            *any_check = true;
         }
         if (s->alm) {
             CK(launch_alm_iteration(alm_args(s, check), s->stream), "ALM iteration");
@@ -921,6 +924,85 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
         s->cur = 1 - s->cur;
         s->iters += 1;
     }
+    return PF_OK;
+}
+
+// Iterations per graph: even (ping-pong buffer and counter parity return to their start) and a multiple
+// of check_every (the residual resets / checks sit at the same positions in every replay).
+int graph_period(const pf_solver *s) {
+    const int k = s->cfg.check_every;
+    if (k <= 0) return 16;
+    return (k % 2) ? 2 * k : k;
+}
+
+bool graph_aligned(const pf_solver *s) {
+    const int k = s->cfg.check_every;
+    return k <= 0 || s->iters % k == 0;
+}
+
+// Capture graph_period() iterations into s->graph (the state bookkeeping is restored afterwards: capture
+// does not execute).  Captured on a private stream (the solver's may be the legacy default stream).
+pf_status capture_graph(pf_solver *s) {
+    const int P = graph_period(s);
+    cudaStream_t cap = nullptr, real = s->stream;
+    if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        s->graph_failed = true;
+        return PF_OK;
+    }
+    const int cur0 = s->cur, par0 = s->launch_parity;
+    const int64_t it0 = s->iters, l0 = s->launches;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    bool dummy = false;
+    if (ok) {
+        s->stream = cap;
+        const pf_status st = launch_iterations(s, P, &dummy);
+        s->stream = real;
+        ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && st == PF_OK;
+    }
+    s->cur = cur0;
+    s->launch_parity = par0;
+    s->iters = it0;
+    s->launches = l0;
+    if (ok) ok = cudaGraphInstantiate(&s->graph, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    cudaGetLastError();
+    if (!ok) {
+        s->graph = nullptr;
+        s->graph_failed = true;
+        return PF_OK;
+    }
+    s->graph_iters = P;
+    s->graph_cur = cur0;
+    s->graph_parity = par0;
+    return PF_OK;
+}
+
+}  // namespace
+
+pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (n < 0) return fail(PF_ERR_INVALID, "n must be >= 0");
+    if (s->phase_pending) return fail(PF_ERR_STATE, "pf_iterate: an iteration split by pf_iterate_phase is open");
+    DeviceGuard dg(s->device);
+    bool any_check = false;
+    // whole periods as CUDA-graph replays (one graph launch instead of P kernel launches + memsets),
+    // the rest as plain launches; PF_GRAPHS=0 disables
+    static const bool graphs_on = !(getenv("PF_GRAPHS") && strcmp(getenv("PF_GRAPHS"), "0") == 0);
+    const int P = graph_period(s);
+    while (graphs_on && !s->alm && !s->graph_failed && n >= P && graph_aligned(s)) {
+        if (!s->graph && (st = capture_graph(s)) != PF_OK) return st;
+        if (!s->graph || s->cur != s->graph_cur || s->launch_parity != s->graph_parity) break;
+        CK(cudaGraphLaunch(s->graph, s->stream), "graph launch");
+        s->iters += P;
+        s->launches += (int64_t)P * (s->cfg.check_every > 0 ? 1 : 1);
+        any_check = any_check || s->cfg.check_every > 0;
+        n -= P;
+    }
+    if ((st = launch_iterations(s, n, &any_check)) != PF_OK) return st;
     return read_residual(s, any_check, residual);
 }
 

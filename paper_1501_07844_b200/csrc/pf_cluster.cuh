@@ -142,9 +142,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     int kbase = 0;
     __shared__ int s_item;
     // one ticket per cluster: rank 0 grabs it and publishes it to both CTAs before a cluster barrier
+    if (blockIdx.x == 0 && tid == 0) *a.ticket_next = 0ull;   // the next launch's counter (see pf_staged.cuh)
     auto grab_publish = [&]() {
         if (rank == 0 && tid == 0) {
-            const unsigned long long t = atomicAdd(a.ticket, 1ull) - a.ticket_base;
+            const unsigned long long t = atomicAdd(a.ticket, 1ull);
             const int it = t < (unsigned long long)(a.items - a.item_begin) ? a.item_begin + (int)t : a.items;
             s_item = it;
             st_cluster_s32(map_to_rank(&s_item, 1), it);

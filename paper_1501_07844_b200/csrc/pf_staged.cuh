@@ -59,8 +59,8 @@ struct StagedArgs {
     float inv_c, ctau;
     unsigned int *resid_bits;
     unsigned long long *err_voxel;
-    unsigned long long *ticket;       // monotone work-item ticket counter (never reset)
-    unsigned long long ticket_base;   // its value at the start of this launch
+    unsigned long long *ticket;        // this launch's work-item ticket counter (0 at launch start)
+    unsigned long long *ticket_next;   // the other counter: zeroed here for the next launch (launches alternate)
     GraphConst g;
 };
 
@@ -226,11 +226,13 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
     // Dynamic work queue: a CTA takes the next ticket when it starts an item, so the items in flight are
     // always a window of ~gridDim consecutive tiles and the halo lines one tile loads from HBM are still in
     // L2 when its neighbours read them (a static round-robin lets CTAs drift apart by whole items on
-    // many-item volumes, which sent ~40 % extra halo traffic to HBM on 768^2 planes).  Every launch
-    // consumes exactly items + gridDim tickets (one failed grab per CTA), so the host knows the base.
+    // many-item volumes, which sent ~40 % extra halo traffic to HBM on 768^2 planes).  Two counters
+    // alternate between launches; each launch zeroes the one the next launch uses, so a launch's
+    // parameters do not depend on history and a sequence of launches can be replayed as a CUDA graph.
+    if (blockIdx.x == 0 && tid == 0) *a.ticket_next = 0ull;
     __shared__ int s_item;
     auto grab = [&]() -> int {
-        const unsigned long long t = atomicAdd(a.ticket, 1ull) - a.ticket_base;
+        const unsigned long long t = atomicAdd(a.ticket, 1ull);
         return t < (unsigned long long)(a.items - a.item_begin) ? a.item_begin + (int)t : a.items;
     };
     if (tid == 0) s_item = grab();

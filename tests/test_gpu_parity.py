@@ -175,6 +175,25 @@ def test_many_label_potts_cluster_kernel(K, dims, shift, monkeypatch):
     s.close()
 
 
+def test_cuda_graph_replay_equals_plain_launches(monkeypatch):
+    """pf_iterate replays whole check periods as a CUDA graph; the result is bitwise that of plain launches
+    (including the fused residual and odd check cadences), also after reset and mixed call sizes."""
+    for name, dims, k in (("C2", (40, 33, 27), 10), ("C5", (35, 21, 12), 3), ("C4", (41, 38, 29), 0)):
+        inp = P.generate(P.config(name).resized(*dims))
+        res = {}
+        for graphs in ("1", "0"):
+            monkeypatch.setenv("PF_GRAPHS", graphs)
+            s = solver_from_inputs(inp, check_every=k)
+            r1 = s.iterate(40, residual=True)
+            s.reset()
+            r2 = s.iterate(23, residual=True)
+            r3 = s.iterate(31, residual=True)
+            res[graphs] = (s.labeling()[0], s.flows(), r1, r2, r3, s.iterations())
+            s.close()
+        a, b = res["1"], res["0"]
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2:] == b[2:]
+
+
 def test_split_calls_equal_one_call():
     """iterate(a) + iterate(b) == iterate(a + b), bitwise (ping-pong bookkeeping)."""
     inp = P.generate(P.config("C2").resized(33, 30, 27))
