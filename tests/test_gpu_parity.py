@@ -65,7 +65,8 @@ def test_configs_scaled(name, dims, n, shift):
 
 
 @pytest.mark.parametrize("case", ["linf_potts", "linf_dag", "field_per_node", "k2", "line_x", "line_y", "single_voxel",
-                                  "one_plane_3d", "two_planes", "2d_ragged", "2d_dag"])
+                                  "one_plane_3d", "two_planes", "2d_ragged", "2d_dag", "k16_line_x", "k16_2d_small",
+                                  "k16_single_voxel", "k16_linf", "k12_per_node_field"])
 def test_edge_cases(case):
     cap = None
     if case == "linf_potts":
@@ -89,10 +90,21 @@ def test_edge_cases(case):
         inp = P.generate(P.config("C2").resized(35, 33, 2))
     elif case == "2d_ragged":
         inp = P.generate(P.config("C1").resized(97, 41, 1))
-    else:
+    elif case == "2d_dag":
         cfg = P.config("C4")
         inp = P.generate(P.Config("dag2d", 2, 45, 38, 1, "dag", 6, 4, 0.15, "sq", "per_node_uniform", 0.0, 0,
                                   seed=cfg.seed))
+    elif case == "k16_line_x":      # many labels: cluster kernel on degenerate shapes
+        inp = P.generate(P.config("C5").resized(41, 1, 1))
+    elif case == "k16_2d_small":
+        inp = P.generate(P.Config("k16_2d", 2, 9, 5, 1, "potts", 16, 3, 0.15, "abs", "scalar", 0.1, 0, seed=55))
+    elif case == "k16_single_voxel":
+        inp = P.generate(P.config("C5").resized(1, 1, 1))
+    elif case == "k16_linf":
+        inp, cap = P.generate(P.config("C5").resized(19, 11, 7)), O.CAP_LINF
+    else:                           # per-node capacity fields: the cluster kernel falls back to one CTA
+        import dataclasses
+        inp = with_field_per_node(P.generate(dataclasses.replace(P.config("C5"), classes=12).resized(17, 13, 6)))
     u, q, ur, qr = _run_both(inp, 150, cap=cap)
     compare(u, q, ur, qr)
 
