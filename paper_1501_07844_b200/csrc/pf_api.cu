@@ -422,6 +422,12 @@ void choose_chunking(pf_solver *s) {
         const int nzi = s->zhi - s->zlo;
         const int64_t wslots = s->cluster ? slots / 2 : slots;   // concurrent work items
         int n = nzi > 0 ? best_chunks(tiles, nzi, wslots) : 0;
+        // cluster kernel: chunks of <= 32 planes.  Its 74 work slots put a tile's y-neighbour (tiles_x
+        // tickets later) about tiles_x / 74 chunk-lengths behind; with 48-plane chunks on 768^2 planes that
+        // is ~15 planes, past the ~10 planes of traffic L2 holds, and the y-halo rows came from HBM
+        // (ncu: 1.31x algorithmic bytes over 20 back-to-back iterations vs 1.08x with 24-plane chunks;
+        // sustained: 32 planes is the fastest, tools/ab.py)
+        if (s->cluster && nzi > 32) n = std::max(n, (nzi + 31) / 32);
         if (const char *zc = getenv("PF_ZCHUNK")) {   // experiments (tools/): force the z-chunk length
             const int want = atoi(zc);
             if (want > 0 && nzi > 0) n = (nzi + want - 1) / want;
