@@ -47,6 +47,13 @@ __device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mb
                  : "memory");
 }
 
+// the (m_h, a_h) pair of one point as ONE 8-byte st.async
+__device__ __forceinline__ void st_async_f32x2(uint32_t addr, float v0, float v1, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+                 "r"(__float_as_uint(v0)), "r"(__float_as_uint(v1)), "r"(mbar)
+                 : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -84,8 +91,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     float *Qo = sm + L::off_Qo(a.s_ch);
     // partner's (m_h, a_h) per point, written remotely; double-buffered by plane parity because the
     // partner may run up to one plane ahead (its sends for plane k+1 need only OUR sends for plane k)
-    float *Xm = sm + CL::off_X(a.s_ch);       // [parity][XPTS]
-    float *Xa = Xm + 2 * CL::XPTS;            // [parity][XPTS]
+    float *X2 = sm + CL::off_X(a.s_ch);       // [parity][XPTS][(m_h, a_h)]
     const int SSZ = L::ssz(a.s_ch);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + CL::floats(a.s_ch));
 
@@ -105,10 +111,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     const int64_t qps = (int64_t)3 * NF * P;
     const float k2 = kLog2e * a.inv_c;
     const int xpt = ly * 33 + (lx < 0 ? 0 : lx);             // this point's exchange slot
-    const uint32_t xm_remote = map_to_rank(Xm + xpt, other);
-    const uint32_t xa_remote = map_to_rank(Xa + xpt, other);
+    const uint32_t x_remote = map_to_rank(X2 + 2 * xpt, other);
     const uint32_t barx_remote = map_to_rank(&bars[2], other);   // partner's "(m_h, a_h) received" mbarriers
-    constexpr uint32_t kXBuf = 4u * CL::XPTS;                      // byte stride of the parity buffers
+    constexpr uint32_t kXBuf = 8u * CL::XPTS;                      // byte stride of the parity buffers
     constexpr uint32_t kXBytes = 4u * (32 * TY + 32 + TY);        // one float per tile + halo point
 
     if (tid == 0) {
@@ -259,13 +264,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
             if (tid == 0) mbar_arrive_expect_tx(&bars[2 + xb], 2 * kXBytes);   // arm (bytes may already be in)
             const float ah = sa + sb;
             if (lx >= 0) {
-                st_async_f32(xm_remote + xb * kXBuf, mh, barx_remote + xb * 8u);
-                st_async_f32(xa_remote + xb * kXBuf, ah, barx_remote + xb * 8u);
+                st_async_f32x2(x_remote + xb * kXBuf, mh, ah, barx_remote + xb * 8u);
             }
             mbar_wait(&bars[2 + xb], (k >> 1) & 1);
             float sum = 1.f;
             if (lx >= 0) {
-                const float mo = Xm[xb * CL::XPTS + xpt], ao = Xa[xb * CL::XPTS + xpt];
+                const float2 xo = reinterpret_cast<const float2 *>(X2)[xb * CL::XPTS + xpt];
+                const float mo = xo.x, ao = xo.y;
                 const float m0 = rank == 0 ? mh : mo, m1 = rank == 0 ? mo : mh;
                 const float a0 = rank == 0 ? ah : ao, a1 = rank == 0 ? ao : ah;
                 float f0 = 1.f, f1 = 1.f;
