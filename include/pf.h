@@ -170,6 +170,11 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual);
  * label id ("thresholded"). */
 pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax);
 
+/* Labeling of any node v of the graph (row a9, "intermediate labels on demand"): u_v(x) =
+ * sum_B W_(v,B) u_B(x) over the end labels (path weights P:199-209), u_S = 1.  node: graph node
+ * id (0 = S).  u_node: [V_local] fp32, host or device.  Errors: PF_ERR_INVALID (node out of range, NULL). */
+pf_status pf_get_node_labeling(pf_solver *s, int32_t node, float *u_node);
+
 /* Spatial flows of the owned slab as [num_nodes-1][ndim][V_local], node-id order. */
 pf_status pf_get_flows(pf_solver *s, float *q);
 

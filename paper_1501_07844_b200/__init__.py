@@ -34,7 +34,7 @@ PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE, PF_S_SCALED_FIELD 
 _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_CUDA", 5: "PF_ERR_UNSUPPORTED",
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
-EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
+EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
@@ -90,6 +90,7 @@ _sig = {
     "pf_run": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_float, _P(ctypes.c_int32), _P(ctypes.c_float)]),
     "pf_get_labeling": (ctypes.c_int, [_vp, _vp, _vp]),
     "pf_get_flows": (ctypes.c_int, [_vp, _vp]),
+    "pf_get_node_labeling": (ctypes.c_int, [_vp, ctypes.c_int32, _vp]),
     "pf_get_energy": (ctypes.c_int, [_vp, _P(ctypes.c_double), _P(ctypes.c_double)]),
     "pf_iterations": (ctypes.c_int, [_vp, _P(ctypes.c_int64)]),
     "pf_set_stream": (ctypes.c_int, [_vp, _vp]),
@@ -202,6 +203,10 @@ def pf_get_labeling(s: int, u=None, argmax=None):
 
 def pf_get_flows(s: int, q):
     _check(_lib.pf_get_flows(s, _ptr(q)))
+
+
+def pf_get_node_labeling(s: int, node: int, out):
+    _check(_lib.pf_get_node_labeling(s, int(node), _ptr(out)))
 
 
 def pf_get_energy(s: int):

@@ -1088,6 +1088,32 @@ pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {
     return check_numeric(s);
 }
 
+pf_status pf_get_node_labeling(pf_solver *s, int32_t node, float *u_node) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (!u_node) return fail(PF_ERR_INVALID, "u_node is NULL");
+    if (node < 0 || node >= s->gc.num_nodes) return fail(PF_ERR_INVALID, "node %d out of range", node);
+    DeviceGuard dg(s->device);
+    NodeWeights w;
+    memset(&w, 0, sizeof(w));
+    const int NL = s->gc.NL;
+    for (int l = 0; l < NL && l < 16; ++l)
+        w.W[l] = node == 0 ? 1.f : s->gc.W[s->gc.pos_of_node[node]][l];   // W_(S, B) = 1 (reading R9)
+    const int64_t V = s->nx * s->ny * s->nzl;
+    const bool dev = is_device_ptr(u_node);
+    float *dst = u_node;
+    if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V * sizeof(float), s->stream), "node labeling scratch");
+    CK(launch_node_labeling(s->u[s->cur], dst, w, NL, (int)s->nx, (int)s->ny, (int)s->pitch, s->nzl, s->stream),
+       "node labeling kernel");
+    s->launches++;
+    if (!dev) {
+        CK(cudaMemcpyAsync(u_node, dst, (size_t)V * sizeof(float), cudaMemcpyDeviceToHost, s->stream), "download");
+        CK(cudaStreamSynchronize(s->stream), "sync");
+        cudaFreeAsync(dst, s->stream);
+    }
+    return check_numeric(s);
+}
+
 pf_status pf_get_flows(pf_solver *s, float *q) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;

@@ -31,6 +31,23 @@ __global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__
     }
 }
 
+// Labeling of any node: u_v(x) = sum_B W_(v,B) u_B(x) over the end labels B (path weights P:199-209),
+// written densely as [z][y][x] (x fastest).
+__global__ void node_labeling_kernel(const float *__restrict__ u, float *__restrict__ out, NodeWeights w, int NL,
+                                     int nx, int ny, int pitch, int64_t nz) {
+    const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / ((int64_t)nx * ny);
+        const int r = (int)(i - z * (int64_t)nx * ny);
+        const int y = r / nx, x = r - y * nx;
+        const float *b = u + z * NL * P + (int64_t)y * pitch + x;
+        float acc = 0.f;
+        for (int l = 0; l < NL; ++l)
+            if (w.W[l] != 0.f) acc = fmaf(w.W[l], b[l * P], acc);
+        out[i] = acc;
+    }
+}
+
 __global__ void min_kernel(const float *__restrict__ p, int64_t n, unsigned int *out_bits_neg) {
     // records whether any value is negative or NaN (out = 1)
     bool bad = false;
@@ -172,6 +189,12 @@ cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, 
 
 cudaError_t launch_f32_to_bf16(const float *src, uint16_t *dst, int64_t n, cudaStream_t st) {
     f32_to_bf16_kernel<<<1184, 256, 0, st>>>(src, dst, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_node_labeling(const float *u, float *out, const NodeWeights &w, int NL, int nx, int ny, int pitch,
+                                 int64_t nz, cudaStream_t st) {
+    node_labeling_kernel<<<1184, 256, 0, st>>>(u, out, w, NL, nx, ny, pitch, nz);
     return cudaGetLastError();
 }
 

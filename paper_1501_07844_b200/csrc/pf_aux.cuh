@@ -23,7 +23,13 @@ struct EnergyArgs {
 
 constexpr int kEnergyBlocks = 592;
 
+struct NodeWeights {
+    float W[16];   // W_(v, B) per end label B (0: B not below v)
+};
+
 cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st);
+cudaError_t launch_node_labeling(const float *u, float *out, const NodeWeights &w, int NL, int nx, int ny, int pitch,
+                                 int64_t nz, cudaStream_t st);
 cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz,
                           cudaStream_t st);
 cudaError_t launch_f32_to_bf16(const float *src, uint16_t *dst, int64_t n, cudaStream_t st);

@@ -8,7 +8,7 @@ import numpy as np
 from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SCALED_FIELD,
                PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_get_energy, pf_get_flows, pf_get_kernel_info,
-               pf_get_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
+               pf_get_labeling, pf_get_node_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
                pf_set_stream)
 
 
@@ -80,6 +80,13 @@ class Solver:
             argmax_out = np.empty(self.shape, dtype=np.uint8)
         pf_get_labeling(self.h, u_out, argmax_out)
         return u_out, argmax_out
+
+    def node_labeling(self, node: int, out=None):
+        """u_v = sum_B W_(v,B) u_B of any graph node (intermediate labels on demand), [z][y][x] float32."""
+        if out is None:
+            out = np.empty(self.shape, dtype=np.float32)
+        pf_get_node_labeling(self.h, node, out)
+        return out
 
     def flows(self):
         q = np.empty((self.num_nodes - 1, self.ndim) + self.shape, dtype=np.float32)

@@ -206,6 +206,28 @@ def test_cuda_graph_replay_equals_plain_launches(monkeypatch):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2:] == b[2:]
 
 
+@pytest.mark.parametrize("name", ["C3", "C4", "I2"])
+def test_intermediate_node_labelings(name):
+    """pf_get_node_labeling: u_v = sum_B W_(v,B) u_B from the GPU end-label state; the
+    source's labeling is sum_L u_L = 1; internal nodes match the children's sum through the edge weights."""
+    inp = P.generate(P.config(name).resized(23, 19, 9))
+    g = inp.graph
+    s = solver_from_inputs(inp)
+    s.iterate(40)
+    u, _ = s.labeling()
+    leaves = [v for v in range(1, g.num_nodes) if v not in set(g.parent)]
+    node_u = {v: s.node_labeling(v).astype(np.float64) for v in range(g.num_nodes)}
+    s.close()
+    assert np.max(np.abs(node_u[0] - 1.0)) < 1e-5
+    for i, v in enumerate(leaves):
+        assert np.array_equal(node_u[v], u[i])
+    for v in range(1, g.num_nodes):
+        kids = [(c, w) for p, c, w in zip(g.parent, g.child, g.weight) if p == v]
+        if kids:
+            want = sum(float(w) * node_u[c] for c, w in kids)
+            assert np.max(np.abs(node_u[v] - want)) < 1e-5
+
+
 def test_split_calls_equal_one_call():
     """iterate(a) + iterate(b) == iterate(a + b), bitwise (ping-pong bookkeeping)."""
     inp = P.generate(P.config("C2").resized(33, 30, 27))
