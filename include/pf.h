@@ -209,6 +209,20 @@ pf_status pf_halo_regions(pf_solver *s, pf_halo *h);
  * after the senders' pending work. */
 pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n);
 
+/* Fused halo exchange for consecutive z-slab solvers[0..n-1] (ascending z) driven from one process,
+ * on one or several devices with peer access: after linking, every iteration
+ * kernel also TMA-stores its boundary planes of the new state straight into the neighbours' halo
+ * planes (plane 0 -> the slab below, q^z of the last plane -> the slab above; peer memory over
+ * NVLink), so no exchange step remains.  Requires the TMA-staged kernel variants that store whole
+ * tiles (PF_ERR_UNSUPPORTED otherwise: use pf_exchange_local) and slabs at the same iteration.  Linked
+ * solvers must be iterated together with pf_iterate_linked (pf_iterate / pf_iterate_phase return
+ * PF_ERR_STATE) and destroyed together. */
+pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n);
+
+/* `iters` iterations of every linked slab; iteration t+1 of a slab is ordered (events, no host sync)
+ * after iteration t of both neighbours.  residual: as pf_iterate, max over the slabs. */
+pf_status pf_iterate_linked(pf_solver *const *solvers, int32_t n, int32_t iters, float *residual);
+
 /* Static description of the kernel configuration (for reports). */
 typedef struct {
     int32_t tile_x, tile_y, z_chunk, threads_per_cta, ctas, regs_per_thread, smem_bytes, ctas_per_sm;

@@ -34,7 +34,8 @@ PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE, PF_S_SCALED_FIELD 
 _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_CUDA", 5: "PF_ERR_UNSUPPORTED",
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
-EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
+EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling",
+            "pf_link_slabs", "pf_iterate_linked", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
@@ -96,6 +97,8 @@ _sig = {
     "pf_set_stream": (ctypes.c_int, [_vp, _vp]),
     "pf_halo_regions": (ctypes.c_int, [_vp, _P(pf_halo)]),
     "pf_exchange_local": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32]),
+    "pf_link_slabs": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32]),
+    "pf_iterate_linked": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int32, _P(ctypes.c_float)]),
     "pf_get_kernel_info": (ctypes.c_int, [_vp, _P(pf_kernel_info)]),
     "pf_destroy": (None, [_vp]),
     "pf_last_error": (ctypes.c_char_p, []),
@@ -234,6 +237,19 @@ def pf_halo_regions(s: int) -> pf_halo:
 def pf_exchange_local(solvers: Sequence[int]):
     arr = (ctypes.c_void_p * len(solvers))(*solvers)
     _check(_lib.pf_exchange_local(ctypes.cast(arr, _P(ctypes.c_void_p)), len(solvers)))
+
+
+def pf_link_slabs(solvers: Sequence[int]):
+    arr = (ctypes.c_void_p * len(solvers))(*solvers)
+    _check(_lib.pf_link_slabs(ctypes.cast(arr, _P(ctypes.c_void_p)), len(solvers)))
+
+
+def pf_iterate_linked(solvers: Sequence[int], iters: int, want_residual: bool = False) -> Optional[float]:
+    arr = (ctypes.c_void_p * len(solvers))(*solvers)
+    r = ctypes.c_float(-1.0)
+    _check(_lib.pf_iterate_linked(ctypes.cast(arr, _P(ctypes.c_void_p)), len(solvers), int(iters),
+                                  ctypes.byref(r) if want_residual else None))
+    return float(r.value) if want_residual else None
 
 
 def pf_get_kernel_info(s: int) -> dict:

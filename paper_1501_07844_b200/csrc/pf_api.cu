@@ -229,6 +229,9 @@ struct pf_solver {
     unsigned int *d_resid = nullptr;
     unsigned long long *d_err = nullptr;   // [0] error voxel, [1], [2] work-item ticket counters
     int launch_parity = 0;                 // which ticket counter the next staged launch uses
+    // fused halo exchange (pf_link_slabs): neighbours and tensor maps of their state buffers
+    pf_solver *nb_below = nullptr, *nb_above = nullptr;
+    CUtensorMap tm_uo_nb[2], tm_qo_nb[2], tm_qz_nb[2];
     // CUDA graph of `graph_iters` whole iterations (pf_iterate), replayed when the state matches the
     // capture: same ping-pong buffer, same counter parity, check iterations at the same positions
     cudaGraphExec_t graph = nullptr;
@@ -847,6 +850,16 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
         sa.u_out = s->u[1 - s->cur];
         sa.q_out = s->q[1 - s->cur];
         sa.check = check;
+        if (s->nb_below) {
+            sa.link_below = 1;
+            sa.tm_uo_nb = s->tm_uo_nb[1 - s->cur];
+            sa.tm_qo_nb = s->tm_qo_nb[1 - s->cur];
+            sa.nb_plane = (int)s->nb_below->nzl + 1;
+        }
+        if (s->nb_above) {
+            sa.link_above = 1;
+            sa.tm_qz_nb = s->tm_qz_nb[1 - s->cur];
+        }
         sa.ticket = s->d_err + 1 + s->launch_parity;
         sa.ticket_next = s->d_err + 2 - s->launch_parity;
         // cluster kernel: 2 CTAs per item and one ticket grab per cluster
@@ -992,6 +1005,7 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
     if (n < 0) return fail(PF_ERR_INVALID, "n must be >= 0");
+    if (s->nb_below || s->nb_above) return fail(PF_ERR_STATE, "linked slab: iterate with pf_iterate_linked");
     if (s->phase_pending) return fail(PF_ERR_STATE, "pf_iterate: an iteration split by pf_iterate_phase is open");
     DeviceGuard dg(s->device);
     bool any_check = false;
@@ -1042,6 +1056,7 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual) {
     if (st != PF_OK) return st;
     if (phase != 0 && phase != 1) return fail(PF_ERR_INVALID, "phase must be 0 or 1");
     if (s->alm) return fail(PF_ERR_UNSUPPORTED, "pf_iterate_phase: not for the explicit-flow ALM");
+    if (s->nb_below || s->nb_above) return fail(PF_ERR_STATE, "linked slab: iterate with pf_iterate_linked");
     if ((phase == 0) == (s->phase_pending != 0))
         return fail(PF_ERR_STATE, phase == 0 ? "phase 0 issued twice" : "phase 1 without phase 0");
     DeviceGuard dg(s->device);
@@ -1263,6 +1278,142 @@ pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n) {
     }
     for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
     return PF_OK;
+}
+
+pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n) {
+    if (!solvers || n < 2) return fail(PF_ERR_INVALID, "need >= 2 solvers");
+    for (int i = 0; i < n; ++i) {
+        pf_status st = check_usable(solvers[i]);
+        if (st != PF_OK) return st;
+        const pf_solver *s = solvers[i];
+        if (!s->staged || !(s->cluster || s->sinfo.ostage == 1))
+            return fail(PF_ERR_UNSUPPORTED, "link: solver %d's kernel variant stores no whole tiles (use "
+                                            "pf_exchange_local)", i);
+        if (s->phase_pending) return fail(PF_ERR_STATE, "link: solver %d has an open split iteration", i);
+    }
+    for (int i = 0; i + 1 < n; ++i) {
+        const pf_solver *lo = solvers[i], *hi = solvers[i + 1];
+        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->pitch != hi->pitch ||
+            lo->gc.NF != hi->gc.NF || lo->gc.NL != hi->gc.NL || lo->cluster != hi->cluster || lo->cur != hi->cur ||
+            lo->sinfo.tile_y != hi->sinfo.tile_y)
+            return fail(PF_ERR_INVALID, "link: solvers %d and %d are not consecutive slabs of one volume in step", i,
+                        i + 1);
+    }
+    for (int i = 0; i + 1 < n; ++i) {   // peer access between devices (TMA stores into the neighbour's memory)
+        const int a = solvers[i]->device, b = solvers[i + 1]->device;
+        if (a == b) continue;
+        int ok1 = 0, ok2 = 0;
+        cudaDeviceCanAccessPeer(&ok1, a, b);
+        cudaDeviceCanAccessPeer(&ok2, b, a);
+        if (!ok1 || !ok2) return fail(PF_ERR_UNSUPPORTED, "link: no peer access between devices %d and %d", a, b);
+        {
+            DeviceGuard dg(a);
+            if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();   // already enabled is fine
+        }
+        {
+            DeviceGuard dg(b);
+            if (cudaDeviceEnablePeerAccess(a, 0) != cudaSuccess) cudaGetLastError();
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        pf_solver *s = solvers[i];
+        const int ty = s->sinfo.tile_y, NF = s->gc.NF, NL = s->gc.NL;
+        const int cq = s->cluster ? NL / 2 : 3 * NF, cl = s->cluster ? NL / 2 : NL, cz = s->cluster ? NL / 2 : NF;
+        bool ok = true;
+        s->nb_below = i > 0 ? solvers[i - 1] : nullptr;
+        s->nb_above = i + 1 < n ? solvers[i + 1] : nullptr;
+        for (int b = 0; b < 2; ++b) {
+            if (s->nb_below) {   // below neighbour's buffers: its upper halo plane receives our plane 0
+                const pf_solver *t = s->nb_below;
+                ok = ok && encode4d(&s->tm_uo_nb[b], t->u_alloc[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl);
+                ok = ok && encode4d(&s->tm_qo_nb[b], t->q_alloc[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2,
+                                    32, ty, cq);
+            }
+            if (s->nb_above) {   // above neighbour's buffers: its lower halo plane receives our last q^z
+                const pf_solver *t = s->nb_above;
+                ok = ok && encode4d(&s->tm_qz_nb[b], t->q_alloc[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2,
+                                    32, ty, cz);
+            }
+        }
+        if (!ok) return fail(PF_ERR_CUDA, "link: cuTensorMapEncodeTiled failed");
+    }
+    return PF_OK;
+}
+
+pf_status pf_iterate_linked(pf_solver *const *solvers, int32_t n, int32_t iters, float *residual) {
+    if (!solvers || n < 1 || iters < 0) return fail(PF_ERR_INVALID, "need >= 1 solver and iters >= 0");
+    for (int i = 0; i < n; ++i) {
+        pf_status st = check_usable(solvers[i]);
+        if (st != PF_OK) return st;
+        if (i > 0 && solvers[i]->nb_below != solvers[i - 1])
+            return fail(PF_ERR_INVALID, "iterate_linked: solvers are not linked in this order");
+    }
+    // iteration t+1 of a slab starts after iteration t of both neighbours: they write its next halo planes
+    // (RAW) and read the buffers its next kernel writes into (WAR)
+    std::vector<cudaEvent_t> ev[2];
+    for (int e = 0; e < 2; ++e) {
+        ev[e].resize(n);
+        for (int i = 0; i < n; ++i) {
+            pf_solver *s = solvers[i];
+            DeviceGuard dg(s->device);
+            CK(cudaEventCreateWithFlags(&ev[e][i], cudaEventDisableTiming), "event");
+        }
+    }
+    bool any_check = false;
+    pf_status st = PF_OK;
+    for (int t = 0; t < iters && st == PF_OK; ++t) {
+        std::vector<cudaEvent_t> &prev = ev[(t + 1) & 1], &curv = ev[t & 1];
+        for (int i = 0; i < n; ++i) {
+            pf_solver *s = solvers[i];
+            DeviceGuard dg(s->device);
+            if (t > 0) {
+                if (i > 0) CK(cudaStreamWaitEvent(s->stream, prev[i - 1], 0), "wait");
+                if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, prev[i + 1], 0), "wait");
+            } else {   // the first iteration waits for whatever the neighbours had queued
+                if (i > 0) {
+                    CK(cudaEventRecord(curv[i - 1], solvers[i - 1]->stream), "record");
+                    CK(cudaStreamWaitEvent(s->stream, curv[i - 1], 0), "wait");
+                }
+                if (i + 1 < n) {
+                    CK(cudaEventRecord(curv[i + 1], solvers[i + 1]->stream), "record");
+                    CK(cudaStreamWaitEvent(s->stream, curv[i + 1], 0), "wait");
+                }
+            }
+            const int check = check_this_iteration(s);
+            if (check) {
+                CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
+                any_check = true;
+            }
+            if ((st = launch_items(s, 0, s->items, check)) != PF_OK) break;
+        }
+        for (int i = 0; i < n && st == PF_OK; ++i) {
+            pf_solver *s = solvers[i];
+            DeviceGuard dg(s->device);
+            CK(cudaEventRecord(curv[i], s->stream), "record");
+            s->cur = 1 - s->cur;
+            s->iters += 1;
+        }
+    }
+    // the neighbours' last kernels wrote this slab's halo planes: later work on its stream waits for them
+    if (iters > 0 && st == PF_OK) {
+        std::vector<cudaEvent_t> &last = ev[(iters - 1) & 1];
+        for (int i = 0; i < n; ++i) {
+            pf_solver *s = solvers[i];
+            DeviceGuard dg(s->device);
+            if (i > 0) CK(cudaStreamWaitEvent(s->stream, last[i - 1], 0), "wait");
+            if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, last[i + 1], 0), "wait");
+        }
+    }
+    float r = -1.f;
+    for (int i = 0; i < n && st == PF_OK; ++i) {
+        float ri = -1.f;
+        st = read_residual(solvers[i], any_check, residual ? &ri : nullptr);
+        r = std::max(r, ri);
+    }
+    for (int e = 0; e < 2; ++e)
+        for (int i = 0; i < n; ++i) cudaEventDestroy(ev[e][i]);
+    if (residual) *residual = r;
+    return st;
 }
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {

@@ -214,9 +214,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
         };
         auto store_q = [&](int z) {   // thread 0: the three k-blocks of the flow tile of plane z
 #pragma unroll
-            for (int k = 0; k < 3; ++k)
-                tma_store_4d(&a.tm_qo, Qo + (z & 1) * L::QOSZ + k * NLC * TY * 32, x0, y0, k * NF + lb, z + 1,
-                             pol_out);
+            for (int k = 0; k < 3; ++k) {
+                const float *blk = Qo + (z & 1) * L::QOSZ + k * NLC * TY * 32;
+                tma_store_4d(&a.tm_qo, blk, x0, y0, k * NF + lb, z + 1, pol_out);
+                // fused halo exchange (pf_staged.cuh): plane 0 -> below, q^z of the last plane -> above
+                if (a.link_below && z == 0) tma_store_4d(&a.tm_qo_nb, blk, x0, y0, k * NF + lb, a.nb_plane, pol_out);
+                if (k == 2 && a.link_above && z == a.nzl - 1)
+                    tma_store_4d(&a.tm_qz_nb, blk, x0, y0, k * NF + lb, 0, pol_out);
+            }
         };
 
         auto plane_step = [&](const int p, float (&qc)[3][NLC], float (&qn)[3][NLC]) {
@@ -309,7 +314,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                     fence_proxy_async();
                     issue(p + 2, st, x0, y0);
                 }
-                if (p < zc1) tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, lb, p + 1, pol_out);
+                if (p < zc1) {
+                    tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, lb, p + 1, pol_out);
+                    if (a.link_below && p == 0)
+                        tma_store_4d(&a.tm_uo_nb, Uo + (p & 1) * L::UOSZ, x0, y0, lb, a.nb_plane, pol_out);
+                }
                 if (p - 2 >= zc0) store_q(p - 2);
                 bulk_commit();
             }

@@ -43,6 +43,12 @@ struct StagedArgs {
     CUtensorMap tm_S;   // S field, 4-D (x, y, channel, plane); unused when s_ch == 0
     CUtensorMap tm_uo;  // output u, store box (32, TY, NL)                                   [OSTAGE]
     CUtensorMap tm_qo;  // output q, store box (32, TY, 3*NF) [OSTAGE 1] or (32, 1, NF/G)   [OSTAGE 2]
+    // fused halo exchange (pf_link_slabs): the boundary planes of the new state are also TMA-stored into
+    // the neighbouring slabs' halo planes (peer memory); tile stores only (OSTAGE 1 / cluster kernel)
+    CUtensorMap tm_uo_nb;   // below neighbour's new u     (box as tm_uo), halo plane coordinate nb_plane
+    CUtensorMap tm_qo_nb;   // below neighbour's new q     (box as tm_qo)
+    CUtensorMap tm_qz_nb;   // above neighbour's new q     (box: the z-component block), coordinate 0
+    int link_below, link_above, nb_plane;
     const float *q_in;  // plane 0 of input q (chunk-start q^z(zc0-1) read)
     float *u_out;
     float *q_out;
@@ -308,6 +314,16 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
             }
         };
 
+        // thread 0, OSTAGE 1: the flow tile of plane z to this slab's new state, and with linked slabs
+        // plane 0 to the below neighbour's upper halo plane, q^z of the last plane to the above
+        // neighbour's lower halo plane (the fused halo exchange)
+        auto store_q = [&](int z) {
+            tma_store_4d(&a.tm_qo, Qo + (z & 1) * L::QOSZ, x0, y0, 0, z + 1, pol_out);
+            if (a.link_below && z == 0) tma_store_4d(&a.tm_qo_nb, Qo + (z & 1) * L::QOSZ, x0, y0, 0, a.nb_plane, pol_out);
+            if (a.link_above && z == a.nzl - 1)
+                tma_store_4d(&a.tm_qz_nb, Qo + (z & 1) * L::QOSZ + 2 * NF * TY * 32, x0, y0, 2 * NF, 0, pol_out);
+        };
+
         auto plane_step = [&](const int p, float (&qc)[3][NFG], float (&qn)[3][NFG]) {
             const int k = kbase + (p - zc0);
             const int st = k & 1;
@@ -434,9 +450,12 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                     issue(p + 2, st, x0, y0);
                 }
                 if (OSTAGE) {
-                    if (p < zc1) tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, 0, p + 1, pol_out);
-                    if (OSTAGE == 1 && p - 2 >= zc0)
-                        tma_store_4d(&a.tm_qo, Qo + (p & 1) * L::QOSZ, x0, y0, 0, p - 1, pol_out);
+                    if (p < zc1) {
+                        tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, 0, p + 1, pol_out);
+                        if (OSTAGE == 1 && a.link_below && p == 0)   // fused halo exchange: plane 0 -> below
+                            tma_store_4d(&a.tm_uo_nb, Uo + (p & 1) * L::UOSZ, x0, y0, 0, a.nb_plane, pol_out);
+                    }
+                    if (OSTAGE == 1 && p - 2 >= zc0) store_q(p - 2);
                     bulk_commit();
                     ++since_q;
                 }
@@ -467,8 +486,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
             fence_proxy_async();
             __syncthreads();
             if (tid == 0) {
-                for (int z = max(zc0, pend - 1); z < zc1; ++z)
-                    tma_store_4d(&a.tm_qo, Qo + (z & 1) * L::QOSZ, x0, y0, 0, z + 1, pol_out);
+                for (int z = max(zc0, pend - 1); z < zc1; ++z) store_q(z);
                 bulk_commit();
             }
         }

@@ -7,7 +7,7 @@ import numpy as np
 
 from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SCALED_FIELD,
                PF_S_SHARED_FIELD,
-               pf_create, pf_destroy, pf_exchange_local, pf_get_energy, pf_get_flows, pf_get_kernel_info,
+               pf_create, pf_destroy, pf_exchange_local, pf_iterate_linked, pf_link_slabs, pf_get_energy, pf_get_flows, pf_get_kernel_info,
                pf_get_labeling, pf_get_node_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
                pf_set_stream)
 
@@ -132,12 +132,20 @@ class SlabSet:
     """A volume split into consecutive z-slab solvers driven from one process (one or several
     devices); halos are exchanged by pf_exchange_local after every iteration."""
 
-    def __init__(self, solvers: Sequence[Solver], phased: bool = False):
+    def __init__(self, solvers: Sequence[Solver], phased: bool = False, fused: bool = False):
+        """phased: every iteration as pf_iterate_phase 0 + 1 (the NCCL multi-GPU schedule); fused: link the
+        slabs (pf_link_slabs) so the iteration kernels store their boundary planes straight into the
+        neighbours' halos (peer memory) -- no exchange step."""
         self.solvers = list(solvers)
         self.handles = [s.h for s in self.solvers]
-        self.phased = phased   # run every iteration as pf_iterate_phase 0 + 1 (the multi-GPU schedule)
+        self.phased = phased
+        self.fused = fused and len(self.solvers) > 1
+        if self.fused:
+            pf_link_slabs(self.handles)
 
     def iterate(self, n: int, residual: bool = False):
+        if self.fused:
+            return pf_iterate_linked(self.handles, n, residual)
         r = None
         for t in range(n):
             last = residual and t == n - 1

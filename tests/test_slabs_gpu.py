@@ -18,7 +18,7 @@ def kernel_variant(request, monkeypatch):
     return request.param
 
 
-@pytest.mark.parametrize("phased", [False, True])
+@pytest.mark.parametrize("phased", [False, True, "fused"])
 @pytest.mark.parametrize("name,dims,parts", [("C2", (48, 40, 36), 2), ("C2", (48, 40, 37), 3), ("C4", (40, 33, 29), 4),
                                              ("C3", (33, 30, 24), 8), ("C5", (36, 33, 20), 5),
                                              ("C2", (40, 33, 9), 9)])   # one-plane slabs
@@ -32,7 +32,13 @@ def test_slabs_bitwise_equal_single_domain(name, dims, parts, phased):
     u_ref, a_ref = ref.labeling()
     q_ref = ref.flows()
     e_ref = ref.energy()
-    slabs = pf.SlabSet([solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, parts)], phased=phased)
+    solvers = [solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, parts)]
+    if phased == "fused":
+        if not all(s.kernel_info()["staged"] for s in solvers):
+            pytest.skip("fused halo stores need the TMA-staged kernels")
+        slabs = pf.SlabSet(solvers, fused=True)
+    else:
+        slabs = pf.SlabSet(solvers, phased=phased)
     slabs.iterate(25)
     u, a = slabs.labeling()
     q = slabs.flows()
@@ -63,3 +69,28 @@ def test_phase_order_errors():
     s.iterate_phase(1)
     assert s.iterations() == 1
     s.close()
+
+
+def test_linked_slab_rules(monkeypatch):
+    """Linked slabs iterate only through pf_iterate_linked; kernel variants without whole-tile stores
+    refuse to link (they keep pf_exchange_local)."""
+    cfg = P.config("C2").resized(40, 33, 12)
+    inp = P.generate(cfg)
+    if solver_from_inputs(inp).kernel_info()["staged"]:
+        ss = [solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, 2)]
+        pf.pf_link_slabs([s.h for s in ss])
+        for s in ss:
+            with pytest.raises(pf.PFError) as ei:
+                s.iterate(1)
+            assert ei.value.status == pf.PF_ERR_STATE
+        pf.pf_iterate_linked([s.h for s in ss], 3)
+        assert all(s.iterations() == 3 for s in ss)
+        for s in ss:
+            s.close()
+    monkeypatch.setenv("PF_ITER_KERNEL", "global")
+    ss = [solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, 2)]
+    with pytest.raises(pf.PFError) as ei:
+        pf.pf_link_slabs([s.h for s in ss])
+    assert ei.value.status == pf.PF_ERR_UNSUPPORTED
+    for s in ss:
+        s.close()
