@@ -163,11 +163,13 @@ def run_ours(args, rank, world, local_rank):
     iters = args.iters or base.iters
     g, slab, D, S = _inputs_for_rank(cfg, rank, world)
 
+    ipc = args.transport == "ipc" and world > 1
+
     def make(slab_):
         return pf.Solver((cfg.nx, cfg.ny, cfg.nz), 3, (g.num_nodes, g.parent, g.child, g.weight), D, s_shared=S,
-                         c=cfg.c, tau=cfg.tau, check_every=10, slab=slab_)
+                         c=cfg.c, tau=cfg.tau, check_every=10, slab=slab_, ipc=ipc)
 
-    ds = DistSolver(make, cfg.nz, rank, world, dev)
+    ds = DistSolver(make, cfg.nz, rank, world, dev, transport=args.transport)
     s = ds.solver
     stream = torch.cuda.current_stream(dev)
     V = cfg.nx * cfg.ny * (slab[1] - slab[0])
@@ -236,14 +238,14 @@ def run_ours(args, rank, world, local_rank):
         def e2e_step():
             def mk(slab_):
                 return pf.Solver((cfg.nx, cfg.ny, cfg.nz), 3, (gH.num_nodes, gH.parent, gH.child, gH.weight), DH,
-                                 s_shared=SH, c=cfg.c, tau=cfg.tau, check_every=10, slab=slab_)
+                                 s_shared=SH, c=cfg.c, tau=cfg.tau, check_every=10, slab=slab_, ipc=ipc)
             if world == 1:   # the single-GPU user path: one Solver on its own stream
                 sv = mk(None)
                 sv.iterate(iters)
                 sv.labeling(u_host, lab_host)
                 sv.close()
                 return
-            d = DistSolver(mk, cfg.nz, rank, world, dev)
+            d = DistSolver(mk, cfg.nz, rank, world, dev, transport=args.transport)
             d.iterate(iters)
             d.solver.labeling(u_host, lab_host)
             d.close()
@@ -276,7 +278,8 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg.name + (": 3D Potts 256^3, K=8, 300 iterations" if world == 1 else
                                                 f": 3D Potts 256x256x{cfg.nz} (256^3 z-slab per GPU), K=8, "
-                                                f"{iters} iterations, halo exchange over NCCL"),
+                                                f"{iters} iterations, halo exchange: " +
+                                                ("fused CUDA-IPC peer stores" if ipc else "NCCL P2P, overlapped")),
                        "voxels_per_gpu": V, "labels": NL, "iterations_per_step": iters, "residual_check_every": 10,
                        "l2": "no flush: per-iteration state 4.9 GB/GPU >> 126 MB L2",
                        "kernel": {k: info[k] for k in ("tile_x", "tile_y", "z_chunk", "threads_per_cta", "ctas",
@@ -303,6 +306,9 @@ def main():
     ap.add_argument("--iters", type=int, default=0, help="override iterations per step (default: config's 300)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--transport", choices=["nccl", "ipc"], default="nccl",
+                    help="N > 1: halo exchange by NCCL P2P overlapped with the interior (default), or fused into "
+                         "the kernels as CUDA-IPC peer stores (pf_ipc_*)")
     args = ap.parse_args()
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)

@@ -103,6 +103,8 @@ typedef struct {
                           * north_star "optionally bf16-stored D_L"): the solver then
                           * solves the problem with data terms bf16(D_L) exactly, 2 B fewer per
                           * voxel-label-iteration.  0: fp32. */
+    int32_t ipc;         /* 1: allocate the state so that another process can map it (pf_ipc_export);
+                          * 0: stream-ordered pool allocations. */
     int32_t method;      /* PF_METHOD_PSEUDO_FLOW (default): Alg. 1 / 2 / 3.  PF_METHOD_EXPLICIT_ALM: the
                           * explicit-flow ("full-flow") augmented-Lagrangian solver of the Potts
                           * model Eq. 3 that stores p_S and p_L, the comparison arm of SURVEY 8(f2):
@@ -133,7 +135,8 @@ typedef struct {
 pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *const *D, const pf_smoothness *S,
                     const pf_config *cfg, const pf_slab *slab, pf_solver **out);
 
-/* Re-initialise u and q (row a0) keeping D and S resident. */
+/* Re-initialise u and q (row a0) keeping D and S resident.  IPC-linked slabs (pf_ipc_*): every rank
+ * resets, then a host barrier, before the next pf_ipc_step. */
 pf_status pf_reset(pf_solver *s);
 
 /* Run n iterations of the while-loop body of Alg. 1 / Alg. 2, one fused kernel
@@ -222,6 +225,28 @@ pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n);
 /* `iters` iterations of every linked slab; iteration t+1 of a slab is ordered (events, no host sync)
  * after iteration t of both neighbours.  residual: as pf_iterate, max over the slabs. */
 pf_status pf_iterate_linked(pf_solver *const *solvers, int32_t n, int32_t iters, float *residual);
+
+/* Fused halo exchange across PROCESSES (one process per GPU, torchrun): the same in-kernel peer
+ * stores as pf_link_slabs, with the neighbours' state buffers shared by CUDA IPC (NVLink peer memory)
+ * and one interprocess event per slab recorded after every iteration.
+ *   pf_ipc_export: the slab's buffers and event as a plain blob for the neighbours; records the event
+ *     once ("initial state in place").  Needs pf_config.ipc = 1 and a tile-storing kernel variant.
+ *   pf_ipc_link:   open the neighbours' blobs (NULL where there is none).
+ *   pf_ipc_step:   one iteration: wait on the neighbours' events, run the linked kernel, record.
+ * Protocol: export, exchange the blobs, link, host barrier; then per iteration pf_ipc_step followed
+ * by a host barrier over the ranks, so that every rank has RECORDED iteration t before any rank
+ * issues the wait of iteration t+1 (the GPU work itself stays asynchronous).  residual: as
+ * pf_iterate.  Errors: PF_ERR_STATE (no ipc config / not exported), PF_ERR_INVALID (blobs that are
+ * not this slab's neighbours at the same iteration), PF_ERR_UNSUPPORTED (kernel variant). */
+typedef struct {
+    uint8_t u[2][64], q[2][64], event[64];   /* cudaIpcMemHandle_t x 4, cudaIpcEventHandle_t */
+    int64_t nx, ny, nzl, z0, pitch;
+    int32_t NF, NL, tile_y, cluster, cur;
+} pf_ipc_slab;
+
+pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out);
+pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab *above);
+pf_status pf_ipc_step(pf_solver *s, float *residual);
 
 /* Static description of the kernel configuration (for reports). */
 typedef struct {

@@ -35,7 +35,7 @@ _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_C
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
 EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling",
-            "pf_link_slabs", "pf_iterate_linked", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
+            "pf_link_slabs", "pf_iterate_linked", "pf_ipc_export", "pf_ipc_link", "pf_ipc_step", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
@@ -57,7 +57,15 @@ class pf_smoothness(ctypes.Structure):
 
 class pf_config(ctypes.Structure):
     _fields_ = [("c", ctypes.c_float), ("tau", ctypes.c_float), ("cap", ctypes.c_int32), ("shift", ctypes.c_int32),
-                ("check_every", ctypes.c_int32), ("d_bf16", ctypes.c_int32), ("method", ctypes.c_int32)]
+                ("check_every", ctypes.c_int32), ("d_bf16", ctypes.c_int32), ("ipc", ctypes.c_int32),
+                ("method", ctypes.c_int32)]
+
+
+class pf_ipc_slab(ctypes.Structure):
+    _fields_ = [("u", (ctypes.c_uint8 * 64) * 2), ("q", (ctypes.c_uint8 * 64) * 2), ("event", ctypes.c_uint8 * 64),
+                ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nzl", ctypes.c_int64), ("z0", ctypes.c_int64),
+                ("pitch", ctypes.c_int64), ("NF", ctypes.c_int32), ("NL", ctypes.c_int32), ("tile_y", ctypes.c_int32),
+                ("cluster", ctypes.c_int32), ("cur", ctypes.c_int32)]
 
 
 class pf_slab(ctypes.Structure):
@@ -98,6 +106,9 @@ _sig = {
     "pf_halo_regions": (ctypes.c_int, [_vp, _P(pf_halo)]),
     "pf_exchange_local": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32]),
     "pf_link_slabs": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32]),
+    "pf_ipc_export": (ctypes.c_int, [_vp, _P(pf_ipc_slab)]),
+    "pf_ipc_link": (ctypes.c_int, [_vp, _P(pf_ipc_slab), _P(pf_ipc_slab)]),
+    "pf_ipc_step": (ctypes.c_int, [_vp, _P(ctypes.c_float)]),
     "pf_iterate_linked": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int32, _P(ctypes.c_float)]),
     "pf_get_kernel_info": (ctypes.c_int, [_vp, _P(pf_kernel_info)]),
     "pf_destroy": (None, [_vp]),
@@ -145,7 +156,7 @@ def pf_last_error() -> str:
 def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, weight, D: Sequence, s_kind: int, s_scalars=None,
               s_fields: Optional[Sequence] = None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2,
               shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None,
-              d_bf16: bool = False, method: int = 0) -> int:
+              d_bf16: bool = False, method: int = 0, ipc: bool = False) -> int:
     """pf_create.  dims = (nx, ny, nz) global.  D: one float32 volume per end label (node-id order)
     covering the slab plus the plane above it.  Returns the opaque solver handle."""
     nx, ny, nz = [int(v) for v in dims]
@@ -168,7 +179,7 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
         keep.append(fp)
     sm = pf_smoothness(s_kind, sc.ctypes.data_as(_P(ctypes.c_float)) if sc is not None else None,
                        ctypes.cast(fp, _P(ctypes.c_void_p)) if fp is not None else None)
-    cfg = pf_config(c, tau, cap, shift, check_every, 1 if d_bf16 else 0, int(method))
+    cfg = pf_config(c, tau, cap, shift, check_every, 1 if d_bf16 else 0, 1 if ipc else 0, int(method))
     sl = pf_slab(int(slab[0]), int(slab[1])) if slab is not None else None
     out = ctypes.c_void_p()
     _check(_lib.pf_create(ctypes.byref(d), ctypes.byref(g), ctypes.cast(Dp, _P(ctypes.c_void_p)), ctypes.byref(sm),
@@ -249,6 +260,25 @@ def pf_iterate_linked(solvers: Sequence[int], iters: int, want_residual: bool = 
     r = ctypes.c_float(-1.0)
     _check(_lib.pf_iterate_linked(ctypes.cast(arr, _P(ctypes.c_void_p)), len(solvers), int(iters),
                                   ctypes.byref(r) if want_residual else None))
+    return float(r.value) if want_residual else None
+
+
+def pf_ipc_export(s: int) -> bytes:
+    """The slab's IPC blob (pf_ipc_slab) as bytes, to be sent to the neighbouring ranks."""
+    out = pf_ipc_slab()
+    _check(_lib.pf_ipc_export(s, ctypes.byref(out)))
+    return bytes(out)
+
+
+def pf_ipc_link(s: int, below: Optional[bytes], above: Optional[bytes]):
+    b = pf_ipc_slab.from_buffer_copy(below) if below is not None else None
+    a = pf_ipc_slab.from_buffer_copy(above) if above is not None else None
+    _check(_lib.pf_ipc_link(s, ctypes.byref(b) if b is not None else None, ctypes.byref(a) if a is not None else None))
+
+
+def pf_ipc_step(s: int, want_residual: bool = False) -> Optional[float]:
+    r = ctypes.c_float(-1.0)
+    _check(_lib.pf_ipc_step(s, ctypes.byref(r) if want_residual else None))
     return float(r.value) if want_residual else None
 
 

@@ -230,8 +230,16 @@ struct pf_solver {
     unsigned long long *d_err = nullptr;   // [0] error voxel, [1], [2] work-item ticket counters
     int launch_parity = 0;                 // which ticket counter the next staged launch uses
     // fused halo exchange (pf_link_slabs): neighbours and tensor maps of their state buffers
-    pf_solver *nb_below = nullptr, *nb_above = nullptr;
+    pf_solver *nb_below = nullptr, *nb_above = nullptr;   // in-process links (pf_link_slabs)
+    bool link_below = false, link_above = false;           // in-process or IPC links
+    int nb_plane = 0;                                      // below neighbour's upper halo plane coordinate
     CUtensorMap tm_uo_nb[2], tm_qo_nb[2], tm_qz_nb[2];
+    // cross-process links (pf_ipc_*): state from cudaMalloc (IPC-exportable), an interprocess event
+    // recorded after every iteration, the neighbours' opened buffers and events
+    bool ipc = false;
+    cudaEvent_t ipc_ev = nullptr;
+    std::vector<void *> ipc_opened;
+    cudaEvent_t nb_ev[2] = {nullptr, nullptr};
     // CUDA graph of `graph_iters` whole iterations (pf_iterate), replayed when the state matches the
     // capture: same ping-pong buffer, same counter parity, check iterations at the same positions
     cudaGraphExec_t graph = nullptr;
@@ -301,6 +309,19 @@ void free_all(pf_solver *s) {
         cudaGraphExecDestroy(s->graph);
         s->graph = nullptr;
     }
+    for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
+    s->ipc_opened.clear();
+    for (int i = 0; i < 2; ++i)
+        if (s->nb_ev[i]) { cudaEventDestroy(s->nb_ev[i]); s->nb_ev[i] = nullptr; }
+    if (s->ipc_ev) { cudaEventDestroy(s->ipc_ev); s->ipc_ev = nullptr; }
+    if (s->ipc) {   // cudaMalloc'd state (exportable); synchronise before the synchronous frees
+        cudaStreamSynchronize(s->stream);
+        for (int i = 0; i < 2; ++i) {
+            if (s->u_alloc[i]) cudaFree(s->u_alloc[i]);
+            if (s->q_alloc[i]) cudaFree(s->q_alloc[i]);
+            s->u_alloc[i] = s->q_alloc[i] = nullptr;
+        }
+    }
     void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc, s->D16,
                     s->p_alloc, s->pS_alloc, s->uint_alloc,
                     s->d_resid, s->d_err, s->d_flag, s->d_energy};
@@ -317,8 +338,10 @@ void free_all(pf_solver *s) {
     s->d_energy = nullptr;
 }
 
-pf_status alloc(pf_solver *s, void **p, size_t bytes, const char *what) {
-    cudaError_t e = cudaMallocAsync(p, bytes, s->stream);
+// ipc: a plain cudaMalloc allocation (pool allocations cannot be exported with cudaIpcGetMemHandle);
+// free_all releases those with cudaFree (s->ipc)
+pf_status alloc(pf_solver *s, void **p, size_t bytes, const char *what, bool ipc = false) {
+    cudaError_t e = ipc ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, s->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(PF_ERR_OOM, "cudaMallocAsync(%zu bytes) for %s failed: %s", bytes, what, cudaGetErrorString(e));
@@ -590,8 +613,10 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         return fail(PF_ERR_UNSUPPORTED, "explicit-flow ALM: Potts / HMF / DAG graphs (<= 16 non-source nodes), whole "
                                         "volumes, scalar, shared or per-node capacities only");
 
+    if (cfg->ipc && alm) return fail(PF_ERR_UNSUPPORTED, "config: ipc is for the pseudo-flow kernels");
     pf_solver *s = new pf_solver();
     s->alm = alm;
+    s->ipc = cfg->ipc != 0;
     cudaGetDevice(&s->device);
     s->ndim = dims->ndim;
     s->nx = dims->nx;
@@ -657,10 +682,12 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     for (int i = 0; i < 2; ++i) {
         if (alm && i == 1) {
             s->u_alloc[1] = nullptr;
-        } else if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u")) != PF_OK) {
+        } else if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u", cfg->ipc))
+                   != PF_OK) {
             return bail(st);
         }
-        if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * 3 * NF * P) * sizeof(float), "q")) != PF_OK)
+        if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * 3 * NF * P) * sizeof(float), "q", cfg->ipc))
+            != PF_OK)
             return bail(st);
         s->u[i] = (alm ? s->u_alloc[0] : s->u_alloc[i]) + NL * P;
         s->q[i] = s->q_alloc[i] + (int64_t)3 * NF * P;
@@ -791,7 +818,13 @@ pf_status pf_reset(pf_solver *s) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
     DeviceGuard dg(s->device);
-    return init_state(s);
+    // IPC-linked: the neighbours' last kernels (which write into this slab's halo planes) must be done
+    // before the re-init, and their next kernels must start after it
+    for (int i = 0; i < 2; ++i)
+        if (s->nb_ev[i]) CK(cudaStreamWaitEvent(s->stream, s->nb_ev[i], 0), "wait neighbour");
+    if ((st = init_state(s)) != PF_OK) return st;
+    if (s->ipc_ev) CK(cudaEventRecord(s->ipc_ev, s->stream), "record");
+    return PF_OK;
 }
 
 pf_status pf_set_stream(pf_solver *s, void *stream) {
@@ -850,13 +883,13 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
         sa.u_out = s->u[1 - s->cur];
         sa.q_out = s->q[1 - s->cur];
         sa.check = check;
-        if (s->nb_below) {
+        if (s->link_below) {
             sa.link_below = 1;
             sa.tm_uo_nb = s->tm_uo_nb[1 - s->cur];
             sa.tm_qo_nb = s->tm_qo_nb[1 - s->cur];
-            sa.nb_plane = (int)s->nb_below->nzl + 1;
+            sa.nb_plane = s->nb_plane;
         }
-        if (s->nb_above) {
+        if (s->link_above) {
             sa.link_above = 1;
             sa.tm_qz_nb = s->tm_qz_nb[1 - s->cur];
         }
@@ -1005,7 +1038,7 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
     if (n < 0) return fail(PF_ERR_INVALID, "n must be >= 0");
-    if (s->nb_below || s->nb_above) return fail(PF_ERR_STATE, "linked slab: iterate with pf_iterate_linked");
+    if (s->link_below || s->link_above) return fail(PF_ERR_STATE, "linked slab: iterate with pf_iterate_linked / pf_ipc_step");
     if (s->phase_pending) return fail(PF_ERR_STATE, "pf_iterate: an iteration split by pf_iterate_phase is open");
     DeviceGuard dg(s->device);
     bool any_check = false;
@@ -1056,7 +1089,7 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual) {
     if (st != PF_OK) return st;
     if (phase != 0 && phase != 1) return fail(PF_ERR_INVALID, "phase must be 0 or 1");
     if (s->alm) return fail(PF_ERR_UNSUPPORTED, "pf_iterate_phase: not for the explicit-flow ALM");
-    if (s->nb_below || s->nb_above) return fail(PF_ERR_STATE, "linked slab: iterate with pf_iterate_linked");
+    if (s->link_below || s->link_above) return fail(PF_ERR_STATE, "linked slab: iterate with pf_iterate_linked / pf_ipc_step");
     if ((phase == 0) == (s->phase_pending != 0))
         return fail(PF_ERR_STATE, phase == 0 ? "phase 0 issued twice" : "phase 1 without phase 0");
     DeviceGuard dg(s->device);
@@ -1322,6 +1355,9 @@ pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n) {
         bool ok = true;
         s->nb_below = i > 0 ? solvers[i - 1] : nullptr;
         s->nb_above = i + 1 < n ? solvers[i + 1] : nullptr;
+        s->link_below = s->nb_below != nullptr;
+        s->link_above = s->nb_above != nullptr;
+        if (s->nb_below) s->nb_plane = (int)s->nb_below->nzl + 1;
         for (int b = 0; b < 2; ++b) {
             if (s->nb_below) {   // below neighbour's buffers: its upper halo plane receives our plane 0
                 const pf_solver *t = s->nb_below;
@@ -1414,6 +1450,100 @@ pf_status pf_iterate_linked(pf_solver *const *solvers, int32_t n, int32_t iters,
         for (int i = 0; i < n; ++i) cudaEventDestroy(ev[e][i]);
     if (residual) *residual = r;
     return st;
+}
+
+pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (!out) return fail(PF_ERR_INVALID, "out is NULL");
+    if (!s->ipc) return fail(PF_ERR_STATE, "ipc_export: create the solver with pf_config.ipc = 1");
+    if (!s->staged || !(s->cluster || s->sinfo.ostage == 1))
+        return fail(PF_ERR_UNSUPPORTED, "ipc_export: this kernel variant stores no whole tiles");
+    DeviceGuard dg(s->device);
+    memset(out, 0, sizeof(*out));
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)out->u[i], s->u_alloc[i]), "ipc handle u");
+        CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)out->q[i], s->q_alloc[i]), "ipc handle q");
+    }
+    if (!s->ipc_ev) CK(cudaEventCreateWithFlags(&s->ipc_ev, cudaEventDisableTiming | cudaEventInterprocess), "ipc event");
+    CK(cudaIpcGetEventHandle((cudaIpcEventHandle_t *)out->event, s->ipc_ev), "ipc event handle");
+    CK(cudaEventRecord(s->ipc_ev, s->stream), "record");   // "my initial state is in place"
+    out->nx = s->nx;
+    out->ny = s->ny;
+    out->nzl = s->nzl;
+    out->z0 = s->z0;
+    out->pitch = s->pitch;
+    out->NF = s->gc.NF;
+    out->NL = s->gc.NL;
+    out->tile_y = s->sinfo.tile_y;
+    out->cluster = s->cluster ? 1 : 0;
+    out->cur = s->cur;
+    return PF_OK;
+}
+
+pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab *above) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (!s->ipc || !s->ipc_ev) return fail(PF_ERR_STATE, "ipc_link: export first (pf_ipc_export)");
+    DeviceGuard dg(s->device);
+    const int ty = s->sinfo.tile_y, NF = s->gc.NF, NL = s->gc.NL;
+    const int cq = s->cluster ? NL / 2 : 3 * NF, cl = s->cluster ? NL / 2 : NL, cz = s->cluster ? NL / 2 : NF;
+    const pf_ipc_slab *nb[2] = {below, above};
+    for (int side = 0; side < 2; ++side) {
+        const pf_ipc_slab *t = nb[side];
+        if (!t) continue;
+        const bool adjacent = side == 0 ? t->z0 + t->nzl == s->z0 : t->z0 == s->z1;
+        if (!adjacent || t->nx != s->nx || t->ny != s->ny || t->pitch != s->pitch || t->NF != NF || t->NL != NL ||
+            t->tile_y != ty || t->cluster != (s->cluster ? 1 : 0) || t->cur != s->cur)
+            return fail(PF_ERR_INVALID, "ipc_link: the %s blob is not this slab's neighbour in step",
+                        side == 0 ? "below" : "above");
+        void *ub[2] = {nullptr, nullptr}, *qb[2] = {nullptr, nullptr};
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaIpcOpenMemHandle(&ub[b], *(const cudaIpcMemHandle_t *)t->u[b], cudaIpcMemLazyEnablePeerAccess),
+               "open ipc u");
+            s->ipc_opened.push_back(ub[b]);
+            CK(cudaIpcOpenMemHandle(&qb[b], *(const cudaIpcMemHandle_t *)t->q[b], cudaIpcMemLazyEnablePeerAccess),
+               "open ipc q");
+            s->ipc_opened.push_back(qb[b]);
+        }
+        CK(cudaIpcOpenEventHandle(&s->nb_ev[side], *(const cudaIpcEventHandle_t *)t->event), "open ipc event");
+        bool ok = true;
+        for (int b = 0; b < 2; ++b) {
+            if (side == 0) {   // below: its upper halo plane receives our plane 0
+                ok = ok && encode4d(&s->tm_uo_nb[b], ub[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl);
+                ok = ok && encode4d(&s->tm_qo_nb[b], qb[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2, 32,
+                                    ty, cq);
+            } else {           // above: its lower halo plane receives our last q^z
+                ok = ok && encode4d(&s->tm_qz_nb[b], qb[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2, 32,
+                                    ty, cz);
+            }
+        }
+        if (!ok) return fail(PF_ERR_CUDA, "ipc_link: cuTensorMapEncodeTiled failed");
+        if (side == 0) {
+            s->link_below = true;
+            s->nb_plane = (int)t->nzl + 1;
+        } else {
+            s->link_above = true;
+        }
+    }
+    return PF_OK;
+}
+
+pf_status pf_ipc_step(pf_solver *s, float *residual) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (!s->ipc || !s->ipc_ev) return fail(PF_ERR_STATE, "ipc_step: export and link first");
+    DeviceGuard dg(s->device);
+    // the neighbours' latest recorded iteration (the caller's host barrier makes it the previous one)
+    for (int i = 0; i < 2; ++i)
+        if (s->nb_ev[i]) CK(cudaStreamWaitEvent(s->stream, s->nb_ev[i], 0), "wait neighbour");
+    const int check = check_this_iteration(s);
+    if (check) CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
+    if ((st = launch_items(s, 0, s->items, check)) != PF_OK) return st;
+    CK(cudaEventRecord(s->ipc_ev, s->stream), "record");
+    s->cur = 1 - s->cur;
+    s->iters += 1;
+    return read_residual(s, check != 0, residual);
 }
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {

@@ -11,6 +11,11 @@ solver's stream S; the exchange is posted on a communication stream C that waits
 recorded between the two phases, so NCCL moves the boundary planes while phase 1 computes the
 interior.  S waits for the exchange before the next phase 0 (which reads the received halos).
 The received planes land in halo planes of the new state that phase 1 neither reads nor writes.
+
+transport="ipc" (solvers created with ipc=True): no exchange step at all -- the iteration kernels store
+their boundary planes straight into the neighbours' halo planes through CUDA-IPC-mapped peer memory
+(pf_ipc_*), ordered by interprocess events; a host barrier per iteration only orders the event records
+and waits of the ranks (the GPU work stays queued).
 """
 from __future__ import annotations
 
@@ -19,6 +24,7 @@ from typing import Dict, Optional
 import torch
 import torch.distributed as dist
 
+from . import pf_ipc_export, pf_ipc_link, pf_ipc_step
 from .solver import Solver, slab_bounds
 
 
@@ -61,8 +67,10 @@ def halo_exchange(regions: Dict[str, Optional[torch.Tensor]], rank: int, world: 
 class DistSolver:
     """The rank's slab solver plus its halo exchange.  `make_solver(slab)` builds the Solver."""
 
-    def __init__(self, make_solver, nz: int, rank: int, world: int, device: torch.device, group=None):
+    def __init__(self, make_solver, nz: int, rank: int, world: int, device: torch.device, group=None,
+                 transport: str = "nccl"):
         self.rank, self.world, self.group = rank, world, group
+        self.transport = transport
         self.device = device
         self.bounds = slab_bounds(nz, world)
         assert len(self.bounds) == world, "every rank needs at least one plane"
@@ -71,6 +79,16 @@ class DistSolver:
         self.cuda = torch.device(device).type == "cuda"
         if self.cuda:
             self.solver.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        self.host_group = group
+        if transport == "ipc" and world > 1:
+            # per-iteration ordering barrier on the host only (a NCCL barrier would block on the GPU work)
+            if dist.get_backend(group) != "gloo":
+                self.host_group = dist.new_group(backend="gloo")
+            blobs = [None] * world
+            dist.all_gather_object(blobs, pf_ipc_export(self.solver.h), group=group)
+            pf_ipc_link(self.solver.h, blobs[rank - 1] if rank > 0 else None,
+                        blobs[rank + 1] if rank < world - 1 else None)
+            dist.barrier(group=self.host_group)   # every rank has recorded "initial state in place"
 
     def _regions(self):
         h = self.solver.halo()
@@ -84,18 +102,34 @@ class DistSolver:
             "recv_down_qz": device_view(h.recv_down_qz, h.bytes_qz, dv) if h.recv_down_qz else None,
         }
 
+    def _last_check_index(self, n: int):
+        """Index t in [0, n) of the last check iteration of this call (pf_iterate's residual), or None."""
+        k = getattr(self.solver, "check_every", 0)
+        if k <= 0:
+            return None
+        it0 = self.solver.iterations()
+        t = n - 1 - ((it0 + n) % k)
+        return t if t >= 0 else None
+
     def iterate(self, n: int, residual: bool = False, overlap: bool = True):
-        """n iterations with the halo exchange after each; residual=True: max over ranks of the last
-        iteration's residual (-1 if it was not a check iteration)."""
+        """n iterations with the halo exchange after each.  residual=True: as pf_iterate -- the residual of
+        the last check iteration of this call, max over ranks (-1 if there was none)."""
         if self.world == 1:
             return self.solver.iterate(n, residual)
+        want = self._last_check_index(n) if residual else None
+        r = -1.0 if residual else None
+        if self.transport == "ipc":
+            for t in range(n):
+                val = pf_ipc_step(self.solver.h, t == want)
+                dist.barrier(group=self.host_group)   # all ranks recorded iteration t before any waits on it
+                if t == want:
+                    r = self._max_over_ranks(val)
+            return r
         overlap = overlap and self.cuda
-        r = None
         S = torch.cuda.current_stream(self.device) if self.cuda else None
         C = self._comm_stream() if overlap else None
         works = []
         for t in range(n):
-            last = residual and t == n - 1
             for w in works:      # S waits for the previous exchange (the halos phase 0 reads)
                 w.wait()
             works = []
@@ -103,20 +137,26 @@ class DistSolver:
                 self.solver.iterate_phase(0)
                 ev = torch.cuda.Event()
                 ev.record(S)
-                val = self.solver.iterate_phase(1, last)
+                val = self.solver.iterate_phase(1, t == want)
                 C.wait_event(ev)
                 with torch.cuda.stream(C):
                     works = halo_exchange(self._regions(), self.rank, self.world, self.group, wait=False)
             else:
-                val = self.solver.iterate(1, last)
+                val = self.solver.iterate(1, t == want)
                 halo_exchange(self._regions(), self.rank, self.world, self.group)
-            if last:
-                rt = torch.tensor([val], dtype=torch.float64, device=self.device)
-                dist.all_reduce(rt, op=dist.ReduceOp.MAX, group=self.group)
-                r = float(rt.item())
+            if t == want:
+                r = self._max_over_ranks(val)
         for w in works:
             w.wait()
         return r
+
+    def _reduce_device(self):
+        return self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+
+    def _max_over_ranks(self, val: float) -> float:
+        rt = torch.tensor([val], dtype=torch.float64, device=self._reduce_device())
+        dist.all_reduce(rt, op=dist.ReduceOp.MAX, group=self.group)
+        return float(rt.item())
 
     def run(self, max_iters: int, tol: float):
         """"while not converged" across the slabs: iterate until the residual of a check iteration, max
@@ -142,7 +182,7 @@ class DistSolver:
         e, f = self.solver.energy()
         if self.world == 1:
             return e, f
-        t = torch.tensor([e, f], dtype=torch.float64, device=self.device)
+        t = torch.tensor([e, f], dtype=torch.float64, device=self._reduce_device())
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return float(t[0]), float(t[1])
 
@@ -153,6 +193,11 @@ class DistSolver:
 
     def reset(self):
         self.solver.reset()
+        if self.transport == "ipc" and self.world > 1:
+            dist.barrier(group=self.host_group)   # every rank's re-init is recorded before iterating
 
     def close(self):
+        if self.transport == "ipc" and self.world > 1:   # no neighbour kernel may still write into our buffers
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.host_group)
         self.solver.close()
