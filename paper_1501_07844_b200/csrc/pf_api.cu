@@ -1,28 +1,13 @@
-// pf_api.cu -- the C-ABI of include/pf.h: graph compilation (row a10), device state
-// and layouts, the per-iteration launch loop (rows a0-a8), labeling (a9), halo
-// regions for z-slab decomposition (row e).
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdarg>
-#include <cstdio>
-#include <cstring>
-#include <string>
-#include <vector>
-
-#include <cuda.h>
-
-#include "pf.h"
-#include "pf_alm.cuh"
-#include "pf_aux.cuh"
-#include "pf_kernels.cuh"
-#include "pf_staged.cuh"
-#include "pf_cluster.cuh"
+// pf_api.cu -- the C-ABI of include/pf.h: device state and layouts, the per-iteration launch loop
+// (rows a0-a8, CUDA-graph replay, convergence stop, split iterations), labeling (a9), energies.
+// Graph compilation (a10) is in pf_graph.cu, the z-slab entry points (row e) in pf_slabs.cu.
+#include "pf_internal.h"
 
 using namespace pf;
+using namespace pfi;
 
-namespace {
+namespace pfi {
+
 
 thread_local std::string g_last_error;
 
@@ -36,18 +21,7 @@ pf_status fail(pf_status st, const char *fmt, ...) {
     return st;
 }
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
+
 
 bool is_device_ptr(const void *p) {
     cudaPointerAttributes at;
@@ -58,218 +32,6 @@ bool is_device_ptr(const void *p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-// --------------------------------------------------------------------------
-// Label-graph compilation (reading R9)
-// --------------------------------------------------------------------------
-struct Compiled {
-    int num_nodes = 0, NI = 0, NL = 0, NV = 0;
-    bool chain = false;  // Ishikawa chain shape (see pf.h); model 1 also needs zero end-label capacities
-    int model = 0;       // 0: Alg. 1/2, 1: Alg. 3 (Ishikawa chain)
-    int NF = 0;          // flow-carrying nodes (positions 0..NF-1)
-    std::vector<int> pos_of_node;  // node id -> position, S -> -1
-    std::vector<int> node_of_pos;
-    GraphConst g;
-    std::vector<std::vector<float>> W;  // W[pos][leaf slot] path weights
-    std::vector<float> w_src;           // weight of the edge S -> position (0: none)
-};
-
-pf_status compile_graph(const pf_graph *gr, Compiled *out) {
-    if (!gr || gr->num_nodes < 3 || gr->num_edges < 2 || !gr->parent || !gr->child || !gr->weight)
-        return fail(PF_ERR_GRAPH, "graph: need >= 3 nodes (S + 2 end labels), >= 2 edges and non-NULL arrays");
-    const int n = gr->num_nodes, ne = gr->num_edges;
-    std::string errs;
-    auto add = [&](const std::string &s) { errs += (errs.empty() ? "" : "; ") + s; };
-    std::vector<std::vector<std::pair<int, float>>> kids(n), pars(n);
-    bool idx_ok = true;
-    for (int e = 0; e < ne; ++e) {
-        const int p = gr->parent[e], c = gr->child[e];
-        const float w = gr->weight[e];
-        if (p < 0 || p >= n || c < 0 || c >= n) {
-            add("edge " + std::to_string(e) + " has a node id out of range");
-            idx_ok = false;
-            continue;
-        }
-        if (!(w > 0.f) || !std::isfinite(w)) add("edge " + std::to_string(e) + " weight must be > 0");
-        if (p == c) add("self-loop at node " + std::to_string(p));
-        kids[p].push_back({c, w});
-        pars[c].push_back({p, w});
-    }
-    if (!idx_ok) return fail(PF_ERR_GRAPH, "graph: %s", errs.c_str());
-    if (!pars[0].empty()) add("source S (node 0) has parents");
-    // Kahn with lowest-id tie-break
-    std::vector<int> indeg(n, 0), order;
-    for (int v = 0; v < n; ++v) indeg[v] = (int)pars[v].size();
-    std::vector<bool> placed(n, false);
-    for (int k = 0; k < n; ++k) {
-        int pick = -1;
-        for (int v = 0; v < n; ++v)
-            if (!placed[v] && indeg[v] == 0) { pick = v; break; }
-        if (pick < 0) break;
-        placed[pick] = true;
-        order.push_back(pick);
-        for (auto &c : kids[pick]) indeg[c.first]--;
-    }
-    if ((int)order.size() != n) add("graph has a cycle");
-    // reachability from S
-    std::vector<bool> reach(n, false);
-    std::vector<int> stack{0};
-    reach[0] = true;
-    while (!stack.empty()) {
-        int v = stack.back();
-        stack.pop_back();
-        for (auto &c : kids[v])
-            if (!reach[c.first]) { reach[c.first] = true; stack.push_back(c.first); }
-    }
-    for (int v = 1; v < n; ++v)
-        if (!reach[v]) add("node " + std::to_string(v) + " unreachable from S");
-    std::vector<int> leaves, internals;
-    for (int v = 1; v < n; ++v) (kids[v].empty() ? leaves : internals).push_back(v);
-    if (leaves.size() < 2) add("fewer than 2 end labels");
-    if (!errs.empty()) return fail(PF_ERR_GRAPH, "graph: %s", errs.c_str());
-    // W_(v, B) by memoised recursion in reverse topological order
-    const int NL = (int)leaves.size();
-    std::vector<std::vector<double>> Wd(n, std::vector<double>(NL, 0.0));
-    for (int k = n - 1; k >= 0; --k) {
-        const int v = order[k];
-        if (kids[v].empty() && v != 0) {
-            Wd[v][std::find(leaves.begin(), leaves.end(), v) - leaves.begin()] = 1.0;
-        } else {
-            for (auto &c : kids[v])
-                for (int l = 0; l < NL; ++l) Wd[v][l] += (double)c.second * Wd[c.first][l];
-        }
-    }
-    for (int l = 0; l < NL; ++l)
-        if (std::fabs(Wd[0][l] - 1.0) > 1e-6)
-            add("W_(S," + std::to_string(leaves[l]) + ") = " + std::to_string(Wd[0][l]) +
-                " != 1 (sum of end labels must equal u_S = 1, reading R9)");
-    if (!errs.empty()) return fail(PF_ERR_GRAPH, "graph: %s", errs.c_str());
-    const int NI = (int)internals.size();
-    // Ishikawa chain: internals in topological order N_1..N_N, S -> {N_1, L_0}, N_i -> {N_{i+1}, L_i},
-    // N_N -> L_N, all weights 1, end labels in increasing id order L_0..L_N
-    bool chain = NL == NI + 1 && NI >= 1 && kids[0].size() == 2;
-    std::vector<int> lev;
-    for (int k = 0; k < n && chain; ++k)
-        if (order[k] != 0 && !kids[order[k]].empty()) lev.push_back(order[k]);
-    auto has_edge = [&](int p, int c) {
-        for (auto &e : kids[p])
-            if (e.first == c && e.second == 1.f) return true;
-        return false;
-    };
-    if (chain) {
-        chain = (int)lev.size() == NI && has_edge(0, lev[0]) && has_edge(0, leaves[0]);
-        for (int i = 0; i < NI && chain; ++i) {
-            const bool last = i == NI - 1;
-            chain = kids[lev[i]].size() == (last ? 1u : 2u) && has_edge(lev[i], leaves[i + 1]) &&
-                    (last || has_edge(lev[i], lev[i + 1]));
-        }
-    }
-    if (!chain && (NI > kMaxInternal || NI + NL > kMaxNodes))
-        return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes exceeds the compiled kernel set "
-                                        "(<= %d internal, <= %d non-source nodes)", NI, NL, kMaxInternal, kMaxNodes);
-    if (chain && NL > kMaxNodes)
-        return fail(PF_ERR_UNSUPPORTED, "graph: Ishikawa chain with %d labels exceeds %d", NL, kMaxNodes);
-    out->chain = chain;
-    out->num_nodes = n;
-    out->NI = NI;
-    out->NL = NL;
-    out->NV = NI + NL;
-    out->pos_of_node.assign(n, -1);
-    out->node_of_pos.clear();
-    for (int k = 0; k < n; ++k) {  // internal nodes in topological order
-        const int v = order[k];
-        if (v != 0 && !kids[v].empty()) {
-            out->pos_of_node[v] = (int)out->node_of_pos.size();
-            out->node_of_pos.push_back(v);
-        }
-    }
-    for (int v : leaves) {  // end labels in node-id order
-        out->pos_of_node[v] = (int)out->node_of_pos.size();
-        out->node_of_pos.push_back(v);
-    }
-    memset(&out->g, 0, sizeof(out->g));
-    for (int v = 1; v < n && NI <= kMaxInternal; ++v) {  // dense weights (unused by the chain kernels)
-        if (kids[v].empty()) continue;
-        const int i = out->pos_of_node[v];
-        for (auto &c : kids[v]) out->g.w[i][out->pos_of_node[c.first]] += c.second;
-    }
-    out->w_src.assign(out->NV, 0.f);
-    for (auto &c : kids[0]) out->w_src[out->pos_of_node[c.first]] += c.second;
-    out->W.assign(out->NV, std::vector<float>(NL, 0.f));  // W_(v, B), for reports
-    for (int p = 0; p < out->NV; ++p)
-        for (int l = 0; l < NL; ++l) out->W[p][l] = (float)Wd[out->node_of_pos[p]][l];
-    return PF_OK;
-}
-
-}  // namespace
-
-struct pf_solver {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    bool poisoned = false;
-    int ndim = 3;
-    int64_t nx = 0, ny = 0, nz = 0;
-    int64_t z0 = 0, z1 = 0, nzl = 0;
-    int64_t P = 0;       // channel-plane stride = pitch * ny
-    int64_t pitch = 0;   // row pitch (elements), multiple of 4 for TMA
-    Compiled gc;
-    pf_config cfg{};
-    int s_kind = 0;
-    // allocations (base pointers) and plane-0 pointers
-    float *u_alloc[2] = {nullptr, nullptr}, *q_alloc[2] = {nullptr, nullptr};
-    float *D_alloc = nullptr, *S_alloc = nullptr;   // D_alloc: fp32 D (nullptr when D is stored as bf16)
-    uint16_t *D16 = nullptr;                          // bf16 D (cfg.d_bf16), same [z][l][y][pitch] layout
-    bool alm = false;                                 // PF_METHOD_EXPLICIT_ALM (pf_alm.cu)
-    float *p_alloc = nullptr, *pS_alloc = nullptr;    // ALM sink flows [z][l][y][pitch], source flow [z][y][pitch]
-    float *uint_alloc = nullptr;                      // ALM on a DAG: u of the internal nodes [z][NI][y][pitch]
-    const void *Dptr() const { return D16 ? (const void *)D16 : (const void *)D_alloc; }
-    float *u[2] = {nullptr, nullptr}, *q[2] = {nullptr, nullptr};
-    int cur = 0;
-    int64_t iters = 0;
-    unsigned int *d_resid = nullptr;
-    unsigned long long *d_err = nullptr;   // [0] error voxel, [1], [2] work-item ticket counters
-    int launch_parity = 0;                 // which ticket counter the next staged launch uses
-    // fused halo exchange (pf_link_slabs): neighbours and tensor maps of their state buffers
-    pf_solver *nb_below = nullptr, *nb_above = nullptr;   // in-process links (pf_link_slabs)
-    bool link_below = false, link_above = false;           // in-process or IPC links
-    int nb_plane = 0;                                      // below neighbour's upper halo plane coordinate
-    CUtensorMap tm_uo_nb[2], tm_qo_nb[2], tm_qz_nb[2];
-    // cross-process links (pf_ipc_*): state from cudaMalloc (IPC-exportable), an interprocess event
-    // recorded after every iteration, the neighbours' opened buffers and events
-    bool ipc = false;
-    cudaEvent_t ipc_ev = nullptr;
-    std::vector<void *> ipc_opened;
-    cudaEvent_t nb_ev[2] = {nullptr, nullptr};
-    // CUDA graph of `graph_iters` whole iterations (pf_iterate), replayed when the state matches the
-    // capture: same ping-pong buffer, same counter parity, check iterations at the same positions
-    cudaGraphExec_t graph = nullptr;
-    int graph_iters = 0, graph_cur = 0, graph_parity = 0;
-    bool graph_failed = false;
-    unsigned int *d_flag = nullptr;
-    double *d_energy = nullptr;  // partials + result
-    IterKernelInfo kinfo{};
-    int zchunk = 0;
-    dim3 grid;
-    int ctas_per_sm = 0;
-    int regs = 0;
-    int64_t device_bytes = 0;
-    bool last_resid_valid = false;
-    int64_t launches = 0;
-    // TMA-staged persistent kernel (default) -- see pf_staged.cuh
-    bool staged = false;
-    bool cluster = false;   // staged work split over a 2-CTA cluster (pf_cluster.cuh; Potts, many labels)
-    StagedKernelInfo sinfo{};
-    CUtensorMap tm_q[2], tm_u[2], tm_D, tm_S, tm_qo[2], tm_uo[2];
-    int staged_smem = 0;
-    int s_ch = 0;
-    int tiles_x = 0, tiles = 0, items = 0, sgrid = 0;
-    // boundary / interior split of the z-chunks (slabs with neighbours; pf_iterate_phase)
-    int nb = 0, bplane[2] = {0, 0}, zlo = 0, zhi = 0, items_b = 0;
-    int phase_pending = 0;  // 1 after pf_iterate_phase(0) until its phase 1
-    unsigned int tx_bytes = 0;
-};
-
-namespace {
 
 pf_status cuda_fail(pf_solver *s, cudaError_t e, const char *what) {
     if (s) s->poisoned = true;
@@ -277,15 +39,9 @@ pf_status cuda_fail(pf_solver *s, cudaError_t e, const char *what) {
     return fail(PF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-#define CK(expr, what)                                     \
-    do {                                                   \
-        cudaError_t e__ = (expr);                          \
-        if (e__ != cudaSuccess) return cuda_fail(s, e__, what); \
-    } while (0)
 
-int64_t ups(const pf_solver *s) { return (int64_t)s->gc.NL * s->P; }
-// q always carries 3 components internally (q^z == 0 for 2-D volumes), so the kernels need no ndim branch
-int64_t qps(const pf_solver *s) { return (int64_t)3 * s->gc.NF * s->P; }
+
+
 
 // Device memory comes from the device's stream-ordered pool, which keeps up to kPoolKeep bytes of freed
 // memory for reuse: a solver created right after another one was destroyed (the end-to-end
@@ -492,7 +248,7 @@ EncodeTiledFn encode_fn() {
 // 4-D fp32 tensor map over an internal array [plane][channel][y][pitch] (x fastest); elements with
 // x >= nx, y outside [0, ny) or plane outside [0, nplanes) read as 0 (TMA out-of-bounds fill).
 bool encode4d(CUtensorMap *m, const void *base, int64_t nx, int64_t ny, int64_t pitch, int64_t nch, int64_t nplanes,
-              int bx, int by, int bc, bool bf16 = false) {
+              int bx, int by, int bc, bool bf16) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     const int64_t es_b = bf16 ? 2 : 4;
@@ -548,7 +304,7 @@ cudaError_t copy_volume(bool to_internal, float *internal_c, int64_t nch, float 
     return cudaMemcpy3DAsync(&p, st);
 }
 
-}  // namespace
+}  // namespace pfi
 
 extern "C" {
 
@@ -840,7 +596,9 @@ pf_status pf_set_stream(pf_solver *s, void *stream) {
     return PF_OK;
 }
 
-namespace {
+}  // extern "C"
+
+namespace pfi {
 
 // Launch items [ib, ie) of one iteration reading state `cur` (no swap).  ie == ib launches nothing.
 pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
@@ -1032,7 +790,9 @@ pf_status capture_graph(pf_solver *s) {
     return PF_OK;
 }
 
-}  // namespace
+}  // namespace pfi
+
+extern "C" {
 
 pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     pf_status st = check_usable(s);
@@ -1229,321 +989,6 @@ pf_status pf_iterations(const pf_solver *s, int64_t *done) {
     if (!s || !done) return fail(PF_ERR_INVALID, "NULL argument");
     *done = s->iters;
     return PF_OK;
-}
-
-pf_status pf_halo_regions(pf_solver *s, pf_halo *h) {
-    pf_status st = check_usable(s);
-    if (st != PF_OK) return st;
-    if (!h) return fail(PF_ERR_INVALID, "h is NULL");
-    memset(h, 0, sizeof(*h));
-    const int NV = s->gc.NF;  // flow-carrying nodes
-    const int64_t P = s->P, nzl = s->nzl;
-    float *u = s->u[s->cur], *q = s->q[s->cur];
-    h->bytes_u = ups(s) * (int64_t)sizeof(float);
-    h->bytes_q = qps(s) * (int64_t)sizeof(float);
-    h->bytes_qz = s->ndim == 3 ? (int64_t)NV * P * (int64_t)sizeof(float) : 0;
-    if (s->z0 > 0) {  // neighbour below exists
-        h->send_down_u = u;
-        h->send_down_q = q;
-        if (s->ndim == 3) h->recv_down_qz = q - qps(s) + 2 * NV * P;
-    }
-    if (s->z1 < s->nz) {  // neighbour above exists
-        h->recv_up_u = u + nzl * ups(s);
-        h->recv_up_q = q + nzl * qps(s);
-        if (s->ndim == 3) h->send_up_qz = q + (nzl - 1) * qps(s) + 2 * NV * P;
-    }
-    return PF_OK;
-}
-
-pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n) {
-    if (!solvers || n < 1) return fail(PF_ERR_INVALID, "need >= 1 solver");
-    for (int i = 0; i < n; ++i) {
-        pf_status st = check_usable(solvers[i]);
-        if (st != PF_OK) return st;
-    }
-    for (int i = 0; i + 1 < n; ++i) {
-        pf_solver *lo = solvers[i], *hi = solvers[i + 1];
-        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->gc.NF != hi->gc.NF)
-            return fail(PF_ERR_INVALID, "exchange: solvers %d and %d are not consecutive slabs of one volume", i, i + 1);
-    }
-    // order: every receiver waits for every sender's pending work, copies on the receiver's stream,
-    // then every sender waits for the copies that read its current state.
-    std::vector<cudaEvent_t> ev(n);
-    for (int i = 0; i < n; ++i) {
-        pf_solver *s = solvers[i];
-        DeviceGuard dg(s->device);
-        CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event");
-        CK(cudaEventRecord(ev[i], s->stream), "record");
-    }
-    for (int i = 0; i < n; ++i) {
-        pf_solver *s = solvers[i];
-        DeviceGuard dg(s->device);
-        if (i > 0) CK(cudaStreamWaitEvent(s->stream, ev[i - 1], 0), "wait");
-        if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, ev[i + 1], 0), "wait");
-    }
-    for (int i = 0; i + 1 < n; ++i) {
-        pf_solver *lo = solvers[i], *hi = solvers[i + 1];
-        pf_halo hl, hh;
-        pf_halo_regions(lo, &hl);
-        pf_halo_regions(hi, &hh);
-        pf_solver *s = lo;
-        {
-            DeviceGuard dg(lo->device);
-            CK(cudaMemcpyAsync(hl.recv_up_u, hh.send_down_u, hl.bytes_u, cudaMemcpyDefault, lo->stream), "halo u");
-            CK(cudaMemcpyAsync(hl.recv_up_q, hh.send_down_q, hl.bytes_q, cudaMemcpyDefault, lo->stream), "halo q");
-        }
-        s = hi;
-        if (hh.bytes_qz) {
-            DeviceGuard dg(hi->device);
-            CK(cudaMemcpyAsync(hh.recv_down_qz, hl.send_up_qz, hh.bytes_qz, cudaMemcpyDefault, hi->stream), "halo qz");
-        }
-    }
-    for (int i = 0; i < n; ++i) {
-        pf_solver *s = solvers[i];
-        DeviceGuard dg(s->device);
-        CK(cudaEventRecord(ev[i], s->stream), "record");
-    }
-    for (int i = 0; i < n; ++i) {
-        pf_solver *s = solvers[i];
-        DeviceGuard dg(s->device);
-        if (i > 0) CK(cudaStreamWaitEvent(s->stream, ev[i - 1], 0), "wait");
-        if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, ev[i + 1], 0), "wait");
-    }
-    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
-    return PF_OK;
-}
-
-pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n) {
-    if (!solvers || n < 2) return fail(PF_ERR_INVALID, "need >= 2 solvers");
-    for (int i = 0; i < n; ++i) {
-        pf_status st = check_usable(solvers[i]);
-        if (st != PF_OK) return st;
-        const pf_solver *s = solvers[i];
-        if (!s->staged || !(s->cluster || s->sinfo.ostage == 1))
-            return fail(PF_ERR_UNSUPPORTED, "link: solver %d's kernel variant stores no whole tiles (use "
-                                            "pf_exchange_local)", i);
-        if (s->phase_pending) return fail(PF_ERR_STATE, "link: solver %d has an open split iteration", i);
-    }
-    for (int i = 0; i + 1 < n; ++i) {
-        const pf_solver *lo = solvers[i], *hi = solvers[i + 1];
-        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->pitch != hi->pitch ||
-            lo->gc.NF != hi->gc.NF || lo->gc.NL != hi->gc.NL || lo->cluster != hi->cluster || lo->cur != hi->cur ||
-            lo->sinfo.tile_y != hi->sinfo.tile_y)
-            return fail(PF_ERR_INVALID, "link: solvers %d and %d are not consecutive slabs of one volume in step", i,
-                        i + 1);
-    }
-    for (int i = 0; i + 1 < n; ++i) {   // peer access between devices (TMA stores into the neighbour's memory)
-        const int a = solvers[i]->device, b = solvers[i + 1]->device;
-        if (a == b) continue;
-        int ok1 = 0, ok2 = 0;
-        cudaDeviceCanAccessPeer(&ok1, a, b);
-        cudaDeviceCanAccessPeer(&ok2, b, a);
-        if (!ok1 || !ok2) return fail(PF_ERR_UNSUPPORTED, "link: no peer access between devices %d and %d", a, b);
-        {
-            DeviceGuard dg(a);
-            if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();   // already enabled is fine
-        }
-        {
-            DeviceGuard dg(b);
-            if (cudaDeviceEnablePeerAccess(a, 0) != cudaSuccess) cudaGetLastError();
-        }
-    }
-    for (int i = 0; i < n; ++i) {
-        pf_solver *s = solvers[i];
-        const int ty = s->sinfo.tile_y, NF = s->gc.NF, NL = s->gc.NL;
-        const int cq = s->cluster ? NL / 2 : 3 * NF, cl = s->cluster ? NL / 2 : NL, cz = s->cluster ? NL / 2 : NF;
-        bool ok = true;
-        s->nb_below = i > 0 ? solvers[i - 1] : nullptr;
-        s->nb_above = i + 1 < n ? solvers[i + 1] : nullptr;
-        s->link_below = s->nb_below != nullptr;
-        s->link_above = s->nb_above != nullptr;
-        if (s->nb_below) s->nb_plane = (int)s->nb_below->nzl + 1;
-        for (int b = 0; b < 2; ++b) {
-            if (s->nb_below) {   // below neighbour's buffers: its upper halo plane receives our plane 0
-                const pf_solver *t = s->nb_below;
-                ok = ok && encode4d(&s->tm_uo_nb[b], t->u_alloc[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl);
-                ok = ok && encode4d(&s->tm_qo_nb[b], t->q_alloc[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2,
-                                    32, ty, cq);
-            }
-            if (s->nb_above) {   // above neighbour's buffers: its lower halo plane receives our last q^z
-                const pf_solver *t = s->nb_above;
-                ok = ok && encode4d(&s->tm_qz_nb[b], t->q_alloc[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2,
-                                    32, ty, cz);
-            }
-        }
-        if (!ok) return fail(PF_ERR_CUDA, "link: cuTensorMapEncodeTiled failed");
-    }
-    return PF_OK;
-}
-
-pf_status pf_iterate_linked(pf_solver *const *solvers, int32_t n, int32_t iters, float *residual) {
-    if (!solvers || n < 1 || iters < 0) return fail(PF_ERR_INVALID, "need >= 1 solver and iters >= 0");
-    for (int i = 0; i < n; ++i) {
-        pf_status st = check_usable(solvers[i]);
-        if (st != PF_OK) return st;
-        if (i > 0 && solvers[i]->nb_below != solvers[i - 1])
-            return fail(PF_ERR_INVALID, "iterate_linked: solvers are not linked in this order");
-    }
-    // iteration t+1 of a slab starts after iteration t of both neighbours: they write its next halo planes
-    // (RAW) and read the buffers its next kernel writes into (WAR)
-    std::vector<cudaEvent_t> ev[2];
-    for (int e = 0; e < 2; ++e) {
-        ev[e].resize(n);
-        for (int i = 0; i < n; ++i) {
-            pf_solver *s = solvers[i];
-            DeviceGuard dg(s->device);
-            CK(cudaEventCreateWithFlags(&ev[e][i], cudaEventDisableTiming), "event");
-        }
-    }
-    bool any_check = false;
-    pf_status st = PF_OK;
-    for (int t = 0; t < iters && st == PF_OK; ++t) {
-        std::vector<cudaEvent_t> &prev = ev[(t + 1) & 1], &curv = ev[t & 1];
-        for (int i = 0; i < n; ++i) {
-            pf_solver *s = solvers[i];
-            DeviceGuard dg(s->device);
-            if (t > 0) {
-                if (i > 0) CK(cudaStreamWaitEvent(s->stream, prev[i - 1], 0), "wait");
-                if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, prev[i + 1], 0), "wait");
-            } else {   // the first iteration waits for whatever the neighbours had queued
-                if (i > 0) {
-                    CK(cudaEventRecord(curv[i - 1], solvers[i - 1]->stream), "record");
-                    CK(cudaStreamWaitEvent(s->stream, curv[i - 1], 0), "wait");
-                }
-                if (i + 1 < n) {
-                    CK(cudaEventRecord(curv[i + 1], solvers[i + 1]->stream), "record");
-                    CK(cudaStreamWaitEvent(s->stream, curv[i + 1], 0), "wait");
-                }
-            }
-            const int check = check_this_iteration(s);
-            if (check) {
-                CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
-                any_check = true;
-            }
-            if ((st = launch_items(s, 0, s->items, check)) != PF_OK) break;
-        }
-        for (int i = 0; i < n && st == PF_OK; ++i) {
-            pf_solver *s = solvers[i];
-            DeviceGuard dg(s->device);
-            CK(cudaEventRecord(curv[i], s->stream), "record");
-            s->cur = 1 - s->cur;
-            s->iters += 1;
-        }
-    }
-    // the neighbours' last kernels wrote this slab's halo planes: later work on its stream waits for them
-    if (iters > 0 && st == PF_OK) {
-        std::vector<cudaEvent_t> &last = ev[(iters - 1) & 1];
-        for (int i = 0; i < n; ++i) {
-            pf_solver *s = solvers[i];
-            DeviceGuard dg(s->device);
-            if (i > 0) CK(cudaStreamWaitEvent(s->stream, last[i - 1], 0), "wait");
-            if (i + 1 < n) CK(cudaStreamWaitEvent(s->stream, last[i + 1], 0), "wait");
-        }
-    }
-    float r = -1.f;
-    for (int i = 0; i < n && st == PF_OK; ++i) {
-        float ri = -1.f;
-        st = read_residual(solvers[i], any_check, residual ? &ri : nullptr);
-        r = std::max(r, ri);
-    }
-    for (int e = 0; e < 2; ++e)
-        for (int i = 0; i < n; ++i) cudaEventDestroy(ev[e][i]);
-    if (residual) *residual = r;
-    return st;
-}
-
-pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out) {
-    pf_status st = check_usable(s);
-    if (st != PF_OK) return st;
-    if (!out) return fail(PF_ERR_INVALID, "out is NULL");
-    if (!s->ipc) return fail(PF_ERR_STATE, "ipc_export: create the solver with pf_config.ipc = 1");
-    if (!s->staged || !(s->cluster || s->sinfo.ostage == 1))
-        return fail(PF_ERR_UNSUPPORTED, "ipc_export: this kernel variant stores no whole tiles");
-    DeviceGuard dg(s->device);
-    memset(out, 0, sizeof(*out));
-    for (int i = 0; i < 2; ++i) {
-        CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)out->u[i], s->u_alloc[i]), "ipc handle u");
-        CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)out->q[i], s->q_alloc[i]), "ipc handle q");
-    }
-    if (!s->ipc_ev) CK(cudaEventCreateWithFlags(&s->ipc_ev, cudaEventDisableTiming | cudaEventInterprocess), "ipc event");
-    CK(cudaIpcGetEventHandle((cudaIpcEventHandle_t *)out->event, s->ipc_ev), "ipc event handle");
-    CK(cudaEventRecord(s->ipc_ev, s->stream), "record");   // "my initial state is in place"
-    out->nx = s->nx;
-    out->ny = s->ny;
-    out->nzl = s->nzl;
-    out->z0 = s->z0;
-    out->pitch = s->pitch;
-    out->NF = s->gc.NF;
-    out->NL = s->gc.NL;
-    out->tile_y = s->sinfo.tile_y;
-    out->cluster = s->cluster ? 1 : 0;
-    out->cur = s->cur;
-    return PF_OK;
-}
-
-pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab *above) {
-    pf_status st = check_usable(s);
-    if (st != PF_OK) return st;
-    if (!s->ipc || !s->ipc_ev) return fail(PF_ERR_STATE, "ipc_link: export first (pf_ipc_export)");
-    DeviceGuard dg(s->device);
-    const int ty = s->sinfo.tile_y, NF = s->gc.NF, NL = s->gc.NL;
-    const int cq = s->cluster ? NL / 2 : 3 * NF, cl = s->cluster ? NL / 2 : NL, cz = s->cluster ? NL / 2 : NF;
-    const pf_ipc_slab *nb[2] = {below, above};
-    for (int side = 0; side < 2; ++side) {
-        const pf_ipc_slab *t = nb[side];
-        if (!t) continue;
-        const bool adjacent = side == 0 ? t->z0 + t->nzl == s->z0 : t->z0 == s->z1;
-        if (!adjacent || t->nx != s->nx || t->ny != s->ny || t->pitch != s->pitch || t->NF != NF || t->NL != NL ||
-            t->tile_y != ty || t->cluster != (s->cluster ? 1 : 0) || t->cur != s->cur)
-            return fail(PF_ERR_INVALID, "ipc_link: the %s blob is not this slab's neighbour in step",
-                        side == 0 ? "below" : "above");
-        void *ub[2] = {nullptr, nullptr}, *qb[2] = {nullptr, nullptr};
-        for (int b = 0; b < 2; ++b) {
-            CK(cudaIpcOpenMemHandle(&ub[b], *(const cudaIpcMemHandle_t *)t->u[b], cudaIpcMemLazyEnablePeerAccess),
-               "open ipc u");
-            s->ipc_opened.push_back(ub[b]);
-            CK(cudaIpcOpenMemHandle(&qb[b], *(const cudaIpcMemHandle_t *)t->q[b], cudaIpcMemLazyEnablePeerAccess),
-               "open ipc q");
-            s->ipc_opened.push_back(qb[b]);
-        }
-        CK(cudaIpcOpenEventHandle(&s->nb_ev[side], *(const cudaIpcEventHandle_t *)t->event), "open ipc event");
-        bool ok = true;
-        for (int b = 0; b < 2; ++b) {
-            if (side == 0) {   // below: its upper halo plane receives our plane 0
-                ok = ok && encode4d(&s->tm_uo_nb[b], ub[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl);
-                ok = ok && encode4d(&s->tm_qo_nb[b], qb[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2, 32,
-                                    ty, cq);
-            } else {           // above: its lower halo plane receives our last q^z
-                ok = ok && encode4d(&s->tm_qz_nb[b], qb[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2, 32,
-                                    ty, cz);
-            }
-        }
-        if (!ok) return fail(PF_ERR_CUDA, "ipc_link: cuTensorMapEncodeTiled failed");
-        if (side == 0) {
-            s->link_below = true;
-            s->nb_plane = (int)t->nzl + 1;
-        } else {
-            s->link_above = true;
-        }
-    }
-    return PF_OK;
-}
-
-pf_status pf_ipc_step(pf_solver *s, float *residual) {
-    pf_status st = check_usable(s);
-    if (st != PF_OK) return st;
-    if (!s->ipc || !s->ipc_ev) return fail(PF_ERR_STATE, "ipc_step: export and link first");
-    DeviceGuard dg(s->device);
-    // the neighbours' latest recorded iteration (the caller's host barrier makes it the previous one)
-    for (int i = 0; i < 2; ++i)
-        if (s->nb_ev[i]) CK(cudaStreamWaitEvent(s->stream, s->nb_ev[i], 0), "wait neighbour");
-    const int check = check_this_iteration(s);
-    if (check) CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
-    if ((st = launch_items(s, 0, s->items, check)) != PF_OK) return st;
-    CK(cudaEventRecord(s->ipc_ev, s->stream), "record");
-    s->cur = 1 - s->cur;
-    s->iters += 1;
-    return read_residual(s, check != 0, residual);
 }
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
