@@ -187,6 +187,11 @@ pf_status pf_get_flows(pf_solver *s, float *q);
  * halos must be current; the caller sums over ranks. */
 pf_status pf_get_energy(pf_solver *s, double *primal, double *dual);
 
+/* Change the step constants c (entropic proximal weight, Eq. 7 / P:119) and tau (flow step)
+ * between calls, e.g. for a c-annealing schedule; the state is kept.  Errors:
+ * PF_ERR_INVALID (non-positive or non-finite). */
+pf_status pf_set_step(pf_solver *s, float c, float tau);
+
 /* Iterations run since create / reset. */
 pf_status pf_iterations(const pf_solver *s, int64_t *done);
 

@@ -34,7 +34,7 @@ PF_S_SCALAR_PER_NODE, PF_S_SHARED_FIELD, PF_S_FIELD_PER_NODE, PF_S_SCALED_FIELD 
 _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_CUDA", 5: "PF_ERR_UNSUPPORTED",
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
-EXPORTED = ["pf_create", "pf_reset", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling",
+EXPORTED = ["pf_create", "pf_reset", "pf_set_step", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling",
             "pf_link_slabs", "pf_iterate_linked", "pf_ipc_export", "pf_ipc_link", "pf_ipc_step", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
@@ -94,6 +94,7 @@ _sig = {
     "pf_create": (ctypes.c_int, [_P(pf_dims), _P(pf_graph), _P(ctypes.c_void_p), _P(pf_smoothness), _P(pf_config),
                                  _P(pf_slab), _P(ctypes.c_void_p)]),
     "pf_reset": (ctypes.c_int, [_vp]),
+    "pf_set_step": (ctypes.c_int, [_vp, ctypes.c_float, ctypes.c_float]),
     "pf_iterate": (ctypes.c_int, [_vp, ctypes.c_int32, _P(ctypes.c_float)]),
     "pf_iterate_phase": (ctypes.c_int, [_vp, ctypes.c_int32, _P(ctypes.c_float)]),
     "pf_run": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_float, _P(ctypes.c_int32), _P(ctypes.c_float)]),
@@ -189,6 +190,10 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
 
 def pf_reset(s: int):
     _check(_lib.pf_reset(s))
+
+
+def pf_set_step(s: int, c: float, tau: float):
+    _check(_lib.pf_set_step(s, float(c), float(tau)))
 
 
 def pf_iterate(s: int, n: int, want_residual: bool = False) -> Optional[float]:

@@ -583,6 +583,22 @@ pf_status pf_reset(pf_solver *s) {
     return PF_OK;
 }
 
+pf_status pf_set_step(pf_solver *s, float c, float tau) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (!(c > 0.f) || !(tau > 0.f) || !std::isfinite(c) || !std::isfinite(tau))
+        return fail(PF_ERR_INVALID, "set_step: c and tau must be finite and > 0");
+    s->cfg.c = c;
+    s->cfg.tau = tau;
+    if (s->graph) {   // the captured launches carry the old constants
+        DeviceGuard dg(s->device);
+        cudaStreamSynchronize(s->stream);
+        cudaGraphExecDestroy(s->graph);
+        s->graph = nullptr;
+    }
+    return PF_OK;
+}
+
 pf_status pf_set_stream(pf_solver *s, void *stream) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;

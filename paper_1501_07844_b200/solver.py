@@ -9,6 +9,7 @@ from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NOD
                PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_iterate_linked, pf_link_slabs, pf_get_energy, pf_get_flows, pf_get_kernel_info,
                pf_get_labeling, pf_get_node_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
+               pf_set_step,
                pf_set_stream)
 
 
@@ -58,6 +59,10 @@ class Solver:
 
     def iterate(self, n: int, residual: bool = False):
         return pf_iterate(self.h, n, residual)
+
+    def set_step(self, c: float, tau: float):
+        """New step constants for the following iterations (c-annealing); the state is kept."""
+        pf_set_step(self.h, c, tau)
 
     def run(self, max_iters: int, tol: float):
         """Iterate until converged (residual <= tol at a check iteration) or max_iters: (iterations, residual)."""

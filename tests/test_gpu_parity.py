@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+import paper_1501_07844_b200 as pf
 import phantoms as P
 from helpers import bf16_rounded, compare, solver_from_inputs, with_field_per_node
 
@@ -226,6 +227,23 @@ def test_intermediate_node_labelings(name):
         if kids:
             want = sum(float(w) * node_u[c] for c, w in kids)
             assert np.max(np.abs(node_u[v] - want)) < 1e-5
+
+
+def test_c_annealing_schedule():
+    """pf_set_step between calls (SURVEY 8(f3) c-annealing): the GPU follows the oracle through a schedule
+    of c values, also across CUDA-graph replays captured with the old constants."""
+    inp = P.generate(P.config("C2").resized(37, 29, 21))
+    s = solver_from_inputs(inp)
+    state = None
+    for c, n in ((0.5, 20), (0.25, 20), (0.125, 13)):
+        s.set_step(c, 0.1)
+        s.iterate(n)
+        state = O.run_inputs(inp, n, c=c, tau=0.1, state=state)
+    u, _ = s.labeling()
+    compare(u, s.flows(), *state)
+    with pytest.raises(pf.PFError):
+        s.set_step(0.0, 0.1)
+    s.close()
 
 
 def test_split_calls_equal_one_call():
