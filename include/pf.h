@@ -2,9 +2,10 @@
  * pf.h -- C-ABI of the B200 pseudo-flow continuous max-flow solver (arXiv 1501.07844).
  *
  * The library (paper_1501_07844_b200/libpf.so) runs the per-iteration hot path of
- * the paper's Algorithm 1 (Potts) and Algorithm 2
- * (HMF / DAGMF) on one sm_100a GPU per solver, entirely in its own CUDA
- * kernels.  No torch types cross this boundary; PyTorch (above it) only provides
+ * the paper's Algorithm 1 (Potts), Algorithm 2 (HMF / DAGMF,
+ * P:279-305) and Algorithm 3 (Ishikawa) on one sm_100a GPU per solver,
+ * entirely in its own CUDA kernels; z-slab solvers cooperate across devices and
+ * processes (pf_halo_regions, pf_exchange_local, pf_link_slabs, pf_ipc_*).  No torch types cross this boundary; PyTorch (above it) only provides
  * device selection, streams and process groups.
  *
  * Problem statement (BASELINE.json north_star):
@@ -51,7 +52,8 @@ typedef enum {
     PF_ERR_CUDA = 4,    /* CUDA runtime error (message carries cudaGetErrorString) */
     PF_ERR_UNSUPPORTED = 5, /* graph shape outside the compiled kernel set */
     PF_ERR_NUMERIC = 6, /* a(x) <= 0 or not finite detected at a check (message names the voxel) */
-    PF_ERR_STATE = 7    /* solver poisoned by an earlier error */
+    PF_ERR_STATE = 7    /* solver poisoned by an earlier error, or calls out of order (split iterations,
+                           linked slabs, IPC protocol) */
 } pf_status;
 
 typedef enum { PF_CAP_L2 = 0, PF_CAP_LINF = 1 } pf_capacity;
@@ -106,10 +108,12 @@ typedef struct {
     int32_t ipc;         /* 1: allocate the state so that another process can map it (pf_ipc_export);
                           * 0: stream-ordered pool allocations. */
     int32_t method;      /* PF_METHOD_PSEUDO_FLOW (default): Alg. 1 / 2 / 3.  PF_METHOD_EXPLICIT_ALM: the
-                          * explicit-flow ("full-flow") augmented-Lagrangian solver of the Potts
-                          * model Eq. 3 that stores p_S and p_L, the comparison arm of SURVEY 8(f2):
-                          * c = the ALM penalty, tau = its flow step; Potts graphs, whole volumes, l2 or
-                          * box capacities only (else PF_ERR_UNSUPPORTED); no split iterations. */
+                          * explicit-flow ("full-flow") augmented-Lagrangian solver that stores
+                          * the source / sink flows -- Eq. 3 for Potts, Eq. 11 for
+                          * HMF / DAG graphs -- the comparison arm of SURVEY 8(f2): c = the ALM penalty, tau
+                          * = its flow step; whole volumes, scalar / shared / per-node capacities, <= 16
+                          * non-source nodes, no Ishikawa model (else PF_ERR_UNSUPPORTED); no split or
+                          * linked iterations. */
 } pf_config;
 
 enum { PF_METHOD_PSEUDO_FLOW = 0, PF_METHOD_EXPLICIT_ALM = 1 };
