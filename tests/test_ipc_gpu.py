@@ -91,3 +91,28 @@ def test_ipc_fused_exchange_bitwise(name, dims, world, iters):
         assert all(float(p["r"]) == r_ref for p in parts)          # residual: max over ranks
         e = parts[0]["e"]
         assert abs(e[0] - e_ref[0]) <= 1e-9 * abs(e_ref[0]) and abs(e[1] - e_ref[1]) <= 1e-9 * abs(e_ref[0])
+
+
+def test_ipc_protocol_errors():
+    import paper_1501_07844_b200 as pf
+    import phantoms as P
+    from helpers import solver_from_inputs
+
+    inp = P.generate(P.config("C2").resized(40, 17, 12))
+    s = solver_from_inputs(inp, slab=(0, 6))            # not created with ipc=True
+    with pytest.raises(pf.PFError) as ei:
+        pf.pf_ipc_export(s.h)
+    assert ei.value.status == pf.PF_ERR_STATE
+    with pytest.raises(pf.PFError) as ei:
+        pf.pf_ipc_step(s.h)
+    assert ei.value.status == pf.PF_ERR_STATE
+    s.close()
+    a, b = _ipc_solver(inp, (0, 6)), _ipc_solver(inp, (6, 12))
+    if not a.kernel_info()["staged"]:
+        pytest.skip("fused halo stores need the TMA-staged kernels")
+    blob_a = pf.pf_ipc_export(a.h)
+    with pytest.raises(pf.PFError) as ei:               # a's own blob is not the slab above it
+        pf.pf_ipc_link(a.h, None, blob_a)
+    assert ei.value.status == pf.PF_ERR_INVALID
+    a.close()
+    b.close()
