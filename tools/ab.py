@@ -1,6 +1,6 @@
 """A/B timing of library builds in ONE GPU session (boxes differ from call to call, so only
 interleaved runs on the same GPU compare kernel variants).
-usage: python tools/ab.py --libs libpf_ref.so libpf.so libpf.so:PF_CLUSTER=0 --configs C2 C5slab [--rounds 3]
+usage: python tools/ab.py --libs libpf_ref.so libpf.so libpf.so:PF_CLUSTER=0 --configs C2 C5slab [--rounds 3] [--alm]
 Each (round, config, lib) runs tools/bench_configs.py in a fresh process with PF_LIB=<lib>."""
 import argparse
 import json
@@ -15,6 +15,7 @@ ap.add_argument("--libs", nargs="+", required=True)
 ap.add_argument("--configs", nargs="+", default=["C2", "C5slab"])
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--alm", action="store_true", help="time the explicit-flow ALM arm (bench_configs.py --alm)")
 args = ap.parse_args()
 res = {}
 for r in range(args.rounds):
@@ -27,7 +28,7 @@ for r in range(args.rounds):
                 k, _, v = kv.partition("=")
                 env[k] = v
             pr = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_configs.py"), c, "--steps",
-                                 str(args.steps)], env=env, capture_output=True, text=True)
+                                 str(args.steps)] + (["--alm"] if args.alm else []), env=env, capture_output=True, text=True)
             out = pr.stdout
             if pr.returncode != 0:
                 print(json.dumps({"round": r, "config": c, "lib": lib, "failed": pr.returncode,
