@@ -191,6 +191,18 @@ pf_status pf_get_flows(pf_solver *s, float *q);
  * halos must be current; the caller sums over ranks. */
 pf_status pf_get_energy(pf_solver *s, double *primal, double *dual);
 
+/* Restore a state saved with pf_get_labeling (u) and pf_get_flows (q) -- checkpoint / resume
+ * (SURVEY "Checkpoint/resume", test P11: 150 + resume + 150 iterations == 300, bitwise).
+ * u: [|L|][z][y][x] of the owned slab, end-label order (as pf_get_labeling); q: [num_nodes-1][ndim]
+ * [z][y][x], node-id order (as pf_get_flows; the zero flows of Ishikawa end labels are not read);
+ * host or device pointers, read before the call returns (host) or in stream order (device); the caller
+ * keeps ownership.  `iterations` = pf_iterations at save time: it fixes which later iterations are
+ * residual-check iterations.  c and tau are not part of the state (pf_set_step).  Slab solvers: only
+ * the owned planes are written -- refresh the halo planes with the exchange before iterating.
+ * Errors: PF_ERR_INVALID (NULL u / q, negative iterations), PF_ERR_UNSUPPORTED (explicit-flow ALM,
+ * whose state also holds p and p_S). */
+pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t iterations);
+
 /* Change the step constants c (entropic proximal weight, Eq. 7 / P:119) and tau (flow step)
  * between calls, e.g. for a c-annealing schedule; the state is kept.  Errors:
  * PF_ERR_INVALID (non-positive or non-finite). */

@@ -35,7 +35,7 @@ _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_C
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
 EXPORTED = ["pf_create", "pf_reset", "pf_set_step", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling",
-            "pf_link_slabs", "pf_iterate_linked", "pf_ipc_export", "pf_ipc_link", "pf_ipc_step", "pf_get_labeling", "pf_get_flows", "pf_get_energy",
+            "pf_link_slabs", "pf_iterate_linked", "pf_ipc_export", "pf_ipc_link", "pf_ipc_step", "pf_get_labeling", "pf_get_flows", "pf_set_state", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
@@ -100,6 +100,7 @@ _sig = {
     "pf_run": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_float, _P(ctypes.c_int32), _P(ctypes.c_float)]),
     "pf_get_labeling": (ctypes.c_int, [_vp, _vp, _vp]),
     "pf_get_flows": (ctypes.c_int, [_vp, _vp]),
+    "pf_set_state": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
     "pf_get_node_labeling": (ctypes.c_int, [_vp, ctypes.c_int32, _vp]),
     "pf_get_energy": (ctypes.c_int, [_vp, _P(ctypes.c_double), _P(ctypes.c_double)]),
     "pf_iterations": (ctypes.c_int, [_vp, _P(ctypes.c_int64)]),
@@ -222,6 +223,10 @@ def pf_get_labeling(s: int, u=None, argmax=None):
 
 def pf_get_flows(s: int, q):
     _check(_lib.pf_get_flows(s, _ptr(q)))
+
+
+def pf_set_state(s: int, u, q, iterations: int):
+    _check(_lib.pf_set_state(s, None if u is None else _ptr(u), None if q is None else _ptr(q), int(iterations)))
 
 
 def pf_get_node_labeling(s: int, node: int, out):

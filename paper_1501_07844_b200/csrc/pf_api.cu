@@ -583,6 +583,41 @@ pf_status pf_reset(pf_solver *s) {
     return PF_OK;
 }
 
+pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t iterations) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (s->alm) return fail(PF_ERR_UNSUPPORTED, "set_state: the explicit-flow ALM state also holds p, p_S");
+    if (!u || !q) return fail(PF_ERR_INVALID, "set_state: u and q are required");
+    if (iterations < 0) return fail(PF_ERR_INVALID, "set_state: iterations must be >= 0");
+    DeviceGuard dg(s->device);
+    const int NL = s->gc.NL, NV = s->gc.NV, NF = s->gc.NF, nd = s->ndim;
+    const int64_t P = s->P, nzl = s->nzl;
+    const int64_t V = s->nx * s->ny * nzl;
+    // (a replayable graph captured the old state parity / iteration alignment)
+    if (s->graph) {
+        cudaStreamSynchronize(s->stream);
+        cudaGraphExecDestroy(s->graph);
+        s->graph = nullptr;
+    }
+    for (int l = 0; l < NL; ++l)
+        CK(copy_volume(true, s->u[s->cur] + l * P, NL, const_cast<float *>(u) + l * V, s->nx, s->ny, s->pitch, nzl,
+                       s->stream),
+           "upload u");
+    for (int p = 0; p < NF && p < NV; ++p) {   // nodes without a stored flow (Ishikawa end labels): not read
+        const int v = s->gc.node_of_pos[p];
+        for (int k = 0; k < nd; ++k)
+            CK(copy_volume(true, s->q[s->cur] + ((int64_t)k * NF + p) * P, (int64_t)3 * NF,
+                           const_cast<float *>(q) + ((int64_t)(v - 1) * nd + k) * V, s->nx, s->ny, s->pitch, nzl,
+                           s->stream),
+               "upload q");
+    }
+    CK(cudaMemsetAsync(s->d_err, 0xff, sizeof(unsigned long long), s->stream), "init err");
+    if (!is_device_ptr(u) || !is_device_ptr(q)) CK(cudaStreamSynchronize(s->stream), "sync");   // host buffers
+    s->iters = iterations;
+    if (s->ipc_ev) CK(cudaEventRecord(s->ipc_ev, s->stream), "record");
+    return PF_OK;
+}
+
 pf_status pf_set_step(pf_solver *s, float c, float tau) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;

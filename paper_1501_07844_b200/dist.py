@@ -186,6 +186,24 @@ class DistSolver:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return float(t[0]), float(t[1])
 
+    # ------------------------------------------------------------ checkpoint / resume (pf_set_state)
+    def _rank_path(self, prefix: str) -> str:
+        return f"{prefix}.rank{self.rank}of{self.world}.npz"
+
+    def save(self, prefix: str, **meta):
+        """Every rank writes its own slab (u, q, iteration count) to <prefix>.rank<r>of<P>.npz."""
+        return self.solver.save(self._rank_path(prefix), **meta)
+
+    def load(self, prefix: str):
+        """Every rank restores its slab, then the halo planes are refreshed with one exchange (the
+        checkpoint holds only owned planes).  Returns the saved (c, tau)."""
+        if self.transport == "ipc" and self.world > 1:
+            raise NotImplementedError("resume over the IPC transport: the halos are only pushed by iterations")
+        out = self.solver.load(self._rank_path(prefix))
+        if self.world > 1:
+            halo_exchange(self._regions(), self.rank, self.world, self.group)
+        return out
+
     def _comm_stream(self):
         if getattr(self, "_C", None) is None:
             self._C = torch.cuda.Stream(self.device)

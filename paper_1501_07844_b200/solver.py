@@ -9,7 +9,7 @@ from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NOD
                PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_iterate_linked, pf_link_slabs, pf_get_energy, pf_get_flows, pf_get_kernel_info,
                pf_get_labeling, pf_get_node_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
-               pf_set_step,
+               pf_set_state, pf_set_step,
                pf_set_stream)
 
 
@@ -100,6 +100,39 @@ class Solver:
 
     def energy(self):
         return pf_get_energy(self.h)
+
+    # ---------------------------------------------------------------- checkpoint / resume
+    def state(self):
+        """(u, q, iterations): the resumable state of the owned slab (pf_get_labeling / pf_get_flows)."""
+        u, _ = self.labeling()
+        return u, self.flows(), self.iterations()
+
+    def set_state(self, u, q, iterations: int):
+        """Restore a state from state() (pf_set_state); slab solvers then need a halo exchange."""
+        pf_set_state(self.h, np.ascontiguousarray(u, dtype=np.float32) if isinstance(u, np.ndarray) else u,
+                     np.ascontiguousarray(q, dtype=np.float32) if isinstance(q, np.ndarray) else q, iterations)
+
+    def save(self, path: str, c: Optional[float] = None, tau: Optional[float] = None):
+        """Checkpoint to one .npz: u, q (raw float32), the iteration count and the geometry it belongs to
+        (plus the current c, tau if given: they are configuration, not state)."""
+        u, q, it = self.state()
+        meta = {"dims": self.dims, "ndim": self.ndim, "num_nodes": self.num_nodes, "labels": self.NL,
+                "slab": self.slab, "iterations": it, "c": c, "tau": tau}
+        np.savez(path, u=u, q=q, meta=np.frombuffer(repr(meta).encode(), dtype=np.uint8))
+
+    def load(self, path: str):
+        """Resume from save(): checks the geometry, restores u, q and the iteration count; returns the
+        saved (c, tau) (None where not saved) so a schedule can continue with pf_set_step."""
+        import ast
+        z = np.load(path)
+        meta = ast.literal_eval(bytes(z["meta"]).decode())
+        mine = {"dims": self.dims, "ndim": self.ndim, "num_nodes": self.num_nodes, "labels": self.NL,
+                "slab": self.slab}
+        for k, v in mine.items():
+            if (tuple(meta[k]) if isinstance(v, tuple) else meta[k]) != v:
+                raise ValueError(f"checkpoint {k} = {meta[k]} does not match this solver's {v}")
+        self.set_state(z["u"], z["q"], meta["iterations"])
+        return meta.get("c"), meta.get("tau")
 
     def iterations(self) -> int:
         return pf_iterations(self.h)

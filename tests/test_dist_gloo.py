@@ -133,6 +133,13 @@ class _StubSolver:
     def energy(self):
         return 1.5 * (self.rank + 1), 0.5 * (self.rank + 1)
 
+    def save(self, path, **meta):
+        self.saved = path
+
+    def load(self, path):
+        self.loaded = path
+        return 0.25, 0.1
+
 
 def _dist_worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -157,7 +164,18 @@ def _dist_worker(rank, world, port, out):
     ds = CpuDist(lambda slab: _StubSolver(rank), 16, rank, world, torch.device("cpu"))
     n, r = ds.run(1000, 0.05)            # rank r reports (r+1)/it: the max over ranks is world/it
     e = ds.energy()
-    out[rank] = (n, r, e)
+    # resume: each rank loads its own file, then the halos are refreshed by one exchange
+    got = {}
+
+    def regions():
+        r = CpuDist._regions(ds)
+        got.update(r)
+        return r
+    ds._regions = regions
+    ds.save("/tmp/ck")
+    ct = ds.load("/tmp/ck")
+    halos = {k: float(v[0]) for k, v in got.items() if v is not None and k.startswith("recv")}
+    out[rank] = (n, r, e, ds.solver.saved, ds.solver.loaded, ct, halos)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -169,6 +187,13 @@ def test_dist_run_uses_global_residual_and_sums_energies(world):
     mp.spawn(_dist_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     want_it = 5 * int(np.ceil(world / 0.05 / 5))            # first check iteration with world / it <= 0.05
     for rank in range(world):
-        n, r, (e, f) = out[rank]
+        n, r, (e, f), saved, loaded, ct, halos = out[rank]
         assert n == want_it and abs(r - world / want_it) < 1e-6
         assert e == 1.5 * world * (world + 1) / 2 and f == 0.5 * world * (world + 1) / 2
+        assert saved == loaded == f"/tmp/ck.rank{rank}of{world}.npz" and ct == (0.25, 0.1)
+        want = {}
+        if rank > 0:
+            want["recv_down_qz"] = float(rank - 1)          # the lower neighbour's last-plane q^z
+        if rank < world - 1:
+            want["recv_up_u"] = want["recv_up_q"] = float(rank + 1)
+        assert halos == want
