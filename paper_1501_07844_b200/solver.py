@@ -201,6 +201,17 @@ class SlabSet:
     def exchange(self):
         pf_exchange_local(self.handles)
 
+    def state(self):
+        """(u, q, iterations) of the whole volume (slabs concatenated along z)."""
+        return self.labeling()[0], self.flows(), self.solvers[0].iterations()
+
+    def set_state(self, u, q, iterations: int):
+        """Restore a whole-volume state: every slab takes its planes, then one halo exchange."""
+        for sv in self.solvers:
+            z0, z1 = sv.slab
+            sv.set_state(np.ascontiguousarray(u[:, z0:z1]), np.ascontiguousarray(q[:, :, z0:z1]), iterations)
+        pf_exchange_local(self.handles)
+
     def labeling(self):
         us, ams = zip(*[s.labeling() for s in self.solvers])
         return np.concatenate(us, axis=1), np.concatenate(ams, axis=0)

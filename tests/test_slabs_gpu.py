@@ -94,3 +94,27 @@ def test_linked_slab_rules(monkeypatch):
     assert ei.value.status == pf.PF_ERR_UNSUPPORTED
     for s in ss:
         s.close()
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_slab_resume_from_single_domain_state(fused):
+    """Checkpoint of a single-domain run restored into a slab set (pf_set_state per slab + one halo
+    exchange): the continued slab run equals the uninterrupted single-domain run, bitwise."""
+    cfg = P.config("C2").resized(40, 33, 23)
+    inp = P.generate(cfg)
+    ref = solver_from_inputs(inp)
+    ref.iterate(17)
+    u, q, it = ref.state()
+    ref.iterate(14)
+    solvers = [solver_from_inputs(inp, slab=b) for b in pf.solver.slab_bounds(cfg.nz, 3)]
+    if fused and not all(s.kernel_info()["staged"] for s in solvers):
+        pytest.skip("fused halo stores need the TMA-staged kernels")
+    slabs = pf.SlabSet(solvers, fused=fused)
+    slabs.iterate(3)                     # some other state first
+    slabs.set_state(u, q, it)
+    slabs.iterate(14)
+    u2, q2, it2 = slabs.state()
+    assert it2 == it + 14
+    assert np.array_equal(u2, ref.labeling()[0]) and np.array_equal(q2, ref.flows())
+    slabs.close()
+    ref.close()
