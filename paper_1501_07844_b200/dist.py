@@ -40,11 +40,35 @@ def device_view(ptr: int, nbytes: int, device: torch.device) -> torch.Tensor:
     return torch.as_tensor(_CudaBuf(ptr, nbytes), device=device)
 
 
+class _StreamWork:
+    """Work handle of a host-staged exchange: wait() orders the caller's current stream after it."""
+
+    def __init__(self, ev):
+        self.ev = ev
+
+    def wait(self):
+        torch.cuda.current_stream().wait_event(self.ev)
+
+
 def halo_exchange(regions: Dict[str, Optional[torch.Tensor]], rank: int, world: int, group=None, wait: bool = True):
     """Exchange one iteration's halo planes.  regions: send_down_u, send_down_q, recv_up_u, recv_up_q,
     send_up_qz, recv_down_qz (None where the neighbour does not exist).  Per peer pair the messages
     are posted in the same order on both sides (u, then q downward; q^z upward).  wait=False returns
-    the work handles (their wait() orders the caller's current stream after the transfer)."""
+    the work handles (their wait() orders the caller's current stream after the transfer).
+    Device regions over a backend without device transport (gloo: multi-process tests on one GPU)
+    are staged through host memory on the current stream; NCCL moves them device to device."""
+    if dist.get_backend(group) != "nccl" and any(v is not None and v.is_cuda for v in regions.values()):
+        host = {k: (v.cpu() if k.startswith("send") else torch.empty(v.shape, dtype=v.dtype))
+                for k, v in regions.items() if v is not None}
+        halo_exchange({k: host.get(k) for k in regions}, rank, world, group, wait=True)
+        for k, v in regions.items():
+            if v is not None and k.startswith("recv"):
+                v.copy_(host[k])
+        if wait:
+            return []
+        ev = torch.cuda.Event()
+        ev.record()
+        return [_StreamWork(ev)]
     ops = []
     if rank > 0:
         ops.append(dist.P2POp(dist.isend, regions["send_down_u"], rank - 1, group))
