@@ -279,7 +279,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": cfg.name + (": 3D Potts 256^3, K=8, 300 iterations" if world == 1 else
                                                 f": 3D Potts 256x256x{cfg.nz} (256^3 z-slab per GPU), K=8, "
                                                 f"{iters} iterations, halo exchange: " +
-                                                ("fused CUDA-IPC peer stores" if ipc else "NCCL P2P, overlapped")),
+                                                ("fused CUDA-IPC peer stores" if ipc else "NCCL P2P, overlapped" if dist.get_backend() == "nccl" else f"{dist.get_backend()} host-staged (validation only, not a measurement)")),
                        "voxels_per_gpu": V, "labels": NL, "iterations_per_step": iters, "residual_check_every": 10,
                        "l2": "no flush: per-iteration state 4.9 GB/GPU >> 126 MB L2",
                        "kernel": {k: info[k] for k in ("tile_x", "tile_y", "z_chunk", "threads_per_cta", "ctas",
@@ -316,11 +316,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    # validation only (never for a reported number): PF_BENCH_BACKEND=gloo with PF_BENCH_ONE_GPU=1 runs the
+    # N-rank code path as N processes on cuda:0 (host-staged halo exchange, see dist.halo_exchange)
+    backend = os.environ.get("PF_BENCH_BACKEND", "nccl")
+    if os.environ.get("PF_BENCH_ONE_GPU") == "1":
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
