@@ -31,7 +31,8 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 SHIFT_MIN, SHIFT_NONE = 0, 1
-U_FLOOR = 2.0 ** -126   # reading R18: labels below the fp32 normal range are dead (0)
+U_FLOOR = 0.0          # reading R18: no floor (paper-exact); u_floor > 0 is an opt-in diagnostic only
+FP32_NORMAL_MIN = 2.0 ** -126
 CAP_L2, CAP_LINF = 0, 1
 
 
@@ -177,7 +178,7 @@ def argmax(u: np.ndarray) -> np.ndarray:
 
 
 def run_inputs(inp, niter: int, shift: int = SHIFT_MIN, cap: Optional[int] = None, c: Optional[float] = None,
-               tau: Optional[float] = None, state=None):
+               tau: Optional[float] = None, state=None, u_floor: float = U_FLOOR):
     """Run the oracle on a phantoms.Inputs object from the initial state (or `state`)."""
     cfg, g = inp.cfg, inp.graph
     cap = (CAP_L2 if cfg.cap == "l2" else CAP_LINF) if cap is None else cap
@@ -194,12 +195,12 @@ def run_inputs(inp, niter: int, shift: int = SHIFT_MIN, cap: Optional[int] = Non
     else:
         u, q = state
     if cfg.kind == "potts":
-        potts_iterate(D, np.ascontiguousarray(S[1:]), u, q, cfg.ndim, c, tau, niter, shift, cap)
+        potts_iterate(D, np.ascontiguousarray(S[1:]), u, q, cfg.ndim, c, tau, niter, shift, cap, u_floor)
     elif cfg.kind == "ishikawa":
         # Alg. 3 on the level flows (node ids 1..N); end labels (ids N+1..) carry no flow and stay 0
         N = NL - 1
-        ishikawa_iterate(D, np.ascontiguousarray(S[1:N + 1]), u, q[:N], cfg.ndim, c, tau, niter, shift, cap)
+        ishikawa_iterate(D, np.ascontiguousarray(S[1:N + 1]), u, q[:N], cfg.ndim, c, tau, niter, shift, cap, u_floor)
     else:
         dag_iterate(g.num_nodes, g.parent, g.child, g.weight.astype(np.float64), D, S, u, q, cfg.ndim, c, tau,
-                    niter, shift, cap)
+                    niter, shift, cap, u_floor)
     return u, q

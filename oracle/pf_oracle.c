@@ -21,9 +21,9 @@
  *   R5  |q| <= S: cap==0 Euclidean ball, cap==1 box (|q^k| <= S, dual of l1-TV).
  *   R14 Proj: if |q| > S then q*S/|q| else q (S = 0, q = 0 gives 0).
  *   R8  q starts at 0; u starts at 1/|L| -- set by the caller.
- *   R18 u is stored in fp32 (BASELINE north_star): a normalised label value below the fp32
- *       normal range (u_floor, 2^-126 by default; 0 disables) is set to 0 -- "the label has died"
- *       is decided at the precision the labels are stored in.
+ *   R18 no floor: the listings never set a label to 0, so the oracle does
+ *       not either (u_floor = 0, the default of the Python wrapper).  u_floor > 0 is an opt-in
+ *       DIAGNOSTIC only (normalised values below it set to 0); no parity test uses it.
  *
  * Layouts (the C-ABI boundary layout): every field is one volume of V = nx*ny*nz
  * values, x fastest.  u: [NL][V] (end labels in node-id order), q: [node][k][V]

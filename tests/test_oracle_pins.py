@@ -122,12 +122,12 @@ def test_zero_smoothness_closed_form(shift):
     u, q = O.init_state(K, K, D.shape[1:], 3)
     u0, q0 = O.init_state(K, K, D.shape[1:], 3)
     for t in range(1, 31):
-        O.potts_iterate(D, S, u, q, 3, c, 0.1, 1, shift)
-        O.potts_iterate(D, S, u0, q0, 3, c, 0.1, 1, shift, u_floor=0.0)
+        O.potts_iterate(D, S, u, q, 3, c, 0.1, 1, shift, u_floor=O.FP32_NORMAL_MIN)   # opt-in floor (diagnostic)
+        O.potts_iterate(D, S, u0, q0, 3, c, 0.1, 1, shift)                             # default: paper-exact
         z = -t * D / c
         ref = np.exp(z - z.max(0)) / np.exp(z - z.max(0)).sum(0)
         np.testing.assert_allclose(u0, ref, rtol=1e-12, atol=1e-300)           # exact closed form
-        np.testing.assert_allclose(u, np.where(ref < O.U_FLOOR, 0.0, ref), rtol=1e-12, atol=1e-300)   # R18
+        np.testing.assert_allclose(u, np.where(ref < O.FP32_NORMAL_MIN, 0.0, ref), rtol=1e-12, atol=1e-300)
         assert np.all(q == 0)
 
 
