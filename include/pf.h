@@ -174,7 +174,9 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual);
 
 /* Current labeling of the owned slab: u (may be NULL) as [|L|][V_local] and the
  * thresholded labeling argmax (may be NULL) as uint8 [V_local], ties to the lowest
- * label id ("thresholded"). */
+ * label id ("thresholded"), taken on the exported u values.  The pseudo-flow
+ * state is log2 u (reading R18); u is exported as 2^lambda in fp32 (labels below
+ * 2^-126 read as 0).  Host or device buffers. */
 pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax);
 
 /* Labeling of any node v of the graph (row a9, "intermediate labels on demand"): u_v(x) =
@@ -191,9 +193,17 @@ pf_status pf_get_flows(pf_solver *s, float *q);
  * halos must be current; the caller sums over ranks. */
 pf_status pf_get_energy(pf_solver *s, double *primal, double *dual);
 
-/* Restore a state saved with pf_get_labeling (u) and pf_get_flows (q) -- checkpoint / resume
- * (SURVEY "Checkpoint/resume", test P11: 150 + resume + 150 iterations == 300, bitwise).
- * u: [|L|][z][y][x] of the owned slab, end-label order (as pf_get_labeling); q: [num_nodes-1][ndim]
+/* The exact resumable state of the owned slab (checkpoint; SURVEY "Checkpoint/resume", test P11).  The
+ * pseudo-flow solver stores the labeling as lambda_L = log2 u_L in fp32 (reading R18: a stored label cannot
+ * underflow; pf_get_labeling exports u = 2^lambda), so a bitwise resume needs lambda itself:
+ * u_log2: [|L|][z][y][x] of lambda (may be NULL); q: [num_nodes-1][ndim][z][y][x] as pf_get_flows (may be
+ * NULL); host or device.  Errors: PF_ERR_UNSUPPORTED (explicit-flow ALM). */
+pf_status pf_get_state(pf_solver *s, float *u_log2, float *q);
+
+/* Restore a state -- checkpoint / resume (test P11: 150 + resume + 150 iterations == 300, bitwise, from
+ * pf_get_state), or start from a given labeling.  u: [|L|][z][y][x] of the owned slab, end-label order:
+ * lambda = log2 u as pf_get_state returns it (u_is_log2 = 1), or the labeling u itself (u_is_log2 = 0,
+ * converted with a correctly rounded log2; u = 0 is a dead label, lambda = -inf).  q: [num_nodes-1][ndim]
  * [z][y][x], node-id order (as pf_get_flows; the zero flows of Ishikawa end labels are not read);
  * host or device pointers, read before the call returns (host) or in stream order (device); the caller
  * keeps ownership.  `iterations` = pf_iterations at save time: it fixes which later iterations are
@@ -201,7 +211,7 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual);
  * the owned planes are written -- refresh the halo planes with the exchange before iterating.
  * Errors: PF_ERR_INVALID (NULL u / q, negative iterations), PF_ERR_UNSUPPORTED (explicit-flow ALM,
  * whose state also holds p and p_S). */
-pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t iterations);
+pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t iterations, int32_t u_is_log2);
 
 /* Change the step constants c (entropic proximal weight, Eq. 7 / P:119) and tau (flow step)
  * between calls, e.g. for a c-annealing schedule; the state is kept.  Errors:

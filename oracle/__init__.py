@@ -40,8 +40,8 @@ def build(force: bool = False) -> str:
     """Compile pf_oracle.c with plain IEEE semantics (no fast-math, no contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared",
-                               "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fno-fast-math", "-ffp-contract=off", "-fopenmp", "-fPIC",
+                               "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -66,10 +66,18 @@ def _load():
         lib.oracle_grad.argtypes = [i32, i64, i64, i64, dp, i32, dp]
         lib.oracle_div.restype = i32
         lib.oracle_div.argtypes = [i32, i64, i64, i64, dp, dp]
+        lib.oracle_set_threads.restype = None
+        lib.oracle_set_threads.argtypes = [i32]
         lib.oracle_project.restype = i32
         lib.oracle_project.argtypes = [i32, i64, i64, i64, dp, dp, i32]
         _lib = lib
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Threads for the oracle's whole-field passes (default 1, the plain single-threaded oracle).  Every pass
+    is a per-voxel pure function, so the results are bit-identical for any n (tests/test_oracle_pins.py)."""
+    _load().oracle_set_threads(int(n))
 
 
 def _dp(a: np.ndarray):

@@ -6,8 +6,13 @@
  * product path (paper_1501_07844_b200/) never includes, links or calls it, and
  * it shares no header, helper or constant with the CUDA code.
  *
- * Plain, slow, obviously-correct: fp64, single thread, one whole-field pass per
- * line of the paper's listings, in the listings' order and notation.
+ * Plain, slow, obviously-correct: fp64, one whole-field pass per line of the
+ * paper's listings, in the listings' order and notation.  Single-threaded by
+ * default; oracle_set_threads(n) splits every whole-field pass over n OpenMP
+ * threads by voxel range.  Every pass is a per-voxel pure function (it writes
+ * only voxel i of its output, from inputs no pass of the same loop writes), so
+ * the result is bit-identical for any thread count; the
+ * first-failing-voxel scans stay serial.
  *   oracle_potts    -- Algorithm 1
  *   oracle_dag      -- Algorithm 2, d_L recursion P:190-197
  *   oracle_ishikawa -- Algorithm 3
@@ -33,16 +38,32 @@
  * finite), -1000000000000 on bad arguments.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
 #define BAD_ARGS (-1000000000000LL)
 
+static int g_threads = 1;
+
+/* Threads for the whole-field passes (1 = the plain single-threaded oracle); results do not depend on it. */
+void oracle_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+
+#define PFOR _Pragma("omp parallel for schedule(static) num_threads(g_threads)")
+
 typedef struct {
     int ndim;
     int64_t nx, ny, nz;
 } odims;
+
+/* -1 - (first voxel with a(x) <= 0 or not finite), or 0: a serial scan, so the reported
+ * voxel does not depend on the thread count */
+static int64_t first_bad(const double *a, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+        if (!(a[i] > 0.0) || !isfinite(a[i])) return -1 - i;
+    return 0;
+}
 
 static int64_t vol(const odims *d) { return d->nx * d->ny * d->nz; }
 
@@ -57,6 +78,7 @@ static int64_t axis_coord(const odims *d, int64_t i, int k) {
 /* (nabla f)^k(x) = f(x+e_k) - f(x), 0 at the last index along k (reading R4). */
 static void grad_axis(const odims *d, const double *f, int k, double *g) {
     const int64_t n = vol(d), s = axis_stride(d, k), len = axis_len(d, k);
+    PFOR
     for (int64_t i = 0; i < n; ++i)
         g[i] = (axis_coord(d, i, k) < len - 1) ? f[i + s] - f[i] : 0.0;
 }
@@ -64,10 +86,12 @@ static void grad_axis(const odims *d, const double *f, int k, double *g) {
 /* div q (x) = sum_k q^k(x) - q^k(x-e_k), with q^k(-1) = 0 (reading R4). */
 static void divergence(const odims *d, const double *q /* [ndim][V] */, double *out) {
     const int64_t n = vol(d);
+    PFOR
     for (int64_t i = 0; i < n; ++i) out[i] = 0.0;
     for (int k = 0; k < d->ndim; ++k) {
         const double *qk = q + (int64_t)k * n;
         const int64_t s = axis_stride(d, k);
+        PFOR
         for (int64_t i = 0; i < n; ++i)
             out[i] += qk[i] - (axis_coord(d, i, k) > 0 ? qk[i - s] : 0.0);
     }
@@ -76,6 +100,7 @@ static void divergence(const odims *d, const double *q /* [ndim][V] */, double *
 /* Proj_{|q(x)| <= S(x)} (readings R5, R14). */
 static void project(const odims *d, double *q /* [ndim][V] */, const double *S, int cap) {
     const int64_t n = vol(d);
+    PFOR
     for (int64_t i = 0; i < n; ++i) {
         if (cap == 0) {
             double nrm2 = 0.0;
@@ -102,6 +127,7 @@ static void flow_step(const odims *d, double *q, const double *f, const double *
     for (int k = 0; k < d->ndim; ++k) {
         grad_axis(d, f, k, tmp);
         double *qk = q + (int64_t)k * n;
+        PFOR
         for (int64_t i = 0; i < n; ++i) qk[i] = qk[i] - ctau * tmp[i];
     }
     project(d, q, S, cap);
@@ -136,28 +162,33 @@ int64_t oracle_potts(int ndim, int64_t nx, int64_t ny, int64_t nz, int K, const 
         /* line 147 */
         for (int L = 0; L < K; ++L) {
             divergence(&d, q + (int64_t)L * ndim * n, arg + (int64_t)L * n);
+            PFOR
             for (int64_t i = 0; i < n; ++i) arg[(int64_t)L * n + i] = D[(int64_t)L * n + i] + arg[(int64_t)L * n + i];
         }
+        PFOR
         for (int64_t i = 0; i < n; ++i) {
             double mm = arg[i];
             for (int L = 1; L < K; ++L) mm = fmin(mm, arg[(int64_t)L * n + i]);
             m[i] = (shift == 0) ? mm : 0.0;
         }
         for (int L = 0; L < K; ++L)
+            PFOR
             for (int64_t i = 0; i < n; ++i)
                 u[(int64_t)L * n + i] = u[(int64_t)L * n + i] * exp(-(arg[(int64_t)L * n + i] - m[i]) / c);
         /* line 148 */
         for (int L = 0; L < K; ++L)
             flow_step(&d, q + (int64_t)L * ndim * n, u + (int64_t)L * n, S + (int64_t)L * n, c * tau, cap, tmp);
         /* line 149 */
+        PFOR
         for (int64_t i = 0; i < n; ++i) {
             a[i] = 0.0;
             for (int L = 0; L < K; ++L) a[i] += u[(int64_t)L * n + i];
-            if (!(a[i] > 0.0) || !isfinite(a[i])) { status = -1 - i; break; }
         }
+        status = first_bad(a, n);
         /* line 150 */
         if (status == 0)
             for (int L = 0; L < K; ++L)
+                PFOR
                 for (int64_t i = 0; i < n; ++i) {
                     u[(int64_t)L * n + i] = u[(int64_t)L * n + i] / a[i];
                     if (u[(int64_t)L * n + i] < u_floor) u[(int64_t)L * n + i] = 0.0; /* R18 */
@@ -236,20 +267,24 @@ int64_t oracle_dag(int ndim, int64_t nx, int64_t ny, int64_t nz, int nn, int ne,
     int64_t status = 0;
     for (int it = 0; it < niter && status == 0; ++it) {
         /* P:282  forall L: d_L <- div q_L   (d_S = 0, S has no flow) */
+        PFOR
         for (int64_t i = 0; i < n; ++i) DROW(0)[i] = 0.0;
         for (int v = 1; v < nn; ++v) divergence(&d, QOF(v), DROW(v));
         /* P:283  forall L in end labels: d_L <- d_L + D_L */
         for (int v = 1; v < nn; ++v)
             if (g.is_leaf[v])
+                PFOR
                 for (int64_t i = 0; i < n; ++i) DROW(v)[i] = DROW(v)[i] + DOF(v)[i];
         /* P:284-288  for L in O\{S}: for L' in L.C: d_L' <- d_L' + w_(L,L') d_L */
         for (int k = 1; k < nn; ++k) {
             int L = g.order[k];
             for (int e = 0; e < ne; ++e)
                 if (par[e] == L)
+                    PFOR
                     for (int64_t i = 0; i < n; ++i) DROW(chi[e])[i] = DROW(chi[e])[i] + w[e] * DROW(L)[i];
         }
         /* P:290  forall L in end labels: u_L <- u_L exp(-d_L / c)   [R1: minus m(x)] */
+        PFOR
         for (int64_t i = 0; i < n; ++i) {
             double mm = INFINITY;
             for (int v = 1; v < nn; ++v)
@@ -258,21 +293,24 @@ int64_t oracle_dag(int ndim, int64_t nx, int64_t ny, int64_t nz, int nn, int ne,
         }
         for (int v = 1; v < nn; ++v)
             if (g.is_leaf[v])
+                PFOR
                 for (int64_t i = 0; i < n; ++i) UOF(v)[i] = UOF(v)[i] * exp(-(DROW(v)[i] - m[i]) / c);
         /* P:291  forall L in end labels: d_L <- u_L */
         for (int v = 1; v < nn; ++v)
             if (g.is_leaf[v]) memcpy(DROW(v), UOF(v), sizeof(double) * n);
         /* P:292  a <- sum over end labels of u_L */
+        PFOR
         for (int64_t i = 0; i < n; ++i) {
             a[i] = 0.0;
             for (int v = 1; v < nn; ++v)
                 if (g.is_leaf[v]) a[i] += UOF(v)[i];
-            if (!(a[i] > 0.0) || !isfinite(a[i])) { status = -1 - i; break; }
         }
+        status = first_bad(a, n);
         if (status != 0) break;
         /* P:293  u_L <- u_L / a */
         for (int v = 1; v < nn; ++v)
             if (g.is_leaf[v])
+                PFOR
                 for (int64_t i = 0; i < n; ++i) {
                     UOF(v)[i] = UOF(v)[i] / a[i];
                     if (UOF(v)[i] < u_floor) UOF(v)[i] = 0.0; /* R18 */
@@ -280,6 +318,7 @@ int64_t oracle_dag(int ndim, int64_t nx, int64_t ny, int64_t nz, int nn, int ne,
         /* P:295  forall L not in end labels: d_L <- 0 */
         for (int v = 0; v < nn; ++v)
             if (!g.is_leaf[v])
+                PFOR
                 for (int64_t i = 0; i < n; ++i) DROW(v)[i] = 0.0;
         /* P:296-302  for L in O^-1\{S}: q_L <- Proj(q_L - c tau nabla d_L);
                       for L' in L.P\{S}: d_L' <- d_L' + w_(L',L) d_L */
@@ -288,6 +327,7 @@ int64_t oracle_dag(int ndim, int64_t nx, int64_t ny, int64_t nz, int nn, int ne,
             flow_step(&d, QOF(L), DROW(L), SOF(L), c * tau, cap, tmp);
             for (int e = 0; e < ne; ++e)
                 if (chi[e] == L && par[e] != 0)
+                    PFOR
                     for (int64_t i = 0; i < n; ++i) DROW(par[e])[i] = DROW(par[e])[i] + w[e] * DROW(L)[i];
         }
     }
@@ -361,33 +401,41 @@ int64_t oracle_ishikawa(int ndim, int64_t nx, int64_t ny, int64_t nz, int N, con
 #define QI(i) (q + (int64_t)((i) - 1) * ndim * n)
     int64_t status = 0;
     for (int it = 0; it < niter && status == 0; ++it) {
+        PFOR
         for (int64_t x = 0; x < n; ++x) DI(0)[x] = 0.0;                          /* P:318 */
         for (int i = 1; i <= N; ++i) {                                            /* P:319-321 */
             divergence(&d, QI(i), tmp);
+            PFOR
             for (int64_t x = 0; x < n; ++x) DI(i)[x] = DI(i - 1)[x] + tmp[x];
         }
         for (int i = 0; i <= N; ++i)                                              /* P:322 */
+            PFOR
             for (int64_t x = 0; x < n; ++x) DI(i)[x] = DI(i)[x] + D[(int64_t)i * n + x];
+        PFOR
         for (int64_t x = 0; x < n; ++x) {                                         /* P:324 */
             double mm = DI(0)[x];
             for (int i = 1; i <= N; ++i) mm = fmin(mm, DI(i)[x]);
             m[x] = (shift == 0) ? mm : 0.0;
         }
         for (int i = 0; i <= N; ++i)
+            PFOR
             for (int64_t x = 0; x < n; ++x) UI(i)[x] = UI(i)[x] * exp(-(DI(i)[x] - m[x]) / c);
         for (int i = 0; i <= N; ++i) memcpy(DI(i), UI(i), sizeof(double) * n);    /* P:325 */
+        PFOR
         for (int64_t x = 0; x < n; ++x) {                                         /* P:326 */
             a[x] = 0.0;
             for (int i = 0; i <= N; ++i) a[x] += UI(i)[x];
-            if (!(a[x] > 0.0) || !isfinite(a[x])) { status = -1 - x; break; }
         }
+        status = first_bad(a, n);
         if (status != 0) break;
         for (int i = 0; i <= N; ++i)                                              /* P:327 */
+            PFOR
             for (int64_t x = 0; x < n; ++x) {
                 UI(i)[x] = UI(i)[x] / a[x];
                 if (UI(i)[x] < u_floor) UI(i)[x] = 0.0;
             }
         for (int i = N - 1; i >= 1; --i)                                          /* P:329-331 */
+            PFOR
             for (int64_t x = 0; x < n; ++x) DI(i)[x] = DI(i)[x] + DI(i + 1)[x];
         for (int i = 1; i <= N; ++i)                                              /* P:332 */
             flow_step(&d, QI(i), DI(i), S + (int64_t)(i - 1) * n, c * tau, cap, tmp);

@@ -35,7 +35,7 @@ _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_C
            6: "PF_ERR_NUMERIC", 7: "PF_ERR_STATE"}
 
 EXPORTED = ["pf_create", "pf_reset", "pf_set_step", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling",
-            "pf_link_slabs", "pf_iterate_linked", "pf_ipc_export", "pf_ipc_link", "pf_ipc_step", "pf_get_labeling", "pf_get_flows", "pf_set_state", "pf_get_energy",
+            "pf_link_slabs", "pf_iterate_linked", "pf_ipc_export", "pf_ipc_link", "pf_ipc_step", "pf_get_labeling", "pf_get_flows", "pf_get_state", "pf_set_state", "pf_get_energy",
             "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
@@ -100,7 +100,8 @@ _sig = {
     "pf_run": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_float, _P(ctypes.c_int32), _P(ctypes.c_float)]),
     "pf_get_labeling": (ctypes.c_int, [_vp, _vp, _vp]),
     "pf_get_flows": (ctypes.c_int, [_vp, _vp]),
-    "pf_set_state": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64]),
+    "pf_get_state": (ctypes.c_int, [_vp, _vp, _vp]),
+    "pf_set_state": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int32]),
     "pf_get_node_labeling": (ctypes.c_int, [_vp, ctypes.c_int32, _vp]),
     "pf_get_energy": (ctypes.c_int, [_vp, _P(ctypes.c_double), _P(ctypes.c_double)]),
     "pf_iterations": (ctypes.c_int, [_vp, _P(ctypes.c_int64)]),
@@ -136,15 +137,35 @@ def _check(st: int):
         raise PFError(st, _lib.pf_last_error().decode())
 
 
-def _ptr(a) -> int:
-    """Raw address of a numpy array (host) or torch tensor (host or CUDA); must be C-contiguous."""
+def _ptr(a, dtype=None, numel: Optional[int] = None, what: str = "array") -> int:
+    """Raw address of a C-contiguous numpy array (host) or torch tensor (host or CUDA), validated: the
+    library reads / writes exactly `numel` elements of `dtype` there, so a wrong dtype, size or layout is
+    a ValueError here instead of silently wrong data or an out-of-bounds write in the library."""
     if isinstance(a, np.ndarray):
-        assert a.flags.c_contiguous, "arrays must be C-contiguous"
+        if not a.flags.c_contiguous:
+            raise ValueError(f"{what}: numpy arrays must be C-contiguous")
+        if dtype is not None and a.dtype != np.dtype(dtype):
+            raise ValueError(f"{what}: dtype {a.dtype}, expected {np.dtype(dtype)}")
+        if numel is not None and a.size != numel:
+            raise ValueError(f"{what}: {a.size} elements, expected {numel}")
         return a.ctypes.data
     if hasattr(a, "data_ptr"):
-        assert a.is_contiguous(), "tensors must be contiguous"
+        if not a.is_contiguous():
+            raise ValueError(f"{what}: tensors must be contiguous")
+        if dtype is not None:
+            import torch
+            want = {np.dtype(np.float32): torch.float32, np.dtype(np.uint8): torch.uint8}[np.dtype(dtype)]
+            if a.dtype != want:
+                raise ValueError(f"{what}: dtype {a.dtype}, expected {want}")
+        if numel is not None and a.numel() != numel:
+            raise ValueError(f"{what}: {a.numel()} elements, expected {numel}")
         return a.data_ptr()
-    raise TypeError(type(a))
+    raise TypeError(f"{what}: {type(a)} is neither a numpy array nor a tensor")
+
+
+# geometry per handle, registered by pf_create (V_local, NL, num_nodes, ndim): the sizes the validated
+# output / state pointers must have
+_GEOM = {}
 
 
 def pf_version() -> str:
@@ -169,7 +190,9 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
     g = pf_graph(int(num_nodes), len(par),
                  par.ctypes.data_as(_P(ctypes.c_int32)), chi.ctypes.data_as(_P(ctypes.c_int32)),
                  w.ctypes.data_as(_P(ctypes.c_float)))
-    Dp = (ctypes.c_void_p * len(D))(*[_ptr(x) for x in D])
+    z0, z1 = (0, nz) if slab is None else (int(slab[0]), int(slab[1]))
+    nD = nx * ny * (min(z1 + 1, nz) - z0)
+    Dp = (ctypes.c_void_p * len(D))(*[_ptr(x, np.float32, nD, f"D[{i}]") for i, x in enumerate(D)])
     keep = [par, chi, w, Dp]
     sc = None
     fp = None
@@ -177,7 +200,8 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
         sc = np.ascontiguousarray(s_scalars, dtype=np.float32)
         keep.append(sc)
     if s_fields is not None:
-        fp = (ctypes.c_void_p * len(s_fields))(*[_ptr(x) for x in s_fields])
+        fp = (ctypes.c_void_p * len(s_fields))(*[_ptr(x, np.float32, nx * ny * (z1 - z0), f"S field {i}")
+                                                 for i, x in enumerate(s_fields)])
         keep.append(fp)
     sm = pf_smoothness(s_kind, sc.ctypes.data_as(_P(ctypes.c_float)) if sc is not None else None,
                        ctypes.cast(fp, _P(ctypes.c_void_p)) if fp is not None else None)
@@ -186,6 +210,7 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
     out = ctypes.c_void_p()
     _check(_lib.pf_create(ctypes.byref(d), ctypes.byref(g), ctypes.cast(Dp, _P(ctypes.c_void_p)), ctypes.byref(sm),
                           ctypes.byref(cfg), ctypes.byref(sl) if sl is not None else None, ctypes.byref(out)))
+    _GEOM[out.value] = (nx * ny * (z1 - z0), len(D), int(num_nodes), int(ndim))
     return out.value
 
 
@@ -217,20 +242,38 @@ def pf_iterate_phase(s: int, phase: int, want_residual: bool = False) -> Optiona
     return float(r.value) if want_residual else None
 
 
+def _sizes(s: int):
+    V, NL, nn, nd = _GEOM[s]
+    return V, NL, (nn - 1) * nd * V
+
+
 def pf_get_labeling(s: int, u=None, argmax=None):
-    _check(_lib.pf_get_labeling(s, _ptr(u) if u is not None else None, _ptr(argmax) if argmax is not None else None))
+    V, NL, _ = _sizes(s)
+    _check(_lib.pf_get_labeling(s, _ptr(u, np.float32, NL * V, "u") if u is not None else None,
+                                _ptr(argmax, np.uint8, V, "argmax") if argmax is not None else None))
 
 
 def pf_get_flows(s: int, q):
-    _check(_lib.pf_get_flows(s, _ptr(q)))
+    _check(_lib.pf_get_flows(s, _ptr(q, np.float32, _sizes(s)[2], "q")))
 
 
-def pf_set_state(s: int, u, q, iterations: int):
-    _check(_lib.pf_set_state(s, None if u is None else _ptr(u), None if q is None else _ptr(q), int(iterations)))
+def pf_get_state(s: int, u_log2=None, q=None):
+    """The exact resumable state: lambda = log2 u [NL][z][y][x] and q (see pf.h)."""
+    V, NL, nq = _sizes(s)
+    _check(_lib.pf_get_state(s, _ptr(u_log2, np.float32, NL * V, "u_log2") if u_log2 is not None else None,
+                             _ptr(q, np.float32, nq, "q") if q is not None else None))
+
+
+def pf_set_state(s: int, u, q, iterations: int, u_is_log2: bool = True):
+    """u: lambda = log2 u as pf_get_state returns it (u_is_log2) or the labeling u itself."""
+    V, NL, nq = _sizes(s)
+    _check(_lib.pf_set_state(s, None if u is None else _ptr(u, np.float32, NL * V, "u"),
+                             None if q is None else _ptr(q, np.float32, nq, "q"), int(iterations),
+                             1 if u_is_log2 else 0))
 
 
 def pf_get_node_labeling(s: int, node: int, out):
-    _check(_lib.pf_get_node_labeling(s, int(node), _ptr(out)))
+    _check(_lib.pf_get_node_labeling(s, int(node), _ptr(out, np.float32, _sizes(s)[0], "u_node")))
 
 
 def pf_get_energy(s: int):
@@ -299,6 +342,7 @@ def pf_get_kernel_info(s: int) -> dict:
 
 
 def pf_destroy(s: int):
+    _GEOM.pop(s, None)
     _lib.pf_destroy(s)
 
 

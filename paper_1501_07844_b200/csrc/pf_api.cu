@@ -158,8 +158,10 @@ pf_status init_state(pf_solver *s) {
         s->iters = 0;
         return PF_OK;
     }
+    // u_L = 1/|L|, stored as lambda = log2 u (reading R18)
+    const float lam0 = (float)(-std::log2((double)s->gc.NL));
     for (int i = 0; i < 2; ++i) {
-        CK(launch_fill(s->u_alloc[i], nu, 1.0f / (float)s->gc.NL, s->stream), "init u");
+        CK(launch_fill(s->u_alloc[i], nu, lam0, s->stream), "init u");
         s->launches++;
         CK(cudaMemsetAsync(s->q_alloc[i], 0, nq * sizeof(float), s->stream), "init q");
     }
@@ -583,12 +585,13 @@ pf_status pf_reset(pf_solver *s) {
     return PF_OK;
 }
 
-pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t iterations) {
+pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t iterations, int32_t u_is_log2) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
     if (s->alm) return fail(PF_ERR_UNSUPPORTED, "set_state: the explicit-flow ALM state also holds p, p_S");
     if (!u || !q) return fail(PF_ERR_INVALID, "set_state: u and q are required");
     if (iterations < 0) return fail(PF_ERR_INVALID, "set_state: iterations must be >= 0");
+    if (u_is_log2 != 0 && u_is_log2 != 1) return fail(PF_ERR_INVALID, "set_state: u_is_log2 must be 0 or 1");
     DeviceGuard dg(s->device);
     const int NL = s->gc.NL, NV = s->gc.NV, NF = s->gc.NF, nd = s->ndim;
     const int64_t P = s->P, nzl = s->nzl;
@@ -603,6 +606,10 @@ pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t ite
         CK(copy_volume(true, s->u[s->cur] + l * P, NL, const_cast<float *>(u) + l * V, s->nx, s->ny, s->pitch, nzl,
                        s->stream),
            "upload u");
+    if (!u_is_log2) {   // the labeling itself: lambda = log2 u in place over the owned planes
+        CK(launch_log2_inplace(s->u[s->cur], nzl * NL * P, s->stream), "log2 u");
+        s->launches++;
+    }
     for (int p = 0; p < NF && p < NV; ++p) {   // nodes without a stored flow (Ishikawa end labels): not read
         const int v = s->gc.node_of_pos[p];
         for (int k = 0; k < nd; ++k)
@@ -926,17 +933,27 @@ pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {
     const int NL = s->gc.NL;
     const int64_t P = s->P, nzl = s->nzl;
     const int64_t V = s->nx * s->ny * nzl;
-    if (u) {
-        for (int l = 0; l < NL; ++l)
-            CK(copy_volume(false, s->u[s->cur] + l * P, NL, u + l * V, s->nx, s->ny, s->pitch, nzl, s->stream),
+    const int ulog = s->alm ? 0 : 1;
+    if (u && V > 0) {   // u = 2^lambda into a dense [l][z][y][x] volume (stream-ordered scratch for host outputs)
+        const bool dev = is_device_ptr(u);
+        float *dst = u;
+        if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V * NL * sizeof(float), s->stream), "u scratch");
+        CK(launch_export_u(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, ulog, s->stream),
+           "export u");
+        s->launches++;
+        if (!dev) {
+            CK(cudaMemcpyAsync(u, dst, (size_t)V * NL * sizeof(float), cudaMemcpyDeviceToHost, s->stream),
                "download u");
+            cudaFreeAsync(dst, s->stream);
+        }
     }
     if (argmax) {
         const bool dev = is_device_ptr(argmax);
         uint8_t *dst = argmax;
         // stream-ordered scratch from the (retained) pool: cudaMalloc / cudaFree would synchronize the device
         if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V, s->stream), "argmax scratch");
-        CK(launch_argmax(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, s->stream), "argmax kernel");
+        CK(launch_argmax(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, ulog, s->stream),
+           "argmax kernel");
         s->launches++;
         if (!dev) {
             CK(cudaMemcpyAsync(argmax, dst, (size_t)V, cudaMemcpyDeviceToHost, s->stream), "download argmax");
@@ -962,7 +979,8 @@ pf_status pf_get_node_labeling(pf_solver *s, int32_t node, float *u_node) {
     const bool dev = is_device_ptr(u_node);
     float *dst = u_node;
     if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V * sizeof(float), s->stream), "node labeling scratch");
-    CK(launch_node_labeling(s->u[s->cur], dst, w, NL, (int)s->nx, (int)s->ny, (int)s->pitch, s->nzl, s->stream),
+    CK(launch_node_labeling(s->u[s->cur], dst, w, NL, (int)s->nx, (int)s->ny, (int)s->pitch, s->nzl, s->alm ? 0 : 1,
+                            s->stream),
        "node labeling kernel");
     s->launches++;
     if (!dev) {
@@ -970,6 +988,23 @@ pf_status pf_get_node_labeling(pf_solver *s, int32_t node, float *u_node) {
         CK(cudaStreamSynchronize(s->stream), "sync");
         cudaFreeAsync(dst, s->stream);
     }
+    return check_numeric(s);
+}
+
+pf_status pf_get_state(pf_solver *s, float *u_log2, float *q) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (s->alm) return fail(PF_ERR_UNSUPPORTED, "get_state: the explicit-flow ALM state also holds p, p_S");
+    DeviceGuard dg(s->device);
+    const int NL = s->gc.NL;
+    const int64_t P = s->P, nzl = s->nzl;
+    const int64_t V = s->nx * s->ny * nzl;
+    if (u_log2)
+        for (int l = 0; l < NL; ++l)
+            CK(copy_volume(false, s->u[s->cur] + l * P, NL, u_log2 + l * V, s->nx, s->ny, s->pitch, nzl, s->stream),
+               "download lambda");
+    if (q) return pf_get_flows(s, q);
+    CK(cudaStreamSynchronize(s->stream), "sync");
     return check_numeric(s);
 }
 
@@ -1007,6 +1042,7 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
     EnergyArgs a;
     memset(&a, 0, sizeof(a));
     a.u = s->u[s->cur];
+    a.ulog = s->alm ? 0 : 1;
     a.q = s->q[s->cur];
     a.D = s->Dptr();
     a.d_bf16 = s->D16 ? 1 : 0;

@@ -12,19 +12,24 @@ __global__ void fill_kernel(float *p, int64_t n, float v) {
         p[i] = v;
 }
 
-// argmax over end labels, lowest label id wins ties ("thresholded").
+// The labeling value of a stored u entry: the pseudo-flow state holds lambda = log2 u (ulog = 1, reading R18),
+// the explicit-flow ALM arm holds u itself (ulog = 0).
+__device__ __forceinline__ float u_value(float v, int ulog) { return ulog ? u_of_log2(v) : v; }
+
+// argmax over end labels, lowest label id wins ties ("thresholded"); compared on the same
+// u values pf_get_labeling exports.
 __global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__ out, int NL, int nx, int ny,
-                              int pitch, int64_t nz) {
+                              int pitch, int64_t nz, int ulog) {
     const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = i / ((int64_t)nx * ny);
         const int r = (int)(i - z * (int64_t)nx * ny);
         const int y = r / nx, x = r - y * nx;
         const float *b = u + z * NL * P + (int64_t)y * pitch + x;
-        float best = b[0];
+        float best = u_value(b[0], ulog);
         int arg = 0;
         for (int l = 1; l < NL; ++l) {
-            const float v = b[l * P];
+            const float v = u_value(b[l * P], ulog);
             if (v > best) { best = v; arg = l; }
         }
         out[i] = (uint8_t)arg;
@@ -34,7 +39,7 @@ __global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__
 // Labeling of any node: u_v(x) = sum_B W_(v,B) u_B(x) over the end labels B (path weights P:199-209),
 // written densely as [z][y][x] (x fastest).
 __global__ void node_labeling_kernel(const float *__restrict__ u, float *__restrict__ out, NodeWeights w, int NL,
-                                     int nx, int ny, int pitch, int64_t nz) {
+                                     int nx, int ny, int pitch, int64_t nz, int ulog) {
     const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = i / ((int64_t)nx * ny);
@@ -43,7 +48,7 @@ __global__ void node_labeling_kernel(const float *__restrict__ u, float *__restr
         const float *b = u + z * NL * P + (int64_t)y * pitch + x;
         float acc = 0.f;
         for (int l = 0; l < NL; ++l)
-            if (w.W[l] != 0.f) acc = fmaf(w.W[l], b[l * P], acc);
+            if (w.W[l] != 0.f) acc = fmaf(w.W[l], u_value(b[l * P], ulog), acc);
         out[i] = acc;
     }
 }
@@ -70,7 +75,7 @@ __device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, 
     // u_v for every position: end labels read, internal by bottom-up sums (Eq. 9);
     // Ishikawa chain: u_{N_i} = sum_{j >= i} u_{L_j}
     const int NV = a.NV, NI = a.NI;
-    for (int l = 0; l < a.NL; ++l) out[NI + l] = ub[l * P];
+    for (int l = 0; l < a.NL; ++l) out[NI + l] = u_value(ub[l * P], a.ulog);
     if (a.model == 1) {
         double acc = 0.0;
         for (int f = NI - 1; f >= 0; --f) {
@@ -84,6 +89,26 @@ __device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, 
         for (int j = i + 1; j < NV; ++j) acc += (double)a.g.w[i][j] * out[j];
         out[i] = (float)acc;
     }
+}
+
+// Export of the labeling (pf_get_labeling): internal [z][l][y][pitch] (log2 u or u) -> dense [l][z][y][x] u.
+__global__ void export_u_kernel(const float *__restrict__ u, float *__restrict__ out, int NL, int nx, int ny,
+                                int pitch, int64_t nz, int ulog) {
+    const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / ((int64_t)nx * ny);
+        const int r = (int)(i - z * (int64_t)nx * ny);
+        const int y = r / nx, x = r - y * nx;
+        const float *b = u + z * NL * P + (int64_t)y * pitch + x;
+        for (int l = 0; l < NL; ++l) out[l * V + i] = u_value(b[l * P], ulog);
+    }
+}
+
+// pf_set_state with a linear u: lambda = log2 u in place over n internal values (correctly rounded log2f;
+// u = 0 gives -inf, a label that is exactly dead)
+__global__ void log2_inplace_kernel(float *p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = log2f(p[i]);
 }
 
 __global__ void f32_to_bf16_kernel(const float *__restrict__ src, uint16_t *__restrict__ dst, int64_t n) {
@@ -181,9 +206,20 @@ cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz,
+cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz, int ulog,
                           cudaStream_t st) {
-    argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz);
+    argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz, ulog);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export_u(const float *u, float *out, int NL, int nx, int ny, int pitch, int64_t nz, int ulog,
+                            cudaStream_t st) {
+    export_u_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz, ulog);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_log2_inplace(float *p, int64_t n, cudaStream_t st) {
+    log2_inplace_kernel<<<1184, 256, 0, st>>>(p, n);
     return cudaGetLastError();
 }
 
@@ -193,8 +229,8 @@ cudaError_t launch_f32_to_bf16(const float *src, uint16_t *dst, int64_t n, cudaS
 }
 
 cudaError_t launch_node_labeling(const float *u, float *out, const NodeWeights &w, int NL, int nx, int ny, int pitch,
-                                 int64_t nz, cudaStream_t st) {
-    node_labeling_kernel<<<1184, 256, 0, st>>>(u, out, w, NL, nx, ny, pitch, nz);
+                                 int64_t nz, int ulog, cudaStream_t st) {
+    node_labeling_kernel<<<1184, 256, 0, st>>>(u, out, w, NL, nx, ny, pitch, nz, ulog);
     return cudaGetLastError();
 }
 

@@ -6,11 +6,11 @@
 // stages, updates and stores only the labels [r K/2, (r+1) K/2), i.e. each SM does the work of a K/2-label
 // problem on a TY = 8 tile.  The Potts label update couples the labels of a voxel only through
 //   m(x) = min_L d_L(x)   and   a(x) = sum_L u~_L(x)        (Eq. 7; reading R1)
-// so per plane each CTA writes its partial m and its partial a of every point of the tile (+halo) into the
-// partner's shared memory with st.async (DSMEM), each exchange completing a transaction-counted mbarrier
-// of the receiver (no cluster-wide barrier per plane).  The partial sums
-// are (quarter + quarter) per half and the total is half0 + half1: exactly label_update's order, so the
-// result is bitwise that of the one-CTA kernels.  Everything else -- the TMA z-march, the M ring, the
+// so per plane each CTA writes its half's shift m_h, maximum T_h and sum s_h (label_half, pf_math.cuh; u is
+// stored as lambda = log2 u) of every point of the tile (+halo) into the partner's shared memory with one
+// 16-byte st.async (DSMEM), each exchange completing a transaction-counted mbarrier of the receiver (no
+// cluster-wide barrier per plane).  Both CTAs then combine the two triples exactly as label_update's split
+// form does (label_halves_combine), so the result is bitwise that of the one-CTA kernels.  Everything else -- the TMA z-march, the M ring, the
 // flow step of plane p-1, the staged TMA stores, the ticket queue (one ticket per cluster) -- is the
 // staged kernel's (pf_staged.cuh), restricted to the CTA's labels.
 #pragma once
@@ -47,10 +47,10 @@ __device__ __forceinline__ void st_async_f32(uint32_t addr, float v, uint32_t mb
                  : "memory");
 }
 
-// the (m_h, a_h) pair of one point as ONE 8-byte st.async
-__device__ __forceinline__ void st_async_f32x2(uint32_t addr, float v0, float v1, uint32_t mbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr),
-                 "r"(__float_as_uint(v0)), "r"(__float_as_uint(v1)), "r"(mbar)
+// the (m_h, T_h, s_h) triple of one point as ONE 16-byte st.async (4th word unused)
+__device__ __forceinline__ void st_async_f32x4(uint32_t addr, float v0, float v1, float v2, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+                 "r"(__float_as_uint(v0)), "r"(__float_as_uint(v1)), "r"(__float_as_uint(v2)), "r"(0u), "r"(mbar)
                  : "memory");
 }
 
@@ -66,7 +66,7 @@ struct ClusterLayout {
     using L = StagedLayout<0, NLCP, TY, 1, 0, 1>;
     static constexpr int XPTS = round32((TY + 1) * 33);   // exchange slots: tile + halo points
     __host__ __device__ static constexpr int off_X(int s_ch) { return L::floats(s_ch); }
-    __host__ __device__ static constexpr int floats(int s_ch) { return off_X(s_ch) + 4 * XPTS; }   // (m, a) x 2
+    __host__ __device__ static constexpr int floats(int s_ch) { return off_X(s_ch) + 8 * XPTS; }   // (m, T, s, -) x 2
     __host__ __device__ static constexpr int bytes(int s_ch) { return floats(s_ch) * 4 + 32; }   // + 4 mbarriers
 };
 
@@ -89,9 +89,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     float *R = sm + L::off_R(a.s_ch);
     float *Uo = sm + L::off_Uo(a.s_ch);
     float *Qo = sm + L::off_Qo(a.s_ch);
-    // partner's (m_h, a_h) per point, written remotely; double-buffered by plane parity because the
+    // partner's (m_h, T_h, s_h) per point, written remotely; double-buffered by plane parity because the
     // partner may run up to one plane ahead (its sends for plane k+1 need only OUR sends for plane k)
-    float *X2 = sm + CL::off_X(a.s_ch);       // [parity][XPTS][(m_h, a_h)]
+    float *X2 = sm + CL::off_X(a.s_ch);       // [parity][XPTS][(m_h, T_h, s_h, -)]
     const int SSZ = L::ssz(a.s_ch);
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + CL::floats(a.s_ch));
 
@@ -111,10 +111,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     const int64_t qps = (int64_t)3 * NF * P;
     const float k2 = kLog2e * a.inv_c;
     const int xpt = ly * 33 + (lx < 0 ? 0 : lx);             // this point's exchange slot
-    const uint32_t x_remote = map_to_rank(X2 + 2 * xpt, other);
-    const uint32_t barx_remote = map_to_rank(&bars[2], other);   // partner's "(m_h, a_h) received" mbarriers
-    constexpr uint32_t kXBuf = 8u * CL::XPTS;                      // byte stride of the parity buffers
-    constexpr uint32_t kXBytes = 4u * (32 * TY + 32 + TY);        // one float per tile + halo point
+    const uint32_t x_remote = map_to_rank(X2 + 4 * xpt, other);
+    const uint32_t barx_remote = map_to_rank(&bars[2], other);   // partner's "(m_h, T_h, s_h) received" mbarriers
+    constexpr uint32_t kXBuf = 16u * CL::XPTS;                     // byte stride of the parity buffers
+    constexpr uint32_t kXBytes = 16u * (32 * TY + 32 + TY);       // one 16-byte triple per tile + halo point
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -232,9 +232,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
             const float *Ub = Us + st * L::USZ;
             const float *Db = Ds + st * L::USZ;
             float *Rp = R + (p % 3) * RING;
-            float dl[NLC], uold[NLC], ut[NLC];
-            // this CTA's half of the labels: local shift m_h, local masses, a_h = quarter + quarter
-            float mh = 0.f, sa = 0.f, sb = 0.f;
+            float dl[NLC], uold[NLC], ut[NLC], rr[NLC];   // uold: log2 state; ut: masses u~
+            // this CTA's half of the labels: (m_h, T_h, s_h) and r_L = t_L - T_h, e_L = 2^r_L (label_half)
+            float mh = 0.f, th = 0.f, sh = 1.f;
             if (lx >= 0) {
 #pragma unroll
                 for (int v = 0; v < NLC; ++v) {
@@ -252,55 +252,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                     dl[v] = Dv + dq;                        // Potts: d_L = D_L + div q_L
                     uold[v] = Ub[v * UCS + uoff];
                 }
-                if (a.shift == 0) {
-                    mh = dl[0];
-#pragma unroll
-                    for (int v = 1; v < NLC; ++v) mh = fminf(mh, dl[v]);
-                }
-#pragma unroll
-                for (int v = 0; v < NLC; ++v) {
-                    ut[v] = uold[v] * ex2_approx((mh - dl[v]) * k2);
-                    if (v < NLC / 2) sa += ut[v];
-                    else sb += ut[v];
-                }
+                label_half<NLC>(dl, uold, rr, ut, a.shift, k2, mh, th, sh);
             }
-            // ---- ONE exchange of (m_h, a_h) with the partner CTA (label_update's split form, pf_math.cuh)
+            // ---- ONE exchange of (m_h, T_h, s_h) with the partner CTA (label_update's split form, pf_math.cuh)
             const int xb = k & 1;   // exchange buffer / mbarrier of this plane; phase = (k >> 1) & 1
-            if (tid == 0) mbar_arrive_expect_tx(&bars[2 + xb], 2 * kXBytes);   // arm (bytes may already be in)
-            const float ah = sa + sb;
+            if (tid == 0) mbar_arrive_expect_tx(&bars[2 + xb], kXBytes);   // arm (bytes may already be in)
             if (lx >= 0) {
-                st_async_f32x2(x_remote + xb * kXBuf, mh, ah, barx_remote + xb * 8u);
+                st_async_f32x4(x_remote + xb * kXBuf, mh, th, sh, barx_remote + xb * 8u);
             }
             mbar_wait(&bars[2 + xb], (k >> 1) & 1);
             float sum = 1.f;
             if (lx >= 0) {
-                const float2 xo = reinterpret_cast<const float2 *>(X2)[xb * CL::XPTS + xpt];
-                const float mo = xo.x, ao = xo.y;
-                const float m0 = rank == 0 ? mh : mo, m1 = rank == 0 ? mo : mh;
-                const float a0 = rank == 0 ? ah : ao, a1 = rank == 0 ? ao : ah;
-                float f0 = 1.f, f1 = 1.f;
-                if (a.shift == 0) {
-                    const float m = fminf(m0, m1);
-                    f0 = ex2_approx((m - m0) * k2);
-                    f1 = ex2_approx((m - m1) * k2);
-                }
-                sum = halves_sum(a0, f0, a1, f1);
-                const float fo = rank == 0 ? f0 : f1;
+                const float4 xo = reinterpret_cast<const float4 *>(X2)[xb * CL::XPTS + xpt];
+                float ch, gh;
+                sum = rank == 0 ? label_halves_combine(mh, th, sh, xo.x, xo.y, xo.z, 0, a.shift, k2, ch, gh)
+                                : label_halves_combine(xo.x, xo.y, xo.z, mh, th, sh, 1, a.shift, k2, ch, gh);
 #pragma unroll
-                for (int v = 0; v < NLC; ++v) ut[v] *= fo;
-                const float inv = __frcp_rn(sum);
+                for (int v = 0; v < NLC; ++v) ut[v] *= gh;
                 if (p < zc1 && is_main && valid) {
-                    if (rank == 0 && (!(sum > 0.f) || !(sum <= FLT_MAX))) {
+                    if (rank == 0 && label_sum_bad(sum)) {
                         const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                         atomicMin(a.err_voxel, vox);
                     }
                     float *uo = Uo + (p & 1) * L::UOSZ + ly * 32 + lx;
 #pragma unroll
                     for (int v = 0; v < NLC; ++v) {
-                        const float nu = ut[v] * inv;
-                        const float un = nu < FLT_MIN ? 0.f : nu;
-                        uo[v * TY * 32] = un;
-                        if (a.check) resid = fmaxf(resid, fabsf(un - uold[v]));
+                        const float ln = rr[v] + ch;
+                        uo[v * TY * 32] = ln;
+                        if (a.check) resid = fmaxf(resid, fabsf(u_of_log2(ln) - u_of_log2(uold[v])));
                     }
                 }
 #pragma unroll

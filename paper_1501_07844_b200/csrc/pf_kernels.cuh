@@ -7,6 +7,7 @@
 //   a1  div q_v(x)          backward differences of the OLD flows
 //   a2  d_v = div q_v (+D_L), top-down pushes in O
 //   a3  u~_L = u_L exp(-(d_L - m)/c), a = sum u~, u' = u~/a          (R1)
+//       on the stored log2 state lambda = log2 u (label_update, pf_math.cuh; reading R18)
 //   a4  M_L = u~_L, bottom-up pushes in O^-1
 //   a5  q^ = q_v - c tau nabla M_v                                  (Eq. 8, Eq. 16)
 //   a6  q' = Proj_{|q| <= S_v}(q^)                                   (R5, R14)
@@ -24,7 +25,7 @@
 // have no children).
 //
 // Layouts (internal, per z-plane contiguous so a plane of every label is one
-// chunk for the halo exchange):  u, D: [z][l][y][x];  q: [z][k][v][y][x];
+// chunk for the halo exchange):  u (stored as log2 u), D: [z][l][y][x];  q: [z][k][v][y][x];
 // S field: [z][y][x] (shared) or [z][v][y][x] (per node).
 #pragma once
 #include <cstdint>
@@ -163,21 +164,19 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
             for (int l = 0; l < NL; ++l) Dv[l] = load_D(a.D, Db + l * P, a.d_bf16);
             label_excess<MODEL, NI, NL>(dq, Dv, d, a.g.w);
             const float *ub = a.u_in + (int64_t)p * ups + pix;
-            float uold[NL], ut[NL], un[NL];
+            float uold[NL], ut[NL], un[NL];   // log2 states (old / new), masses u~
 #pragma unroll
             for (int l = 0; l < NL; ++l) uold[l] = ldg(ub + l * P);
             const float sum = label_update<NI, NL>(d, uold, ut, un, a.shift, k2);
             if (is_main && p < zc1) {
-                if (!(sum > 0.f) || !(sum <= FLT_MAX)) {
+                if (label_sum_bad(sum)) {
                     const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                     atomicMin(a.err_voxel, vox);
                 }
                 float *uo = a.u_out + (int64_t)p * ups + pix;
 #pragma unroll
-                for (int l = 0; l < NL; ++l) {
-                    st_stream(uo + l * (int)P, un[l]);
-                    resid = fmaxf(resid, fabsf(un[l] - uold[l]));
-                }
+                for (int l = 0; l < NL; ++l) st_stream(uo + l * (int)P, un[l]);
+                if (a.check) resid = resid_log2<NL>(un, uold, resid);
             }
             float M[NV];
             node_masses<MODEL, NI, NL>(ut, M, a.g.w);

@@ -10,13 +10,25 @@ namespace pf {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
-// 2^x on the SFU (MUFU.EX2, max rel. error ~2^-22); subnormal results flush to 0, consistent with the
-// u floor below.
+// 2^x on the SFU (MUFU.EX2, max rel. error ~2^-22).  Results below 2^-126 flush to 0.  It is only applied
+// to TRANSIENT values -- the per-label factors e_L <= 1 whose sum s >= 1 absorbs anything below 2^-126, the
+// masses u~ and the exported labeling u = 2^lambda -- never to the stored state, which is lambda = log2 u
+// (reading R18): no stored label can underflow and die.
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+
+// log2(x) on the SFU (MUFU.LG2); only called on the label-update sum s in [1, 2K] (max abs. error ~2^-22).
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// The labeling u_L of a stored log2 value (exports, argmax, residual, energies).
+__device__ __forceinline__ float u_of_log2(float lam) { return ex2_approx(lam); }
 
 // 1/sqrt(x) on the SFU (MUFU.RSQ).  Only called on x in [1, 3] (the rescaled squared norm below), where
 // rsqrtf() would return the same value after a denormal-input guard that can never trigger.
@@ -45,82 +57,136 @@ __device__ __forceinline__ void st_stream(float *p, float v) {
     asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
-// Label update of one voxel (P:147-150 / P:290-293, Eq. 7 / Eq. 15; reading R1):
-//   m = min_L d_L (SHIFT_MIN) or 0;  u~_L = u_L exp(-(d_L - m)/c);  a = sum u~;  u'_L = u~_L / a,
-// with u' below the fp32 normal range flushed to 0 (reading R18: u is stored in fp32).
-// d[NI..NI+NL) holds the end-label excesses on entry; ut receives u~ (the unnormalised masses).
-// Returns a; writes u' to unew.
+// Label update of one voxel (P:147-150 / P:290-293, Eq. 7 / Eq. 15; reading R1) on the log2 state
+// lambda_L = log2 u_L (reading R18):
+//   m = min_L d_L (SHIFT_MIN) or 0;   u~_L = u_L exp(-(d_L - m)/c);   a = sum u~;   u'_L = u~_L / a
+// evaluated as
+//   t_L = lambda_L + (m - d_L) log2(e)/c  (= log2 u~_L),   T = max_L t_L,   r_L = t_L - T,   e_L = 2^r_L in (0, 1],
+//   s = sum_L e_L in [1, K],   lambda'_L = r_L - log2 s  (= log2 u'_L),   u~_L = e_L 2^T  (the masses M_L)
+// -- the same quantities (a = s 2^T), but the stored state is a logarithm, so no label underflows and dies in
+// fp32 (which made fp32 trajectories leave the exact iteration where a label decays below 2^-149 and later
+// revives; R18) and a is never formed as a number that could under- or overflow.
+// d[NI..NI+NL) holds the end-label excesses on entry; ut receives u~ (the unnormalised masses), lnew lambda'.
+// Returns s (>= 1; NaN / not finite flags a numerical collapse).
 //
-// Summation order: a = (q0 + q1) + (q2 + q3), q_i the sequential sum of the i-th quarter of the labels
-// (quarters = halves of halves).  With many labels (NL >= kHalfSplitNL) the two halves are shifted
-// separately and rescaled (the "online softmax" identity exp(-(d-m)/c) = exp(-(d-m_h)/c) exp(-(m_h-m)/c)):
-//   m_h = min over half h, u~^h_L = u_L exp(-(d_L - m_h)/c), a_h = quarter + quarter,
-//   f_h = exp(-(m_h - m)/c), a = a_1 f_1 + a_0 f_0 (one fma), u~_L = u~^h_L f_h,
-// which is the arithmetic of the label-split kernels (two warps or two CTAs per voxel row exchange only
-// (m_h, a_h), once), so every variant rounds identically.
+// Summation order: s = (q0 + q1) + (q2 + q3), q_i the sequential sum of the i-th quarter of the labels
+// (quarters = halves of halves).  With many labels (NL >= kHalfSplitNL) the two halves h are reduced
+// separately -- their own shift m_h, maximum T_h and sum s_h = quarter + quarter -- and combined from the
+// three numbers (m_h, T_h, s_h) of each half (label_halves_combine), which is the arithmetic of the
+// label-split kernels (two warps or two CTAs per voxel row exchange exactly those three numbers, once), so
+// every variant rounds identically.
 constexpr int kHalfSplitNL = 10;
 
 __device__ __forceinline__ float halves_sum(float a0, float f0, float a1, float f1) { return fmaf(a1, f1, a0 * f0); }
 
+// One half of the labels (N of them, starting at d / lold): shift m_h, r_L = t_L - T_h, e_L = 2^r_L,
+// s_h = (first N/2) + (rest).  Also the whole-label-set step when called with all labels (then m_h = m).
+template <int N>
+__device__ __forceinline__ void label_half(const float *d, const float *lold, float *r, float *e, int shift, float k2,
+                                           float &mh, float &Th, float &sh) {
+    mh = 0.f;
+    if (shift == 0) {
+        mh = d[0];
+#pragma unroll
+        for (int l = 1; l < N; ++l) mh = fminf(mh, d[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) r[l] = fmaf(mh - d[l], k2, lold[l]);   // t_L
+    // (floor -FLT_MAX: a half whose labels are all exactly dead, lambda = -inf, gives e = 0, s_h = 0 and
+    // lambda' = -inf instead of -inf - (-inf) = NaN)
+    Th = -FLT_MAX;
+#pragma unroll
+    for (int l = 0; l < N; ++l) Th = fmaxf(Th, r[l]);
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        r[l] = r[l] - Th;
+        e[l] = ex2_approx(r[l]);
+        if (l < N / 2) sa += e[l];
+        else sb += e[l];
+    }
+    sh = sa + sb;
+}
+
+// Combine the two halves' (m_h, T_h, s_h): with the common shift m = min(m_0, m_1) the half maxima are
+// G_h = T_h + (m - m_h) log2(e)/c, T = max G_h, s = s_0 2^(G_0 - T) + s_1 2^(G_1 - T).  For half `h` returns
+// lambda offset c_h = (G_h - T) - log2 s (lambda'_L = r_L + c_h) and mass scale g_h = 2^G_h (u~_L = e_L g_h);
+// the return value is s.
+__device__ __forceinline__ float label_halves_combine(float m0, float T0, float s0, float m1, float T1, float s1, int h,
+                                                      int shift, float k2, float &ch, float &gh) {
+    const float m = shift == 0 ? fminf(m0, m1) : 0.f;
+    const float G0 = fmaf(m - m0, k2, T0), G1 = fmaf(m - m1, k2, T1);
+    const float T = fmaxf(G0, G1);
+    const float s = halves_sum(s0, ex2_approx(G0 - T), s1, ex2_approx(G1 - T));
+    const float G = h == 0 ? G0 : G1;
+    ch = (G - T) - lg2_approx(s);
+    gh = ex2_approx(G);
+    return s;
+}
+
 template <int NI, int NL>
-__device__ __forceinline__ float label_update(const float (&d)[NI + NL], const float (&uold)[NL], float (&ut)[NL],
-                                              float (&unew)[NL], int shift, float k2 /* log2(e)/c */) {
-    constexpr int H = NL / 2, Q1 = H / 2, Q3 = H + (NL - H) / 2;
-    float sum;
+__device__ __forceinline__ float label_update(const float (&d)[NI + NL], const float (&lold)[NL], float (&ut)[NL],
+                                              float (&lnew)[NL], int shift, float k2 /* log2(e)/c */) {
+    float r[NL], e[NL];
     if constexpr (NL >= kHalfSplitNL) {
-        float m0 = 0.f, m1 = 0.f;
-        if (shift == 0) {
-            m0 = d[NI];
-#pragma unroll
-            for (int l = 1; l < H; ++l) m0 = fminf(m0, d[NI + l]);
-            m1 = d[NI + H];
-#pragma unroll
-            for (int l = H + 1; l < NL; ++l) m1 = fminf(m1, d[NI + l]);
-        }
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        constexpr int H = NL / 2;
+        float m0, T0, s0, m1, T1, s1;
+        label_half<H>(d + NI, lold, r, e, shift, k2, m0, T0, s0);
+        label_half<NL - H>(d + NI + H, lold + H, r + H, e + H, shift, k2, m1, T1, s1);
+        float c0, g0, c1, g1;
+        const float s = label_halves_combine(m0, T0, s0, m1, T1, s1, 0, shift, k2, c0, g0);
+        label_halves_combine(m0, T0, s0, m1, T1, s1, 1, shift, k2, c1, g1);
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
-            ut[l] = uold[l] * ex2_approx(((l < H ? m0 : m1) - d[NI + l]) * k2);
-            if (l < Q1) s0 += ut[l];
-            else if (l < H) s1 += ut[l];
-            else if (l < Q3) s2 += ut[l];
-            else s3 += ut[l];
+            lnew[l] = r[l] + (l < H ? c0 : c1);
+            ut[l] = e[l] * (l < H ? g0 : g1);
         }
-        float f0 = 1.f, f1 = 1.f;
-        if (shift == 0) {
-            const float m = fminf(m0, m1);
-            f0 = ex2_approx((m - m0) * k2);
-            f1 = ex2_approx((m - m1) * k2);
-        }
-        sum = halves_sum(s0 + s1, f0, s2 + s3, f1);
-#pragma unroll
-        for (int l = 0; l < NL; ++l) ut[l] *= (l < H ? f0 : f1);
+        return s;
     } else {
+        constexpr int H = NL / 2, Q1 = H / 2, Q3 = H + (NL - H) / 2;
         float m = 0.f;
         if (shift == 0) {
             m = d[NI];
 #pragma unroll
             for (int l = 1; l < NL; ++l) m = fminf(m, d[NI + l]);
         }
+#pragma unroll
+        for (int l = 0; l < NL; ++l) r[l] = fmaf(m - d[NI + l], k2, lold[l]);   // t_L
+        float T = -FLT_MAX;   // (as label_half: every label dead gives s = 0, flagged as a collapse)
+#pragma unroll
+        for (int l = 0; l < NL; ++l) T = fmaxf(T, r[l]);
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
-            ut[l] = uold[l] * ex2_approx((m - d[NI + l]) * k2);
-            if (l < Q1) s0 += ut[l];
-            else if (l < H) s1 += ut[l];
-            else if (l < Q3) s2 += ut[l];
-            else s3 += ut[l];
+            r[l] = r[l] - T;
+            e[l] = ex2_approx(r[l]);
+            if (l < Q1) s0 += e[l];
+            else if (l < H) s1 += e[l];
+            else if (l < Q3) s2 += e[l];
+            else s3 += e[l];
         }
-        sum = (s0 + s1) + (s2 + s3);
-    }
-    const float inv = __frcp_rn(sum);
+        const float s = (s0 + s1) + (s2 + s3);
+        const float ls = lg2_approx(s), g = ex2_approx(T);
 #pragma unroll
-    for (int l = 0; l < NL; ++l) {
-        const float nu = ut[l] * inv;
-        unew[l] = nu < FLT_MIN ? 0.f : nu;
+        for (int l = 0; l < NL; ++l) {
+            lnew[l] = r[l] - ls;
+            ut[l] = e[l] * g;
+        }
+        return s;
     }
-    return sum;
 }
+
+// max |u' - u| over the labels of one voxel (residual, row a8) from the old and new log2 states
+template <int N>
+__device__ __forceinline__ float resid_log2(const float *lnew, const float *lold, float acc) {
+#pragma unroll
+    for (int l = 0; l < N; ++l) acc = fmaxf(acc, fabsf(u_of_log2(lnew[l]) - u_of_log2(lold[l])));
+    return acc;
+}
+
+// numerical collapse of the label update (a(x) <= 0 or not finite): s (>= 1 when sane) is 0,
+// infinite or NaN -- e.g. every label of the voxel at lambda = -inf, or a non-finite excess
+__device__ __forceinline__ bool label_sum_bad(float s) { return !(s > 0.f) || !(s <= FLT_MAX); }
 
 // Top-down excess pushes along O \ {S}: d_j += w_ij d_i for internal i (positions < NI).
 template <int NI, int NV>

@@ -28,6 +28,8 @@
 //     the only per-voxel couplings of the label update -- m = min_L d_L and a = sum_L u~_L -- are
 //     combined from per-half (shift, sum) pairs exchanged once through shared memory under a 64-thread named
 //     barrier -- label_update's split form (pf_math.cuh), so G does not change a bit.
+//   * u is stored as lambda = log2 u (pf_math.cuh label_update; reading R18): the u stages, the staged u tile
+//     and the output hold log2 values.
 #pragma once
 #include <cuda.h>
 
@@ -85,7 +87,7 @@ struct StagedLayout {
     static constexpr int UOSZ = OSTAGE ? round32(NL * TY * 32) : 0;       // u staging [l][row][32], x2
     static constexpr int QOSZ = OSTAGE ? round32(3 * NF * TY * 32) : 0;   // q staging: OSTAGE 1 [ch][row][32] x2,
     static constexpr int QOB = OSTAGE == 1 ? 2 : 1;                         //   OSTAGE 2 [row][grp][k][f][32] x1
-    static constexpr int XSZ = G > 1 ? round32(2 * (TY + 2) * G * 32) : 0;  // (m_h, a_h) exchange (G = 2)
+    static constexpr int XSZ = G > 1 ? round32(3 * (TY + 2) * G * 32) : 0;  // (m_h, T_h, s_h) exchange (G = 2)
     static constexpr int kThreads = 32 * G * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
             float Mv[NFG];
             // ---------------- stage A(p): div, excess, label update, masses (tile + halo)
             float dq[NFG];
-            float Dv[NLG], uold[NLG], ut[NLG], un[NLG];
+            float Dv[NLG], uold[NLG], ut[NLG], un[NLG];   // uold / un: log2 states; ut: masses u~
             float dlab[G == 1 ? NI + NL : NLG];   // end-label excesses (G = 1: positions NI..)
             if (lx >= 0) {
 #pragma unroll
@@ -368,51 +370,35 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                     sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
                 }
             } else {
-                // Potts, labels l0 .. l0+NLG-1 = half `grp` of the labels (NL >= kHalfSplitNL): local shift
-                // m_h, local masses and a_h = quarter + quarter, then ONE exchange of (m_h, a_h) with the
-                // partner warp and the rescale of label_update's split form (pf_math.cuh)
+                // Potts, labels l0 .. l0+NLG-1 = half `grp` of the labels (NL >= kHalfSplitNL): the half's
+                // (m_h, T_h, s_h), ONE exchange of the three with the partner warp, then label_update's split
+                // combine (pf_math.cuh)
                 static_assert(G == 2 && NL >= kHalfSplitNL, "label split = label_update's two halves");
                 float *xm = X + (xr * G) * 32 + lane;
-                float *xa = X + ((TY + 2) * G + xr * G) * 32 + lane;
-                float mh = 0.f, sa = 0.f, sb = 0.f;
+                float *xt = X + ((TY + 2) * G + xr * G) * 32 + lane;
+                float *xs = X + (2 * (TY + 2) * G + xr * G) * 32 + lane;
+                float mh = 0.f, th = 0.f, sh = 1.f;
+                float rr[NLG];
                 if (lx >= 0) {
 #pragma unroll
                     for (int l = 0; l < NLG; ++l) dlab[l] = Dv[l] + dq[l];
-                    if (a.shift == 0) {
-                        mh = dlab[0];
-#pragma unroll
-                        for (int l = 1; l < NLG; ++l) mh = fminf(mh, dlab[l]);
-                    }
-#pragma unroll
-                    for (int l = 0; l < NLG; ++l) {
-                        ut[l] = uold[l] * ex2_approx((mh - dlab[l]) * k2);
-                        if (l < NLG / 2) sa += ut[l];
-                        else sb += ut[l];
-                    }
+                    label_half<NLG>(dlab, uold, rr, ut, a.shift, k2, mh, th, sh);
                 }
                 xm[grp * 32] = mh;
-                xa[grp * 32] = sa + sb;
+                xt[grp * 32] = th;
+                xs[grp * 32] = sh;
                 named_bar(1 + xr, 32 * G);
-                const float m0 = xm[0], m1 = xm[32];
-                float f0 = 1.f, f1 = 1.f;
-                if (a.shift == 0) {
-                    const float m = fminf(m0, m1);
-                    f0 = ex2_approx((m - m0) * k2);
-                    f1 = ex2_approx((m - m1) * k2);
-                }
-                sum = halves_sum(xa[0], f0, xa[32], f1);
-                const float fo = grp == 0 ? f0 : f1;
-                const float inv = __frcp_rn(sum);
+                float ch, gh;
+                sum = label_halves_combine(xm[0], xt[0], xs[0], xm[32], xt[32], xs[32], grp, a.shift, k2, ch, gh);
 #pragma unroll
                 for (int l = 0; l < NLG; ++l) {
-                    ut[l] *= fo;
-                    const float nu = ut[l] * inv;
-                    un[l] = nu < FLT_MIN ? 0.f : nu;
+                    un[l] = rr[l] + ch;
+                    ut[l] *= gh;
                 }
             }
             if (lx >= 0) {
                 if (p < zc1 && is_main && valid) {
-                    if (grp == 0 && (!(sum > 0.f) || !(sum <= FLT_MAX))) {
+                    if (grp == 0 && label_sum_bad(sum)) {
                         const unsigned long long vox = ((unsigned long long)(a.zg0 + p) * a.ny + y) * a.nx + x;
                         atomicMin(a.err_voxel, vox);
                     }
@@ -425,10 +411,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
 #pragma unroll
                         for (int l = 0; l < NLG; ++l) st_stream(uo + l * (int)P, un[l]);
                     }
-                    if (a.check) {
-#pragma unroll
-                        for (int l = 0; l < NLG; ++l) resid = fmaxf(resid, fabsf(un[l] - uold[l]));
-                    }
+                    if (a.check) resid = resid_log2<NLG>(un, uold, resid);
                 }
                 if constexpr (G == 1) {
                     node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);

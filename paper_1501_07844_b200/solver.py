@@ -8,7 +8,7 @@ import numpy as np
 from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NODE, PF_S_SCALED_FIELD,
                PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_iterate_linked, pf_link_slabs, pf_get_energy, pf_get_flows, pf_get_kernel_info,
-               pf_get_labeling, pf_get_node_labeling, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
+               pf_get_labeling, pf_get_node_labeling, pf_get_state, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
                pf_set_state, pf_set_step,
                pf_set_stream)
 
@@ -103,18 +103,21 @@ class Solver:
 
     # ---------------------------------------------------------------- checkpoint / resume
     def state(self):
-        """(u, q, iterations): the resumable state of the owned slab (pf_get_labeling / pf_get_flows)."""
-        u, _ = self.labeling()
-        return u, self.flows(), self.iterations()
+        """(lambda = log2 u, q, iterations): the exact resumable state of the owned slab (pf_get_state)."""
+        lam = np.empty((self.NL,) + self.shape, dtype=np.float32)
+        q = np.empty((self.num_nodes - 1, self.ndim) + self.shape, dtype=np.float32)
+        pf_get_state(self.h, lam, q)
+        return lam, q, self.iterations()
 
-    def set_state(self, u, q, iterations: int):
-        """Restore a state from state() (pf_set_state); slab solvers then need a halo exchange."""
-        pf_set_state(self.h, np.ascontiguousarray(u, dtype=np.float32) if isinstance(u, np.ndarray) else u,
-                     np.ascontiguousarray(q, dtype=np.float32) if isinstance(q, np.ndarray) else q, iterations)
+    def set_state(self, u, q, iterations: int, u_is_log2: bool = True):
+        """Restore a state from state() (pf_set_state; u = lambda = log2 u), or start from a labeling u
+        (u_is_log2=False); slab solvers then need a halo exchange."""
+        pf_set_state(self.h, np.ascontiguousarray(u) if isinstance(u, np.ndarray) else u,
+                     np.ascontiguousarray(q) if isinstance(q, np.ndarray) else q, iterations, u_is_log2)
 
     def save(self, path: str, c: Optional[float] = None, tau: Optional[float] = None):
-        """Checkpoint to one .npz: u, q (raw float32), the iteration count and the geometry it belongs to
-        (plus the current c, tau if given: they are configuration, not state)."""
+        """Checkpoint to one .npz: lambda = log2 u, q (raw float32), the iteration count and the geometry it
+        belongs to (plus the current c, tau if given: they are configuration, not state)."""
         u, q, it = self.state()
         meta = {"dims": self.dims, "ndim": self.ndim, "num_nodes": self.num_nodes, "labels": self.NL,
                 "slab": self.slab, "iterations": it, "c": c, "tau": tau}
@@ -202,8 +205,10 @@ class SlabSet:
         pf_exchange_local(self.handles)
 
     def state(self):
-        """(u, q, iterations) of the whole volume (slabs concatenated along z)."""
-        return self.labeling()[0], self.flows(), self.solvers[0].iterations()
+        """(lambda = log2 u, q, iterations) of the whole volume (slabs concatenated along z)."""
+        st = [s.state() for s in self.solvers]
+        return (np.concatenate([x[0] for x in st], axis=1), np.concatenate([x[1] for x in st], axis=2),
+                self.solvers[0].iterations())
 
     def set_state(self, u, q, iterations: int):
         """Restore a whole-volume state: every slab takes its planes, then one halo exchange."""

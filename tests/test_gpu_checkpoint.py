@@ -55,6 +55,42 @@ def test_set_state_from_device_buffers():
     assert np.array_equal(s1.labeling()[0], s2.labeling()[0]) and np.array_equal(s1.flows(), s2.flows())
 
 
+def test_set_state_linear_labeling_matches_oracle():
+    """pf_set_state with the labeling u itself (u_is_log2 = 0): start from the oracle's state after 40
+    iterations, run 60 more, compare with the oracle's 100 (the log2 conversion is the only extra rounding)."""
+    import oracle as O
+    from helpers import compare
+    inp = P.generate(P.config("C4").resized(33, 27, 19))
+    u40, q40 = O.run_inputs(inp, 40)
+    s = solver_from_inputs(inp)
+    s.set_state(u40.astype(np.float32), q40.astype(np.float32), 40, u_is_log2=False)
+    s.iterate(60)
+    u, _ = s.labeling()
+    q = s.flows()
+    O.run_inputs(inp, 60, state=(u40, q40))
+    compare(u, q, u40, q40)
+    s.close()
+
+
+def test_dead_label_stays_dead():
+    """A label set exactly to 0 (lambda = -inf) stays 0 -- the multiplicative update of Eq. 7 keeps
+    u_L = 0 -- in the GPU state as in the oracle, and the other labels follow the oracle."""
+    import oracle as O
+    from helpers import compare
+    inp = P.generate(P.config("C2").resized(29, 23, 17))
+    ur, qr = O.init_state(8, 8, inp.shape, 3)
+    ur[3] = 0.0
+    ur /= ur.sum(0)
+    s = solver_from_inputs(inp)
+    s.set_state(ur.astype(np.float32), qr.astype(np.float32), 0, u_is_log2=False)
+    s.iterate(50)
+    u, am = s.labeling()
+    O.run_inputs(inp, 50, state=(ur, qr))
+    assert np.all(u[3] == 0) and np.all(ur[3] == 0) and not np.any(am == 3)
+    compare(u, s.flows(), ur, qr)
+    s.close()
+
+
 def test_set_state_errors(tmp_path):
     inp = P.generate(P.config("C2").resized(20, 16, 8))
     s = solver_from_inputs(inp)
@@ -63,6 +99,12 @@ def test_set_state_errors(tmp_path):
         pf.pf_set_state(s.h, None, q, 0)
     with pytest.raises(pf.PFError):
         s.set_state(u, q, -1)
+    with pytest.raises(ValueError):               # validated sizes / dtypes in the binding (no silent misuse)
+        s.set_state(u[:, :-1], q, 0)
+    with pytest.raises(ValueError):
+        s.set_state(u.astype(np.float64), q, 0)
+    with pytest.raises(ValueError):
+        s.labeling(u_out=np.empty((u.shape[0] - 1,) + u.shape[1:], np.float32))
     path = str(tmp_path / "ck.npz")
     s.save(path)
     other = solver_from_inputs(P.generate(P.config("C2").resized(20, 16, 9)))

@@ -542,3 +542,20 @@ def test_ishikawa_exhaustive_and_alm():
     ua, qa, p = alm.dag_alm(D, S, g.num_nodes, g.parent, g.child, g.weight, 2, 16000)
     assert abs(float(p[0].sum()) - Erel) <= 1e-8 * Erel
     assert np.max(np.abs(ua - u)) < 1e-6
+
+
+# ---------------------------------------------------------------- threaded oracle
+@pytest.mark.parametrize("name,dims", [("C2", (19, 13, 11)), ("C4", (17, 12, 9)), ("I2", (15, 11, 7)),
+                                       ("C1", (23, 17, 1))])
+def test_threaded_oracle_bit_identical(name, dims):
+    """Every whole-field pass is per-voxel pure, so n threads give the 1-thread result bit for bit."""
+    import phantoms as P
+    inp = P.generate(P.config(name).resized(*dims))
+    try:
+        O.set_threads(1)
+        u1, q1 = O.run_inputs(inp, 25)
+        O.set_threads(4)
+        u4, q4 = O.run_inputs(inp, 25)
+    finally:
+        O.set_threads(1)
+    assert np.array_equal(u1, u4) and np.array_equal(q1, q4)

@@ -115,6 +115,7 @@ def test_slab_resume_from_single_domain_state(fused):
     slabs.iterate(14)
     u2, q2, it2 = slabs.state()
     assert it2 == it + 14
-    assert np.array_equal(u2, ref.labeling()[0]) and np.array_equal(q2, ref.flows())
+    assert np.array_equal(u2, ref.state()[0]) and np.array_equal(q2, ref.flows())
+    assert np.array_equal(slabs.labeling()[0], ref.labeling()[0])
     slabs.close()
     ref.close()
