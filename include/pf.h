@@ -289,6 +289,7 @@ typedef struct {
     int32_t work_items;                      /* (tile, z-chunk) items per iteration */
     int32_t model;                           /* 0: Alg. 1/2 (star / tree / DAG), 1: Alg. 3 (Ishikawa chain) */
     int32_t flow_nodes;                      /* nodes whose spatial flow is stored */
+    int32_t cluster;                         /* 1: labels split over a 2-CTA cluster (pf_iter_cluster) */
 } pf_kernel_info;
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info);

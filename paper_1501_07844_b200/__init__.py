@@ -85,7 +85,7 @@ class pf_kernel_info(ctypes.Structure):
                 ("smem_bytes", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("algorithmic_bytes_per_iteration", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("staged", ctypes.c_int32), ("work_items", ctypes.c_int32),
-                ("model", ctypes.c_int32), ("flow_nodes", ctypes.c_int32)]
+                ("model", ctypes.c_int32), ("flow_nodes", ctypes.c_int32), ("cluster", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p

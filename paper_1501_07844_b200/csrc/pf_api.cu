@@ -1109,6 +1109,7 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     info->kernel_launches = s->launches;
     info->model = s->gc.model;
     info->flow_nodes = s->gc.NF;
+    info->cluster = s->cluster ? 1 : 0;
     return PF_OK;
 }
 
