@@ -179,6 +179,13 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual);
  * 2^-126 read as 0).  Host or device buffers. */
 pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax);
 
+/* Leave `sms` SMs free during the interior launch of a split iteration (pf_iterate_phase(1)), so that a
+ * halo-exchange kernel posted concurrently on another stream (NCCL P2P) finds SMs to run on: the
+ * persistent grid otherwise occupies every SM with one ~216 KB CTA until the interior is done, and the
+ * exchange could not overlap it.  The work-item queue lets any grid size finish the same items; results
+ * are bitwise unchanged.  0 (default) = all SMs.  Errors: PF_ERR_INVALID (sms < 0 or >= the SM count). */
+pf_status pf_set_reserved_sms(pf_solver *s, int32_t sms);
+
 /* Labeling of any node v of the graph (row a9, "intermediate labels on demand"): u_v(x) =
  * sum_B W_(v,B) u_B(x) over the end labels (path weights P:199-209), u_S = 1.  node: graph node
  * id (0 = S).  u_node: [V_local] fp32, host or device.  Errors: PF_ERR_INVALID (node out of range, NULL). */
@@ -258,21 +265,29 @@ pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n);
 pf_status pf_iterate_linked(pf_solver *const *solvers, int32_t n, int32_t iters, float *residual);
 
 /* Fused halo exchange across PROCESSES (one process per GPU, torchrun): the same in-kernel peer
- * stores as pf_link_slabs, with the neighbours' state buffers shared by CUDA IPC (NVLink peer memory)
- * and one interprocess event per slab recorded after every iteration.
- *   pf_ipc_export: the slab's buffers and event as a plain blob for the neighbours; records the event
- *     once ("initial state in place").  Needs pf_config.ipc = 1 and a tile-storing kernel variant.
+ * stores as pf_link_slabs, with the neighbours' state buffers shared by CUDA IPC (NVLink peer memory),
+ * ordered ON THE DEVICE by progress words (no host synchronisation per iteration).
+ *   pf_ipc_export: the slab's buffers and its progress inbox as a plain blob for the neighbours.
+ *     Needs pf_config.ipc = 1 and a tile-storing kernel variant.
  *   pf_ipc_link:   open the neighbours' blobs (NULL where there is none).
- *   pf_ipc_step:   one iteration: wait on the neighbours' events, run the linked kernel, record.
- * Protocol: export, exchange the blobs, link, host barrier; then per iteration pf_ipc_step followed
- * by a host barrier over the ranks, so that every rank has RECORDED iteration t before any rank
- * issues the wait of iteration t+1 (the GPU work itself stays asynchronous).  residual: as
- * pf_iterate.  Errors: PF_ERR_STATE (no ipc config / not exported), PF_ERR_INVALID (blobs that are
- * not this slab's neighbours at the same iteration), PF_ERR_UNSUPPORTED (kernel variant). */
+ *   pf_ipc_step:   one iteration: the stream waits (cuStreamWaitValue32, GEQ) until both neighbours
+ *     have announced the previous step in this slab's inbox, runs the linked kernel (which also stores
+ *     the boundary planes into the neighbours' halo planes), then writes this slab's step count into
+ *     the neighbours' inboxes (cuStreamWriteValue32, after a memory barrier).  Iteration t+1 of a slab
+ *     therefore starts only after iteration t of both neighbours: RAW on the halo planes it reads, WAR on
+ *     the neighbour halo planes it writes.  pf_reset is a step of the same protocol (it re-initialises
+ *     the halo planes the neighbours write into).
+ * Protocol: export, exchange the blobs, link, one host barrier; then every rank issues the same sequence
+ * of pf_ipc_step / pf_reset calls -- no host barrier per iteration (the ranks' streams run ahead on
+ * their own).  residual: as pf_iterate.  Errors: PF_ERR_STATE (no ipc config / not exported),
+ * PF_ERR_INVALID (blobs that are not this slab's neighbours at the same iteration), PF_ERR_UNSUPPORTED
+ * (kernel variant, or stream memory operations unavailable). */
 typedef struct {
-    uint8_t u[2][64], q[2][64], event[64];   /* cudaIpcMemHandle_t x 4, cudaIpcEventHandle_t */
+    uint8_t u[2][64], q[2][64], event[64];   /* cudaIpcMemHandle_t x 4, (unused) */
     int64_t nx, ny, nzl, z0, pitch;
     int32_t NF, NL, tile_y, cluster, cur;
+    uint8_t inbox[64];                       /* cudaIpcMemHandle_t of the progress inbox */
+    uint32_t seq;                            /* protocol steps taken so far */
 } pf_ipc_slab;
 
 pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out);
@@ -290,6 +305,7 @@ typedef struct {
     int32_t model;                           /* 0: Alg. 1/2 (star / tree / DAG), 1: Alg. 3 (Ishikawa chain) */
     int32_t flow_nodes;                      /* nodes whose spatial flow is stored */
     int32_t cluster;                         /* 1: labels split over a 2-CTA cluster (pf_iter_cluster) */
+    int32_t phase1_ctas;                     /* grid of a pf_iterate_phase(1) launch (see pf_set_reserved_sms) */
 } pf_kernel_info;
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info);

@@ -36,7 +36,7 @@ _STATUS = {1: "PF_ERR_INVALID", 2: "PF_ERR_GRAPH", 3: "PF_ERR_OOM", 4: "PF_ERR_C
 
 EXPORTED = ["pf_create", "pf_reset", "pf_set_step", "pf_iterate", "pf_run", "pf_iterate_phase", "pf_get_node_labeling",
             "pf_link_slabs", "pf_iterate_linked", "pf_ipc_export", "pf_ipc_link", "pf_ipc_step", "pf_get_labeling", "pf_get_flows", "pf_get_state", "pf_set_state", "pf_get_energy",
-            "pf_iterations", "pf_set_stream", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
+            "pf_iterations", "pf_set_stream", "pf_set_reserved_sms", "pf_halo_regions", "pf_exchange_local", "pf_get_kernel_info",
             "pf_destroy", "pf_last_error", "pf_version"]
 
 
@@ -65,7 +65,8 @@ class pf_ipc_slab(ctypes.Structure):
     _fields_ = [("u", (ctypes.c_uint8 * 64) * 2), ("q", (ctypes.c_uint8 * 64) * 2), ("event", ctypes.c_uint8 * 64),
                 ("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nzl", ctypes.c_int64), ("z0", ctypes.c_int64),
                 ("pitch", ctypes.c_int64), ("NF", ctypes.c_int32), ("NL", ctypes.c_int32), ("tile_y", ctypes.c_int32),
-                ("cluster", ctypes.c_int32), ("cur", ctypes.c_int32)]
+                ("cluster", ctypes.c_int32), ("cur", ctypes.c_int32), ("inbox", ctypes.c_uint8 * 64),
+                ("seq", ctypes.c_uint32)]
 
 
 class pf_slab(ctypes.Structure):
@@ -85,7 +86,8 @@ class pf_kernel_info(ctypes.Structure):
                 ("smem_bytes", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("algorithmic_bytes_per_iteration", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("staged", ctypes.c_int32), ("work_items", ctypes.c_int32),
-                ("model", ctypes.c_int32), ("flow_nodes", ctypes.c_int32), ("cluster", ctypes.c_int32)]
+                ("model", ctypes.c_int32), ("flow_nodes", ctypes.c_int32), ("cluster", ctypes.c_int32),
+                ("phase1_ctas", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p
@@ -106,6 +108,7 @@ _sig = {
     "pf_get_energy": (ctypes.c_int, [_vp, _P(ctypes.c_double), _P(ctypes.c_double)]),
     "pf_iterations": (ctypes.c_int, [_vp, _P(ctypes.c_int64)]),
     "pf_set_stream": (ctypes.c_int, [_vp, _vp]),
+    "pf_set_reserved_sms": (ctypes.c_int, [_vp, ctypes.c_int32]),
     "pf_halo_regions": (ctypes.c_int, [_vp, _P(pf_halo)]),
     "pf_exchange_local": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32]),
     "pf_link_slabs": (ctypes.c_int, [_P(ctypes.c_void_p), ctypes.c_int32]),
@@ -290,6 +293,11 @@ def pf_iterations(s: int) -> int:
 
 def pf_set_stream(s: int, stream_ptr: int):
     _check(_lib.pf_set_stream(s, stream_ptr))
+
+
+def pf_set_reserved_sms(s: int, sms: int):
+    """Leave `sms` SMs free during pf_iterate_phase(1) launches (a concurrent exchange kernel can run)."""
+    _check(_lib.pf_set_reserved_sms(s, int(sms)))
 
 
 def pf_halo_regions(s: int) -> pf_halo:

@@ -67,9 +67,7 @@ void free_all(pf_solver *s) {
     }
     for (void *p : s->ipc_opened) cudaIpcCloseMemHandle(p);
     s->ipc_opened.clear();
-    for (int i = 0; i < 2; ++i)
-        if (s->nb_ev[i]) { cudaEventDestroy(s->nb_ev[i]); s->nb_ev[i] = nullptr; }
-    if (s->ipc_ev) { cudaEventDestroy(s->ipc_ev); s->ipc_ev = nullptr; }
+    if (s->ipc_inbox) { cudaFree(s->ipc_inbox); s->ipc_inbox = nullptr; }
     if (s->ipc) {   // cudaMalloc'd state (exportable); synchronise before the synchronous frees
         cudaStreamSynchronize(s->stream);
         for (int i = 0; i < 2; ++i) {
@@ -376,6 +374,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     s->alm = alm;
     s->ipc = cfg->ipc != 0;
     cudaGetDevice(&s->device);
+    cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, s->device);
     s->ndim = dims->ndim;
     s->nx = dims->nx;
     s->ny = dims->ny;
@@ -576,12 +575,15 @@ pf_status pf_reset(pf_solver *s) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
     DeviceGuard dg(s->device);
-    // IPC-linked: the neighbours' last kernels (which write into this slab's halo planes) must be done
-    // before the re-init, and their next kernels must start after it
-    for (int i = 0; i < 2; ++i)
-        if (s->nb_ev[i]) CK(cudaStreamWaitEvent(s->stream, s->nb_ev[i], 0), "wait neighbour");
+    // IPC-linked: a step of the device-side protocol -- the neighbours' last kernels (which write into this
+    // slab's halo planes) must be done before the re-init, and their next kernels start after it
+    const bool linked = s->ipc_exported && (s->link_below || s->link_above);
+    if (linked && (st = ipc_wait_neighbours(s, s->ipc_seq)) != PF_OK) return st;
     if ((st = init_state(s)) != PF_OK) return st;
-    if (s->ipc_ev) CK(cudaEventRecord(s->ipc_ev, s->stream), "record");
+    if (linked) {
+        s->ipc_seq += 1;
+        if ((st = ipc_announce(s, s->ipc_seq)) != PF_OK) return st;
+    }
     return PF_OK;
 }
 
@@ -621,7 +623,6 @@ pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t ite
     CK(cudaMemsetAsync(s->d_err, 0xff, sizeof(unsigned long long), s->stream), "init err");
     if (!is_device_ptr(u) || !is_device_ptr(q)) CK(cudaStreamSynchronize(s->stream), "sync");   // host buffers
     s->iters = iterations;
-    if (s->ipc_ev) CK(cudaEventRecord(s->ipc_ev, s->stream), "record");
     return PF_OK;
 }
 
@@ -638,6 +639,14 @@ pf_status pf_set_step(pf_solver *s, float c, float tau) {
         cudaGraphExecDestroy(s->graph);
         s->graph = nullptr;
     }
+    return PF_OK;
+}
+
+pf_status pf_set_reserved_sms(pf_solver *s, int32_t sms) {
+    pf_status st = check_usable(s);
+    if (st != PF_OK) return st;
+    if (sms < 0 || sms >= s->sms) return fail(PF_ERR_INVALID, "reserved SMs must be in [0, %d)", s->sms);
+    s->reserved_sms = sms;
     return PF_OK;
 }
 
@@ -659,7 +668,15 @@ pf_status pf_set_stream(pf_solver *s, void *stream) {
 namespace pfi {
 
 // Launch items [ib, ie) of one iteration reading state `cur` (no swap).  ie == ib launches nothing.
-pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
+int phase1_grid(const pf_solver *s) {
+    if (!s->staged) return (int)(s->grid.x * s->grid.y * s->grid.z);
+    const int per = s->cluster ? 2 : 1;
+    int g = s->sgrid;
+    if (s->reserved_sms > 0) g = std::min(g, std::max(per, (s->sms - s->reserved_sms) * std::max(1, s->ctas_per_sm)));
+    return g / per * per;
+}
+
+pf_status launch_items(pf_solver *s, int ib, int ie, int check, int reserve_sms) {
     if (s->staged) {
         if (ie <= ib) return PF_OK;
         StagedArgs sa;
@@ -713,7 +730,9 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check) {
         sa.ticket_next = s->d_err + 2 - s->launch_parity;
         // cluster kernel: 2 CTAs per item and one ticket grab per cluster
         const int per = s->cluster ? 2 : 1;
-        const int grid = (int)std::min<int64_t>(s->sgrid / per, ie - ib) * per;
+        int sg = s->sgrid;
+        if (reserve_sms > 0) sg = phase1_grid(s);   // leave SMs free for a concurrent exchange kernel
+        const int grid = (int)std::min<int64_t>(sg / per, ie - ib) * per;
         void *args[] = {(void *)&sa};
         CK(cudaLaunchKernel(s->sinfo.func, dim3(grid), dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
            s->cluster ? "launch pf_iter_cluster" : "launch pf_iter_staged");
@@ -760,6 +779,7 @@ int check_this_iteration(pf_solver *s) {
 pf_status read_residual(pf_solver *s, bool any_check, float *residual) {
     if (any_check) s->last_resid_valid = true;
     if (!residual) return PF_OK;
+    NvtxRange nv("pf check (residual read)");
     *residual = -1.f;
     pf_status st;
     if ((st = check_numeric(s)) != PF_OK) return st;
@@ -859,6 +879,7 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
     if (s->link_below || s->link_above) return fail(PF_ERR_STATE, "linked slab: iterate with pf_iterate_linked / pf_ipc_step");
     if (s->phase_pending) return fail(PF_ERR_STATE, "pf_iterate: an iteration split by pf_iterate_phase is open");
     DeviceGuard dg(s->device);
+    NvtxRange nv("pf_iterate");
     bool any_check = false;
     // whole periods as CUDA-graph replays (one graph launch instead of P kernel launches + memsets),
     // the rest as plain launches; PF_GRAPHS=0 disables
@@ -912,6 +933,7 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual) {
         return fail(PF_ERR_STATE, phase == 0 ? "phase 0 issued twice" : "phase 1 without phase 0");
     DeviceGuard dg(s->device);
     const int check = check_this_iteration(s);
+    NvtxRange nv(phase == 0 ? (check ? "pf boundary (check)" : "pf boundary") : (check ? "pf interior (check)" : "pf interior"));
     if (phase == 0) {
         if (check) CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
         // global-load kernel: no split, the whole iteration runs in phase 0
@@ -919,7 +941,7 @@ pf_status pf_iterate_phase(pf_solver *s, int32_t phase, float *residual) {
         s->phase_pending = 1;
         return PF_OK;
     }
-    if (s->staged && (st = launch_items(s, s->items_b, s->items, check)) != PF_OK) return st;
+    if (s->staged && (st = launch_items(s, s->items_b, s->items, check, s->reserved_sms)) != PF_OK) return st;
     s->phase_pending = 0;
     s->cur = 1 - s->cur;
     s->iters += 1;
@@ -1110,6 +1132,7 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     info->model = s->gc.model;
     info->flow_nodes = s->gc.NF;
     info->cluster = s->cluster ? 1 : 0;
+    info->phase1_ctas = phase1_grid(s);
     return PF_OK;
 }
 

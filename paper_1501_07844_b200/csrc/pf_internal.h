@@ -12,6 +12,7 @@
 #include <vector>
 
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "pf.h"
 #include "pf_alm.cuh"
@@ -27,6 +28,12 @@ using namespace pf;
 // last error message of this thread (pf_last_error) and the error constructor
 extern thread_local std::string g_last_error;
 pf_status fail(pf_status st, const char *fmt, ...);
+
+// NVTX range for nsys timelines (boundary / interior / check / ipc step)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct DeviceGuard {
     int prev = -1;
@@ -97,12 +104,14 @@ struct pf_solver {
     bool link_below = false, link_above = false;           // in-process or IPC links
     int nb_plane = 0;                                      // below neighbour's upper halo plane coordinate
     CUtensorMap tm_uo_nb[2], tm_qo_nb[2], tm_qz_nb[2];
-    // cross-process links (pf_ipc_*): state from cudaMalloc (IPC-exportable), an interprocess event
-    // recorded after every iteration, the neighbours' opened buffers and events
+    // cross-process links (pf_ipc_*): state from cudaMalloc (IPC-exportable), a progress inbox the
+    // neighbours announce their steps into, the neighbours' opened buffers and inbox words
     bool ipc = false;
-    cudaEvent_t ipc_ev = nullptr;
+    bool ipc_exported = false;
+    uint32_t *ipc_inbox = nullptr;          // [0]: steps announced by the neighbour below, [1]: by the one above
+    uint32_t *nb_inbox[2] = {nullptr, nullptr};   // the neighbours' inbox words this slab announces into
+    uint32_t ipc_seq = 0;                   // protocol steps (pf_ipc_step / pf_reset) issued so far
     std::vector<void *> ipc_opened;
-    cudaEvent_t nb_ev[2] = {nullptr, nullptr};
     // CUDA graph of `graph_iters` whole iterations (pf_iterate), replayed when the state matches the
     // capture: same ping-pong buffer, same counter parity, check iterations at the same positions
     cudaGraphExec_t graph = nullptr;
@@ -129,6 +138,8 @@ struct pf_solver {
     // boundary / interior split of the z-chunks (slabs with neighbours; pf_iterate_phase)
     int nb = 0, bplane[2] = {0, 0}, zlo = 0, zhi = 0, items_b = 0;
     int phase_pending = 0;  // 1 after pf_iterate_phase(0) until its phase 1
+    int reserved_sms = 0;   // SMs a phase-1 launch leaves free (pf_set_reserved_sms)
+    int sms = 148;
     unsigned int tx_bytes = 0;
 };
 
@@ -150,7 +161,13 @@ pf_status check_usable(const pf_solver *s);
 pf_status check_numeric(pf_solver *s);
 int check_this_iteration(pf_solver *s);
 pf_status read_residual(pf_solver *s, bool any_check, float *residual);
-pf_status launch_items(pf_solver *s, int ib, int ie, int check);
+pf_status launch_items(pf_solver *s, int ib, int ie, int check, int reserve_sms = 0);
+int phase1_grid(const pf_solver *s);
+// device-side ordering of IPC-linked slabs (pf_ipc_step, pf_reset): wait until both neighbours announced
+// step `seq` in this slab's inbox / announce `seq` into theirs
+pf_status ipc_wait_neighbours(pf_solver *s, uint32_t seq);
+bool stream_mem_ops();
+pf_status ipc_announce(pf_solver *s, uint32_t seq);
 bool encode4d(CUtensorMap *m, const void *base, int64_t nx, int64_t ny, int64_t pitch, int64_t nch, int64_t nplanes,
               int bx, int by, int bc, bool bf16 = false);
 

@@ -4,6 +4,55 @@
 
 using namespace pfi;
 
+namespace pfi {
+
+// stream memory operations (driver API, via the runtime's entry-point query: no libcuda link)
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*StreamWriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static StreamWaitValue32Fn g_wait = nullptr;
+static StreamWriteValue32Fn g_write = nullptr;
+
+bool stream_mem_ops() {
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_wait = (StreamWaitValue32Fn)p;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_write = (StreamWriteValue32Fn)p;
+        cudaGetLastError();
+    }
+    return g_wait && g_write;
+}
+
+pf_status ipc_wait_neighbours(pf_solver *s, uint32_t seq) {
+    if (!stream_mem_ops()) return fail(PF_ERR_UNSUPPORTED, "stream memory operations unavailable");
+    const bool has[2] = {s->link_below, s->link_above};
+    for (int i = 0; i < 2; ++i) {
+        if (!has[i]) continue;
+        const CUresult r = g_wait((CUstream)s->stream, (CUdeviceptr)(s->ipc_inbox + i), seq, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) { s->poisoned = true; return fail(PF_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r); }
+    }
+    return PF_OK;
+}
+
+pf_status ipc_announce(pf_solver *s, uint32_t seq) {
+    for (int i = 0; i < 2; ++i) {
+        if (!s->nb_inbox[i]) continue;
+        // default flags: the write is ordered after a memory barrier, so the kernel's peer stores into the
+        // neighbour's halo planes are visible before the neighbour sees the new step count
+        const CUresult r = g_write((CUstream)s->stream, (CUdeviceptr)s->nb_inbox[i], seq, CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) { s->poisoned = true; return fail(PF_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r); }
+    }
+    return PF_OK;
+}
+
+}  // namespace pfi
+
 extern "C" {
 
 pf_status pf_halo_regions(pf_solver *s, pf_halo *h) {
@@ -234,15 +283,21 @@ pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out) {
     if (!s->ipc) return fail(PF_ERR_STATE, "ipc_export: create the solver with pf_config.ipc = 1");
     if (!s->staged || !(s->cluster || s->sinfo.ostage == 1))
         return fail(PF_ERR_UNSUPPORTED, "ipc_export: this kernel variant stores no whole tiles");
+    if (!stream_mem_ops()) return fail(PF_ERR_UNSUPPORTED, "ipc_export: stream memory operations unavailable");
     DeviceGuard dg(s->device);
     memset(out, 0, sizeof(*out));
     for (int i = 0; i < 2; ++i) {
         CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)out->u[i], s->u_alloc[i]), "ipc handle u");
         CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)out->q[i], s->q_alloc[i]), "ipc handle q");
     }
-    if (!s->ipc_ev) CK(cudaEventCreateWithFlags(&s->ipc_ev, cudaEventDisableTiming | cudaEventInterprocess), "ipc event");
-    CK(cudaIpcGetEventHandle((cudaIpcEventHandle_t *)out->event, s->ipc_ev), "ipc event handle");
-    CK(cudaEventRecord(s->ipc_ev, s->stream), "record");   // "my initial state is in place"
+    if (!s->ipc_inbox) {   // progress inbox: [0] from the neighbour below, [1] from the one above
+        CK(cudaMalloc((void **)&s->ipc_inbox, 64), "ipc inbox");
+        CK(cudaMemset(s->ipc_inbox, 0, 64), "ipc inbox");
+        s->ipc_seq = 0;
+    }
+    CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)out->inbox, s->ipc_inbox), "ipc handle inbox");
+    CK(cudaStreamSynchronize(s->stream), "sync");   // the state is in place before anyone links to it
+    s->ipc_exported = true;
     out->nx = s->nx;
     out->ny = s->ny;
     out->nzl = s->nzl;
@@ -253,13 +308,14 @@ pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out) {
     out->tile_y = s->sinfo.tile_y;
     out->cluster = s->cluster ? 1 : 0;
     out->cur = s->cur;
+    out->seq = s->ipc_seq;
     return PF_OK;
 }
 
 pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab *above) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
-    if (!s->ipc || !s->ipc_ev) return fail(PF_ERR_STATE, "ipc_link: export first (pf_ipc_export)");
+    if (!s->ipc || !s->ipc_exported) return fail(PF_ERR_STATE, "ipc_link: export first (pf_ipc_export)");
     DeviceGuard dg(s->device);
     const int ty = s->sinfo.tile_y, NF = s->gc.NF, NL = s->gc.NL;
     const int cq = s->cluster ? NL / 2 : 3 * NF, cl = s->cluster ? NL / 2 : NL, cz = s->cluster ? NL / 2 : NF;
@@ -269,10 +325,10 @@ pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab 
         if (!t) continue;
         const bool adjacent = side == 0 ? t->z0 + t->nzl == s->z0 : t->z0 == s->z1;
         if (!adjacent || t->nx != s->nx || t->ny != s->ny || t->pitch != s->pitch || t->NF != NF || t->NL != NL ||
-            t->tile_y != ty || t->cluster != (s->cluster ? 1 : 0) || t->cur != s->cur)
+            t->tile_y != ty || t->cluster != (s->cluster ? 1 : 0) || t->cur != s->cur || t->seq != s->ipc_seq)
             return fail(PF_ERR_INVALID, "ipc_link: the %s blob is not this slab's neighbour in step",
                         side == 0 ? "below" : "above");
-        void *ub[2] = {nullptr, nullptr}, *qb[2] = {nullptr, nullptr};
+        void *ub[2] = {nullptr, nullptr}, *qb[2] = {nullptr, nullptr}, *ib = nullptr;
         for (int b = 0; b < 2; ++b) {
             CK(cudaIpcOpenMemHandle(&ub[b], *(const cudaIpcMemHandle_t *)t->u[b], cudaIpcMemLazyEnablePeerAccess),
                "open ipc u");
@@ -281,7 +337,11 @@ pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab 
                "open ipc q");
             s->ipc_opened.push_back(qb[b]);
         }
-        CK(cudaIpcOpenEventHandle(&s->nb_ev[side], *(const cudaIpcEventHandle_t *)t->event), "open ipc event");
+        CK(cudaIpcOpenMemHandle(&ib, *(const cudaIpcMemHandle_t *)t->inbox, cudaIpcMemLazyEnablePeerAccess),
+           "open ipc inbox");
+        s->ipc_opened.push_back(ib);
+        // this slab announces its steps into the below neighbour's "from above" word and vice versa
+        s->nb_inbox[side] = reinterpret_cast<uint32_t *>(ib) + (side == 0 ? 1 : 0);
         bool ok = true;
         for (int b = 0; b < 2; ++b) {
             if (side == 0) {   // below: its upper halo plane receives our plane 0
@@ -307,15 +367,16 @@ pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab 
 pf_status pf_ipc_step(pf_solver *s, float *residual) {
     pf_status st = check_usable(s);
     if (st != PF_OK) return st;
-    if (!s->ipc || !s->ipc_ev) return fail(PF_ERR_STATE, "ipc_step: export and link first");
+    if (!s->ipc || !s->ipc_exported) return fail(PF_ERR_STATE, "ipc_step: export and link first");
     DeviceGuard dg(s->device);
-    // the neighbours' latest recorded iteration (the caller's host barrier makes it the previous one)
-    for (int i = 0; i < 2; ++i)
-        if (s->nb_ev[i]) CK(cudaStreamWaitEvent(s->stream, s->nb_ev[i], 0), "wait neighbour");
+    NvtxRange nv("pf ipc step (fused halo stores)");
+    // iteration t + 1 after iteration t of both neighbours: they announced step ipc_seq in our inbox
+    if ((st = ipc_wait_neighbours(s, s->ipc_seq)) != PF_OK) return st;
     const int check = check_this_iteration(s);
     if (check) CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
     if ((st = launch_items(s, 0, s->items, check)) != PF_OK) return st;
-    CK(cudaEventRecord(s->ipc_ev, s->stream), "record");
+    s->ipc_seq += 1;
+    if ((st = ipc_announce(s, s->ipc_seq)) != PF_OK) return st;
     s->cur = 1 - s->cur;
     s->iters += 1;
     return read_residual(s, check != 0, residual);

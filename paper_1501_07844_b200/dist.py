@@ -12,10 +12,17 @@ recorded between the two phases, so NCCL moves the boundary planes while phase 1
 interior.  S waits for the exchange before the next phase 0 (which reads the received halos).
 The received planes land in halo planes of the new state that phase 1 neither reads nor writes.
 
+The persistent interior launch would otherwise hold every SM (one ~216 KB CTA each) until it drains, so
+the exchange kernel could not start before it: with NCCL the solver reserves `reserve_sms` SMs for it
+(pf_set_reserved_sms; the work-item queue finishes the same items on the smaller grid, bitwise equal).
+
 transport="ipc" (solvers created with ipc=True): no exchange step at all -- the iteration kernels store
 their boundary planes straight into the neighbours' halo planes through CUDA-IPC-mapped peer memory
-(pf_ipc_*), ordered by interprocess events; a host barrier per iteration only orders the event records
-and waits of the ranks (the GPU work stays queued).
+(pf_ipc_*), ordered ON THE DEVICE: each step's stream waits (cuStreamWaitValue32) for the neighbours'
+progress words and announces its own (cuStreamWriteValue32) -- no host barrier per iteration.
+
+NVTX ranges (nsys): "pf boundary" / "pf interior" (the library), "pf halo exchange" (here), "pf ipc step",
+"pf check (residual read)".
 """
 from __future__ import annotations
 
@@ -92,7 +99,7 @@ class DistSolver:
     """The rank's slab solver plus its halo exchange.  `make_solver(slab)` builds the Solver."""
 
     def __init__(self, make_solver, nz: int, rank: int, world: int, device: torch.device, group=None,
-                 transport: str = "nccl"):
+                 transport: str = "nccl", reserve_sms: int = 8):
         self.rank, self.world, self.group = rank, world, group
         self.transport = transport
         self.device = device
@@ -103,9 +110,11 @@ class DistSolver:
         self.cuda = torch.device(device).type == "cuda"
         if self.cuda:
             self.solver.set_stream(torch.cuda.current_stream(device).cuda_stream)
+            if transport == "nccl" and world > 1 and reserve_sms > 0:
+                self.solver.set_reserved_sms(reserve_sms)   # room for NCCL's P2P kernel during phase 1
         self.host_group = group
         if transport == "ipc" and world > 1:
-            # per-iteration ordering barrier on the host only (a NCCL barrier would block on the GPU work)
+            # host-only barriers at link and close (a NCCL barrier would queue behind the GPU work)
             if dist.get_backend(group) != "gloo":
                 self.host_group = dist.new_group(backend="gloo")
             blobs = [None] * world
@@ -143,9 +152,9 @@ class DistSolver:
         want = self._last_check_index(n) if residual else None
         r = -1.0 if residual else None
         if self.transport == "ipc":
+            # ordered on the device (progress words); the ranks' streams run ahead without host barriers
             for t in range(n):
                 val = pf_ipc_step(self.solver.h, t == want)
-                dist.barrier(group=self.host_group)   # all ranks recorded iteration t before any waits on it
                 if t == want:
                     r = self._max_over_ranks(val)
             return r
@@ -163,8 +172,10 @@ class DistSolver:
                 ev.record(S)
                 val = self.solver.iterate_phase(1, t == want)
                 C.wait_event(ev)
+                torch.cuda.nvtx.range_push("pf halo exchange")
                 with torch.cuda.stream(C):
                     works = halo_exchange(self._regions(), self.rank, self.world, self.group, wait=False)
+                torch.cuda.nvtx.range_pop()
             else:
                 val = self.solver.iterate(1, t == want)
                 halo_exchange(self._regions(), self.rank, self.world, self.group)
@@ -234,9 +245,7 @@ class DistSolver:
         return self._C
 
     def reset(self):
-        self.solver.reset()
-        if self.transport == "ipc" and self.world > 1:
-            dist.barrier(group=self.host_group)   # every rank's re-init is recorded before iterating
+        self.solver.reset()   # IPC: a step of the device-side protocol (pf_reset), no host barrier
 
     def close(self):
         if self.transport == "ipc" and self.world > 1:   # no neighbour kernel may still write into our buffers

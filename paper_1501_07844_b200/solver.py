@@ -9,7 +9,7 @@ from . import (PF_CAP_L2, PF_SHIFT_MIN, PF_S_FIELD_PER_NODE, PF_S_SCALAR_PER_NOD
                PF_S_SHARED_FIELD,
                pf_create, pf_destroy, pf_exchange_local, pf_iterate_linked, pf_link_slabs, pf_get_energy, pf_get_flows, pf_get_kernel_info,
                pf_get_labeling, pf_get_node_labeling, pf_get_state, pf_halo_regions, pf_iterate, pf_iterate_phase, pf_iterations, pf_reset, pf_run,
-               pf_set_state, pf_set_step,
+               pf_set_reserved_sms, pf_set_state, pf_set_step,
                pf_set_stream)
 
 
@@ -74,6 +74,10 @@ class Solver:
 
     def set_stream(self, stream_ptr: int):
         pf_set_stream(self.h, stream_ptr)
+
+    def set_reserved_sms(self, sms: int):
+        """SMs a pf_iterate_phase(1) launch leaves free for a concurrent exchange kernel (pf_set_reserved_sms)."""
+        pf_set_reserved_sms(self.h, sms)
 
     def labeling(self, u_out=None, argmax_out=None):
         """Return (u [NL][z][y][x] float32, argmax [z][y][x] uint8) as numpy unless outputs are given."""

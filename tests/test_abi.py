@@ -43,3 +43,11 @@ def test_kernel_binary_is_sm100a():
     import paper_1501_07844_b200 as pf
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", pf.LIB_PATH], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_library_carries_nvtx_ranges():
+    """The library marks its phases for nsys (boundary / interior / check / IPC step): NVTX range names."""
+    import paper_1501_07844_b200 as pf
+    data = open(pf.LIB_PATH, "rb").read()
+    for name in (b"pf boundary", b"pf interior", b"pf check (residual read)", b"pf ipc step", b"pf_iterate"):
+        assert name in data, name

@@ -119,3 +119,29 @@ def test_slab_resume_from_single_domain_state(fused):
     assert np.array_equal(slabs.labeling()[0], ref.labeling()[0])
     slabs.close()
     ref.close()
+
+
+def test_phase1_grid_leaves_sms_free_for_the_exchange():
+    """pf_set_reserved_sms: the interior launch of a split iteration (pf_iterate_phase(1)) leaves SMs free for
+    a concurrent exchange kernel (DistSolver reserves 8 for NCCL's P2P kernel); results stay bitwise equal."""
+    import torch
+    cfg = P.config("C2").resized(70, 64, 40)
+    inp = P.generate(cfg)
+    bounds = pf.solver.slab_bounds(cfg.nz, 2)
+    plain = pf.SlabSet([solver_from_inputs(inp, slab=b) for b in bounds], phased=True)
+    resv = pf.SlabSet([solver_from_inputs(inp, slab=b) for b in bounds], phased=True)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    for s in resv.solvers:
+        s.set_reserved_sms(8)
+        k = s.kernel_info()
+        assert k["staged"] == 1
+        assert 0 < k["phase1_ctas"] <= (sms - 8) * k["ctas_per_sm"] < k["ctas"]
+    for s in plain.solvers:
+        assert s.kernel_info()["phase1_ctas"] == s.kernel_info()["ctas"]
+    plain.iterate(12)
+    resv.iterate(12)
+    assert np.array_equal(plain.labeling()[0], resv.labeling()[0]) and np.array_equal(plain.flows(), resv.flows())
+    with pytest.raises(pf.PFError):
+        resv.solvers[0].set_reserved_sms(sms)
+    plain.close()
+    resv.close()

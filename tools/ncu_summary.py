@@ -1,13 +1,14 @@
 """Summarise an ncu --set full report (raw page) for the pseudo-flow kernel into profiles/.
-usage: python tools/ncu_summary.py gpurun_out/prof.ncu-rep out.json [algorithmic_bytes_per_launch] [workload] [tile_x tile_y zchunk]"""
+usage: python tools/ncu_summary.py gpurun_out/prof.ncu-rep out.json [algorithmic_bytes_per_launch] [workload] [tile_x tile_y zchunk] [--traffic]"""
 import csv
 import io
 import json
 import subprocess
 import sys
 
-rep, out = sys.argv[1], sys.argv[2]
-alg = float(sys.argv[3]) if len(sys.argv) > 3 else None
+argv = [a for a in sys.argv if a != "--traffic"]
+rep, out = argv[1], argv[2]
+alg = float(argv[3]) if len(argv) > 3 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
@@ -51,8 +52,26 @@ if alg and res:
     summary["dram_bytes_per_launch"] = rb + wb
     summary["algorithmic_bytes_per_launch"] = alg
     summary["traffic_over_algorithmic"] = (rb + wb) / alg
-if len(sys.argv) > 5:
-    summary["workload"] = sys.argv[4]
-    summary["kernel_config"] = [int(v) for v in sys.argv[5:8]]
+if len(argv) > 4:
+    summary["workload"] = argv[4]
+if len(argv) > 5:
+    summary["kernel_config"] = [int(v) for v in argv[5:8]]
+# the source state this capture measured (bench.py reports the traffic only for the same sources)
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+from bench import source_hash  # noqa: E402
+summary["src_hash"] = source_hash()
 json.dump(summary, open(out, "w"), indent=1)
+if "--traffic" in sys.argv and alg and res:
+    # merge into profiles/ncu_traffic.json (one entry per workload + kernel)
+    import os
+    tp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
+    tj = json.load(open(tp)) if os.path.exists(tp) else {}
+    ents = [e for e in tj.get("entries", []) if not (e.get("workload") == summary.get("workload") and
+                                                      e.get("kernel") == res[-1].get("Kernel Name"))]
+    ents.append({"workload": summary.get("workload"), "kernel": res[-1].get("Kernel Name"),
+                 "src_hash": summary["src_hash"], "dram_bytes_per_launch": summary["dram_bytes_per_launch"],
+                 "algorithmic_bytes_per_launch": alg, "traffic_over_algorithmic": summary["traffic_over_algorithmic"],
+                 "gpu__time_duration": res[-1].get("gpu__time_duration.sum"), "report": rep})
+    json.dump({"note": "ncu --set full, one launch each (tools/ncu_summary.py --traffic); bench.py uses an entry only "
+                       "when its src_hash matches the current sources", "entries": ents}, open(tp, "w"), indent=1)
 print(json.dumps(summary, indent=1)[:4000])
