@@ -150,6 +150,18 @@ DESCR = {"C2": "C2: 3D Potts 256^3, K=8, 300 iterations",
          "C5slab": "C5slab: one 8-GPU rank's share of C5 -- 768x768x96, K=16, 200 iterations"}
 
 
+def inputs_sha256(D, kw) -> str:
+    """SHA-256 of the generated inputs of this rank (D volumes, then the capacity field or scalars), logged
+    with every result: the phantoms are regenerated from seeds, so equal hashes = equal inputs."""
+    import numpy as np
+    h = hashlib.sha256()
+    for d in D:
+        h.update(np.ascontiguousarray(d).view(np.uint8))
+    for k in sorted(kw):
+        h.update(np.ascontiguousarray(kw[k], dtype=np.float32).view(np.uint8))
+    return h.hexdigest()
+
+
 def inputs_for_rank(cfg, rank, world, pinned=False):
     """(graph, slab, D list, capacity kwargs) of this rank's z-slab (D covers the slab + the plane above)."""
     import numpy as np
@@ -234,6 +246,7 @@ def time_workload(cfg, rank, world, local_rank, args, iters, steps, warmup, cloc
 
     dev = torch.device("cuda", local_rank)
     g, slab, D, kw = inputs_for_rank(cfg, rank, world)
+    sha = inputs_sha256(D, kw) if rank == 0 else None
     ipc = args.transport == "ipc" and world > 1
     ds = DistSolver(_solver_factory(pf, cfg, g, D, kw, ipc), cfg.nz, rank, world, dev, transport=args.transport)
     del D
@@ -283,7 +296,7 @@ def time_workload(cfg, rank, world, local_rank, args, iters, steps, warmup, cloc
     info = s.kernel_info()
     ds.close()
     V = cfg.nx * cfg.ny * nzl
-    return {"ms": ms, "iter_ms": iter_ms, "info": info, "launches": int(launches), "V": V,
+    return {"ms": ms, "iter_ms": iter_ms, "info": info, "launches": int(launches), "V": V, "inputs_sha256": sha,
             "NF": info["flow_nodes"], "NL": len(g.leaves()), "slab": slab,
             "clocks": clk.summary() if clk else None}
 
@@ -397,6 +410,7 @@ def run_ours(args, rank, world, local_rank):
                        "voxels": cfg.V, "voxels_per_gpu": res["V"], "flow_nodes": res["NF"],
                        "end_labels": res["NL"], "iterations_per_step": iters, "residual_check_every": 10,
                        "value_per_end_label": value * res["NL"] / res["NF"],
+                       "inputs_sha256_rank0": res["inputs_sha256"],
                        "l2": "no flush: per-iteration state >> 126 MB L2 (C4 9.4 GB, C5 33-131 GB per GPU)",
                        "kernel": {k: info[k] for k in ("tile_x", "tile_y", "z_chunk", "threads_per_cta", "ctas",
                                                         "regs_per_thread", "smem_bytes", "ctas_per_sm")}},

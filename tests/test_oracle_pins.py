@@ -103,6 +103,37 @@ def _single_voxel(d_over_c, c=0.25, shift=O.SHIFT_MIN, dag=False):
     return u.ravel()
 
 
+def test_stored_masses_through_first_flow_step():
+    """SPEC S:297 (from Eq. 7, and the listing's flow step on the UNNORMALISED u): the single
+    voxel (0.5, 0.5) with d = (0, c ln 2) stores the masses (0.5, 0.25).  Observed exactly through the first
+    flow step of a 2-voxel line whose other voxel has d = (0, 0) (masses (0.5, 0.5)) and huge capacities:
+    q_L(0) = -c tau (u~_L(1) - u~_L(0)) = -c tau ((0.5, 0.5) - (0.5, 0.25))."""
+    ex = GOLD["single_voxel_update"]
+    c, tau = 0.25, 0.1
+    D = np.zeros((2, 1, 1, 2))
+    D[:, 0, 0, 0] = np.array(ex["d_over_c_times"]) * c
+    S = np.full_like(D, 1e9)
+    u, q = O.init_state(2, 2, (1, 1, 2), 2)
+    O.potts_iterate(D, S, u, q, 2, c, tau, 1)
+    masses0 = np.array(ex["stored_masses"])
+    np.testing.assert_allclose(q[:, 0, 0, 0, 0], -c * tau * (np.array([0.5, 0.5]) - masses0), rtol=1e-14, atol=1e-17)
+    np.testing.assert_allclose(u[:, 0, 0, 0], ex["u1"], rtol=1e-15)
+
+
+def test_buffer_counts_follow_the_paper():
+    """The paper's only quantitative claims are buffer counts (P:309 DAGMF, P:337 Ishikawa, P:5 the 20 % / 30 %
+    reductions).  The golden entries and the BASELINE.md table follow from the stated per-node counts."""
+    for e in GOLD["buffer_counts_3d"]:
+        if e["model"] == "DAGMF":   # pseudo: 5 per end label + 4 per non-end + 1; full: 6 + 7 per non-end + 2
+            assert e["pseudo"] == 5 * e["end"] + 4 * e["nonend"] + 1
+            assert e["full"] == 6 * e["end"] + 7 * e["nonend"] + 2
+        else:                       # Ishikawa: 5N + 2 vs 6N + 1
+            assert (e["pseudo"], e["full"]) == (5 * e["N"] + 2, 6 * e["N"] + 1)
+    # C3 / C4 (6 end labels, 3 internal nodes): 43 vs 59 buffers, 27.1 % fewer (BASELINE.md section 1)
+    p, f = 5 * 6 + 4 * 3 + 1, 6 * 6 + 7 * 3 + 2
+    assert (p, f) == (43, 59) and abs(1 - p / f - 0.271) < 1e-3
+
+
 @pytest.mark.parametrize("dag", [False, True])
 @pytest.mark.parametrize("shift", [O.SHIFT_MIN, O.SHIFT_NONE])
 def test_single_voxel_label_update(dag, shift):
@@ -296,7 +327,7 @@ def test_feasibility_and_weak_duality_every_iteration(name):
         S[v] = inp.s_fields()[v]
     u, q = O.init_state(D.shape[0], g.num_nodes - 1, inp.shape, nd)
     gaps = []
-    for t in range(60):
+    for t in range(200):
         O.run_inputs(inp, 1, state=(u, q))
         assert np.all(u >= 0)
         np.testing.assert_allclose(u.sum(0), 1.0, rtol=0, atol=1e-12)
@@ -310,7 +341,13 @@ def test_feasibility_and_weak_duality_every_iteration(name):
         f = E.dual(q, D, g.num_nodes, g.parent, g.child, g.weight, nd)
         assert e - f >= -1e-9 * abs(e)
         gaps.append(e - f)
-    assert gaps[-1] < 0.5 * gaps[0]
+    # trend (reading R16: the gap is not monotone per step): sampled every 10 iterations it does not grow by
+    # more than 1e-3 G_0, and after 200 iterations it is below 1 % of the first (10 % for the HMF tree, whose
+    # slow convergence SURVEY E5 records: 185 -> 9.4 here)
+    g = np.array(gaps)
+    s10 = g[::10]
+    assert np.all(np.diff(s10) <= 1e-3 * g[0]), s10
+    assert g[-1] < (0.1 if name == "C3s" else 0.01) * g[0], (g[0], g[-1])
 
 
 # ---------------------------------------------------------------- convergence of the fixed point

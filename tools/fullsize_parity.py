@@ -53,6 +53,10 @@ def case(name, shift, threads):
         cfg, slabs = P.config(name), 1
     n = cfg.iters
     inp = P.generate(cfg)
+    import hashlib
+    h = hashlib.sha256(np.ascontiguousarray(inp.D).view(np.uint8))
+    for f in inp.s_fields()[1:]:
+        h.update(np.ascontiguousarray(f).view(np.uint8))
     u, am, q, gpu_s = gpu_run(inp, n, shift, slabs)
     O.set_threads(threads)
     t0 = time.perf_counter()
@@ -71,7 +75,8 @@ def case(name, shift, threads):
             "voxels_du_gt_1e-4": big, "argmax_agree": agree, "voxels": int(cfg.V),
             "pass": bool(du_max <= 1e-4 and dq_max <= 1e-4 and agree >= 0.9999),
             "oracle_s": round(orc_s, 1), "oracle_threads": threads,
-            "oracle_gvl_it_s": round(vl / orc_s / 1e9, 4), "gpu_s_incl_create_and_copies": round(gpu_s, 2)}
+            "oracle_gvl_it_s": round(vl / orc_s / 1e9, 4), "gpu_s_incl_create_and_copies": round(gpu_s, 2),
+            "inputs_sha256": h.hexdigest()}
 
 
 def main():
