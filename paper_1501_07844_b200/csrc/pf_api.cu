@@ -217,6 +217,14 @@ void choose_chunking(pf_solver *s) {
         s->zchunk = nzi > 0 ? (nzi + n - 1) / n : 1;
         const int nch = nzi > 0 ? (nzi + s->zchunk - 1) / s->zchunk : 0;
         s->tiles_x = gx;
+        // tile order (pf_staged.cuh tile_origin): full rows.  Narrower strips (to bring a tile's y-neighbour
+        // closer in the ticket order) measured slower on 768-wide planes: C5slab strips of 12 / 8 / 6 / 4 tiles
+        // 7.15 / 7.21 / 7.32 / 8.77 ms vs 7.10 (full rows of 24), C4 strips of 5: 2.09 vs 1.73 ms (tools/ab.py)
+        s->strip = gx;
+        if (const char *sp = getenv("PF_STRIP")) {   // experiments (tools/ab.py): force the strip width
+            const int want = atoi(sp);
+            if (want > 0) s->strip = std::min(want, gx);
+        }
         s->tiles = (int)tiles;
         s->items_b = (int)(tiles * s->nb);
         s->items = (int)(tiles * (s->nb + nch));
@@ -691,6 +699,7 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check, int reserve_sms)
         sa.nzg = (int)s->nz;
         sa.zchunk = s->zchunk;
         sa.tiles_x = s->tiles_x;
+        sa.strip = s->strip;
         sa.tiles = s->tiles;
         sa.item_begin = ib;
         sa.items = ie;

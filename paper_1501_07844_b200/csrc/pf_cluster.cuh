@@ -160,7 +160,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     cluster_sync_all();
     for (int item = s_item; item < a.items; item = s_item) {
         const int chunk = item / a.tiles, tile = item - chunk * a.tiles;
-        const int x0 = (tile % a.tiles_x) * 32, y0 = (tile / a.tiles_x) * TY;
+        int x0, y0;
+        tile_origin(a, tile, TY, x0, y0);
         const int zc0 = chunk < a.nb ? (chunk == 0 ? a.bplane0 : a.bplane1) : a.zlo + (chunk - a.nb) * a.zchunk;
         const int zc1 = chunk < a.nb ? zc0 + 1 : min(zc0 + a.zchunk, a.zhi);
         const bool has_above = (a.zg0 + zc1) < a.nzg;

@@ -135,6 +135,7 @@ struct pf_solver {
     int staged_smem = 0;
     int s_ch = 0;
     int tiles_x = 0, tiles = 0, items = 0, sgrid = 0;
+    int strip = 1;          // tile-order strip width in tiles (tile_origin)
     // boundary / interior split of the z-chunks (slabs with neighbours; pf_iterate_phase)
     int nb = 0, bplane[2] = {0, 0}, zlo = 0, zhi = 0, items_b = 0;
     int phase_pending = 0;  // 1 after pf_iterate_phase(0) until its phase 1

@@ -56,6 +56,7 @@ struct StagedArgs {
     float *q_out;
     int nx, ny, pitch, nzl, zg0, nzg;
     int zchunk, tiles_x, tiles;
+    int strip;          // tile order inside a z-chunk: column strips of `strip` tiles, row-major inside a strip
     int item_begin, items;  // this launch runs items [item_begin, items)
     // z-chunks: item / tiles < nb: boundary chunk = the single plane bplane[item / tiles] (planes next to
     // a neighbouring slab, computed first so their halo exchange overlaps the rest); otherwise interior
@@ -73,6 +74,20 @@ struct StagedArgs {
 };
 
 __host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
+
+// Tile origin of the t-th tile of a z-chunk.  Tiles are taken in column strips of `strip` tiles (the last
+// strip may be narrower), row-major inside a strip.  The default is one strip of full rows (narrower strips,
+// which bring a tile's y-neighbour closer in the ticket order, measured slower: pf_api.cu choose_chunking).
+__device__ __forceinline__ void tile_origin(const StagedArgs &a, int t, int ty_rows, int &x0, int &y0) {
+    const int tiles_y = a.tiles / a.tiles_x;
+    const int sblk = a.strip * tiles_y;           // tiles per full strip
+    const int sidx = t / sblk;
+    const int w = min(a.strip, a.tiles_x - sidx * a.strip);
+    const int r = t - sidx * sblk;
+    const int ty = r / w;
+    x0 = (sidx * a.strip + (r - ty * w)) * 32;
+    y0 = ty * ty_rows;
+}
 
 template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
 struct StagedLayout {
@@ -247,7 +262,8 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
     __syncthreads();
     for (int item = s_item; item < a.items; item = s_item) {
         const int chunk = item / a.tiles, tile = item - chunk * a.tiles;
-        const int x0 = (tile % a.tiles_x) * 32, y0 = (tile / a.tiles_x) * TY;
+        int x0, y0;
+        tile_origin(a, tile, TY, x0, y0);
         const int zc0 = chunk < a.nb ? (chunk == 0 ? a.bplane0 : a.bplane1) : a.zlo + (chunk - a.nb) * a.zchunk;
         const int zc1 = chunk < a.nb ? zc0 + 1 : min(zc0 + a.zchunk, a.zhi);
         const bool has_above = (a.zg0 + zc1) < a.nzg;
