@@ -114,6 +114,13 @@ typedef struct {
                           * = its flow step; whole volumes, scalar / shared / per-node capacities, <= 16
                           * non-source nodes, no Ishikawa model (else PF_ERR_UNSUPPORTED); no split or
                           * linked iterations. */
+    int32_t u_half;      /* 1: store the labeling state lambda = log2 u as IEEE binary16 instead of fp32
+                          * (reduced-precision storage): 4 B fewer per voxel-label-iteration
+                          * (lambda read + written: 36 -> 32 in 3-D).  Every arithmetic step stays fp32; each stored lambda is
+                          * rounded to nearest binary16, a relative error <= 2^-11 |lambda|, i.e. an absolute
+                          * error in u <= 2^-11 u |ln u| <= 2^-11 / e = 1.8e-4 per store (R25 for the
+                          * re-derived parity bar).  Needs the TMA-staged kernels (PF_ERR_UNSUPPORTED for the
+                          * global-load fallback and the explicit-flow ALM).  0: fp32. */
 } pf_config;
 
 enum { PF_METHOD_PSEUDO_FLOW = 0, PF_METHOD_EXPLICIT_ALM = 1 };
@@ -288,6 +295,7 @@ typedef struct {
     int32_t NF, NL, tile_y, cluster, cur;
     uint8_t inbox[64];                       /* cudaIpcMemHandle_t of the progress inbox */
     uint32_t seq;                            /* protocol steps taken so far */
+    int32_t u_half;                          /* pf_config.u_half of the slab */
 } pf_ipc_slab;
 
 pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out);

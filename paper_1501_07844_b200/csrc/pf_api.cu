@@ -159,7 +159,8 @@ pf_status init_state(pf_solver *s) {
     // u_L = 1/|L|, stored as lambda = log2 u (reading R18)
     const float lam0 = (float)(-std::log2((double)s->gc.NL));
     for (int i = 0; i < 2; ++i) {
-        CK(launch_fill(s->u_alloc[i], nu, lam0, s->stream), "init u");
+        CK(s->cfg.u_half ? launch_fill_half(s->u_alloc[i], nu, lam0, s->stream)
+                         : launch_fill(s->u_alloc[i], nu, lam0, s->stream), "init u");
         s->launches++;
         CK(cudaMemsetAsync(s->q_alloc[i], 0, nq * sizeof(float), s->stream), "init q");
     }
@@ -256,16 +257,18 @@ EncodeTiledFn encode_fn() {
 // 4-D fp32 tensor map over an internal array [plane][channel][y][pitch] (x fastest); elements with
 // x >= nx, y outside [0, ny) or plane outside [0, nplanes) read as 0 (TMA out-of-bounds fill).
 bool encode4d(CUtensorMap *m, const void *base, int64_t nx, int64_t ny, int64_t pitch, int64_t nch, int64_t nplanes,
-              int bx, int by, int bc, bool bf16) {
+              int bx, int by, int bc, int dtype) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
-    const int64_t es_b = bf16 ? 2 : 4;
+    const int64_t es_b = dtype ? 2 : 4;
     cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nch, (cuuint64_t)nplanes};
     cuuint64_t strides[3] = {(cuuint64_t)(pitch * es_b), (cuuint64_t)(pitch * ny * es_b),
                              (cuuint64_t)(pitch * ny * nch * es_b)};
     cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bc, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    return fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)base, dims,
+    return fn(m, dtype == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                                            : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+              4, (void *)base, dims,
               strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -378,6 +381,9 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
                                         "volumes, scalar, shared or per-node capacities only");
 
     if (cfg->ipc && alm) return fail(PF_ERR_UNSUPPORTED, "config: ipc is for the pseudo-flow kernels");
+    if (cfg->u_half != 0 && cfg->u_half != 1) return fail(PF_ERR_INVALID, "config: u_half must be 0 or 1");
+    if (cfg->u_half && (alm || cfg->d_bf16))
+        return fail(PF_ERR_UNSUPPORTED, "config: u_half is for the pseudo-flow kernels with fp32 D");
     pf_solver *s = new pf_solver();
     s->alm = alm;
     s->ipc = cfg->ipc != 0;
@@ -391,7 +397,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     s->z1 = z1;
     s->nzl = z1 - z0;
     // row pitch: 16-byte TMA strides for fp32 (multiple of 4) and, with bf16 D, for bf16 rows (of 8)
-    s->pitch = cfg->d_bf16 ? (dims->nx + 7) / 8 * 8 : (dims->nx + 3) / 4 * 4;
+    s->pitch = (cfg->d_bf16 || cfg->u_half) ? (dims->nx + 7) / 8 * 8 : (dims->nx + 3) / 4 * 4;
     s->P = s->pitch * dims->ny;
     s->gc = gc;
     s->cfg = *cfg;
@@ -403,13 +409,15 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     {
         const char *env = getenv("PF_ITER_KERNEL");
         const bool want_global = env && strcmp(env, "global") == 0;
-        s->staged = !alm && !want_global && staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, &s->sinfo) && encode_fn() != nullptr;
+        s->staged = !alm && !want_global &&
+                    staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, cfg->u_half ? 1 : 0, &s->sinfo) &&
+                    encode_fn() != nullptr;
         // Potts with many labels: the 2-CTA cluster split (scalar / shared capacities; PF_CLUSTER=0 disables)
         const char *cenv = getenv("PF_CLUSTER");
         if (s->staged && gc.model == 0 && gc.NI == 0 && S->kind != PF_S_FIELD_PER_NODE &&
             !(cenv && strcmp(cenv, "0") == 0)) {
             StagedKernelInfo ci{};
-            if (cluster_kernel_lookup(gc.NL, cfg->d_bf16 ? 1 : 0, &ci)) {
+            if (cluster_kernel_lookup(gc.NL, cfg->d_bf16 ? 1 : 0, cfg->u_half ? 1 : 0, &ci)) {
                 s->sinfo = ci;
                 s->cluster = true;
             }
@@ -423,6 +431,10 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
             cudaFuncAttributes fa{};
             cudaFuncGetAttributes(&fa, s->sinfo.func);  // static shared words (work-queue slot) count too
             if (s->staged_smem + (int)fa.sharedSizeBytes > maxsm) s->staged = false;  // e.g. per-node S fields
+        }
+        if (cfg->u_half && !s->staged) {
+            delete s;
+            return fail(PF_ERR_UNSUPPORTED, "config: u_half needs the TMA-staged kernels (not the global-load fallback)");
         }
     }
     cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
@@ -447,14 +459,15 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     for (int i = 0; i < 2; ++i) {
         if (alm && i == 1) {
             s->u_alloc[1] = nullptr;
-        } else if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * sizeof(float), "u", cfg->ipc))
+        } else if ((st = alloc(s, (void **)&s->u_alloc[i], (size_t)((nzl + 2) * NL * P) * ubytes(s), "u", cfg->ipc))
                    != PF_OK) {
             return bail(st);
         }
         if ((st = alloc(s, (void **)&s->q_alloc[i], (size_t)((nzl + 2) * 3 * NF * P) * sizeof(float), "q", cfg->ipc))
             != PF_OK)
             return bail(st);
-        s->u[i] = (alm ? s->u_alloc[0] : s->u_alloc[i]) + NL * P;
+        s->u[i] = reinterpret_cast<float *>(reinterpret_cast<char *>(alm ? s->u_alloc[0] : s->u_alloc[i]) +
+                                            NL * P * ubytes(s));   // plane 0 (storage: fp32 or binary16)
         s->q[i] = s->q_alloc[i] + (int64_t)3 * NF * P;
     }
     if (alm) {
@@ -552,24 +565,27 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         for (int i = 0; i < 2; ++i) {
             ok = ok && encode4d(&s->tm_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 40,
                                 ty + 2, cq);
-            ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 36, ty + 1, cl);
+            // binary16 lambda: 40-element (80-byte) boxes keep the 16-byte box-width rule
+            ok = ok && encode4d(&s->tm_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, cfg->u_half ? 40 : 36,
+                                ty + 1, cl, cfg->u_half ? 2 : 0);
         }
         for (int i = 0; i < 2; ++i) {
             // OSTAGE 2 stores one flow row per warp, OSTAGE 1 the whole tile
             ok = ok && encode4d(&s->tm_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, (int64_t)3 * NF, nzl + 2, 32,
                                 s->sinfo.ostage == 2 ? 1 : ty,
                                 s->sinfo.ostage == 2 ? NF / s->sinfo.groups : (s->cluster ? NL / 2 : 3 * NF));
-            ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, cl);
+            ok = ok && encode4d(&s->tm_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, NL, nzl + 2, 32, ty, cl,
+                                cfg->u_half ? 2 : 0);
         }
         if (s->D16)  // bf16 rows: a 40-element (80-byte) box keeps the 16-byte box-width rule
-            ok = ok && encode4d(&s->tm_D, s->D16, s->nx, s->ny, s->pitch, NL, nzl + 1, 40, ty + 1, cl, true);
+            ok = ok && encode4d(&s->tm_D, s->D16, s->nx, s->ny, s->pitch, NL, nzl + 1, 40, ty + 1, cl, 1);
         else
             ok = ok && encode4d(&s->tm_D, s->D_alloc, s->nx, s->ny, s->pitch, NL, nzl + 1, 36, ty + 1, cl);
         if (s->s_ch) ok = ok && encode4d(&s->tm_S, s->S_alloc, s->nx, s->ny, s->pitch, s->s_ch, nzl, 32, ty, s->s_ch);
         else memset(&s->tm_S, 0, sizeof(s->tm_S));
         if (!ok) return bail(fail(PF_ERR_CUDA, "cuTensorMapEncodeTiled failed"));
-        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * (s->cluster ? NL / 2 : NF) + 36 * (ty + 1) * cl +
-                                      32 * ty * s->s_ch) +
+        s->tx_bytes = (unsigned)(4 * (40 * (ty + 2) * 3 * (s->cluster ? NL / 2 : NF) + 32 * ty * s->s_ch) +
+                                 (cfg->u_half ? 2 * 40 : 4 * 36) * (ty + 1) * cl +
                                  (s->D16 ? 2 * 40 : 4 * 36) * (ty + 1) * cl);
     }
     choose_chunking(s);
@@ -612,13 +628,19 @@ pf_status pf_set_state(pf_solver *s, const float *u, const float *q, int64_t ite
         cudaGraphExecDestroy(s->graph);
         s->graph = nullptr;
     }
-    for (int l = 0; l < NL; ++l)
-        CK(copy_volume(true, s->u[s->cur] + l * P, NL, const_cast<float *>(u) + l * V, s->nx, s->ny, s->pitch, nzl,
-                       s->stream),
-           "upload u");
-    if (!u_is_log2) {   // the labeling itself: lambda = log2 u in place over the owned planes
-        CK(launch_log2_inplace(s->u[s->cur], nzl * NL * P, s->stream), "log2 u");
+    {   // lambda (or u) -> the internal storage, through a stream-ordered device copy for host inputs
+        const float *src = u;
+        float *scratch = nullptr;
+        if (!is_device_ptr(u)) {
+            CK(cudaMallocAsync((void **)&scratch, (size_t)V * NL * sizeof(float), s->stream), "u scratch");
+            CK(cudaMemcpyAsync(scratch, u, (size_t)V * NL * sizeof(float), cudaMemcpyHostToDevice, s->stream), "upload u");
+            src = scratch;
+        }
+        CK(launch_import_u(src, s->u[s->cur], NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, ufmt(s), u_is_log2 ? 0 : 1,
+                           s->stream),
+           "import u");
         s->launches++;
+        if (scratch) cudaFreeAsync(scratch, s->stream);
     }
     for (int p = 0; p < NF && p < NV; ++p) {   // nodes without a stored flow (Ishikawa end labels): not read
         const int v = s->gc.node_of_pos[p];
@@ -964,12 +986,12 @@ pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {
     const int NL = s->gc.NL;
     const int64_t P = s->P, nzl = s->nzl;
     const int64_t V = s->nx * s->ny * nzl;
-    const int ulog = s->alm ? 0 : 1;
+    const int uf = ufmt(s);
     if (u && V > 0) {   // u = 2^lambda into a dense [l][z][y][x] volume (stream-ordered scratch for host outputs)
         const bool dev = is_device_ptr(u);
         float *dst = u;
         if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V * NL * sizeof(float), s->stream), "u scratch");
-        CK(launch_export_u(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, ulog, s->stream),
+        CK(launch_export_u(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, uf, 0, s->stream),
            "export u");
         s->launches++;
         if (!dev) {
@@ -983,7 +1005,7 @@ pf_status pf_get_labeling(pf_solver *s, float *u, uint8_t *argmax) {
         uint8_t *dst = argmax;
         // stream-ordered scratch from the (retained) pool: cudaMalloc / cudaFree would synchronize the device
         if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V, s->stream), "argmax scratch");
-        CK(launch_argmax(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, ulog, s->stream),
+        CK(launch_argmax(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, uf, s->stream),
            "argmax kernel");
         s->launches++;
         if (!dev) {
@@ -1010,7 +1032,7 @@ pf_status pf_get_node_labeling(pf_solver *s, int32_t node, float *u_node) {
     const bool dev = is_device_ptr(u_node);
     float *dst = u_node;
     if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V * sizeof(float), s->stream), "node labeling scratch");
-    CK(launch_node_labeling(s->u[s->cur], dst, w, NL, (int)s->nx, (int)s->ny, (int)s->pitch, s->nzl, s->alm ? 0 : 1,
+    CK(launch_node_labeling(s->u[s->cur], dst, w, NL, (int)s->nx, (int)s->ny, (int)s->pitch, s->nzl, ufmt(s),
                             s->stream),
        "node labeling kernel");
     s->launches++;
@@ -1030,10 +1052,19 @@ pf_status pf_get_state(pf_solver *s, float *u_log2, float *q) {
     const int NL = s->gc.NL;
     const int64_t P = s->P, nzl = s->nzl;
     const int64_t V = s->nx * s->ny * nzl;
-    if (u_log2)
-        for (int l = 0; l < NL; ++l)
-            CK(copy_volume(false, s->u[s->cur] + l * P, NL, u_log2 + l * V, s->nx, s->ny, s->pitch, nzl, s->stream),
+    if (u_log2 && V > 0) {   // lambda as stored (fp32, or binary16 widened exactly)
+        const bool dev = is_device_ptr(u_log2);
+        float *dst = u_log2;
+        if (!dev) CK(cudaMallocAsync((void **)&dst, (size_t)V * NL * sizeof(float), s->stream), "lambda scratch");
+        CK(launch_export_u(s->u[s->cur], dst, NL, (int)s->nx, (int)s->ny, (int)s->pitch, nzl, ufmt(s), 1, s->stream),
+           "export lambda");
+        s->launches++;
+        if (!dev) {
+            CK(cudaMemcpyAsync(u_log2, dst, (size_t)V * NL * sizeof(float), cudaMemcpyDeviceToHost, s->stream),
                "download lambda");
+            cudaFreeAsync(dst, s->stream);
+        }
+    }
     if (q) return pf_get_flows(s, q);
     CK(cudaStreamSynchronize(s->stream), "sync");
     return check_numeric(s);
@@ -1073,7 +1104,7 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
     EnergyArgs a;
     memset(&a, 0, sizeof(a));
     a.u = s->u[s->cur];
-    a.ulog = s->alm ? 0 : 1;
+    a.ufmt = ufmt(s);
     a.q = s->q[s->cur];
     a.D = s->Dptr();
     a.d_bf16 = s->D16 ? 1 : 0;
@@ -1126,7 +1157,7 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     const int64_t V = s->nx * s->ny * s->nzl;
     // per end label: u r/w + D r (+ its flow r/w unless it carries none); per flow-carrying internal node:
     // its flow r/w
-    const int64_t per_leaf = 4 + 4 + (s->D16 ? 2 : 4), per_flow = 8 * s->ndim;
+    const int64_t per_leaf = 2 * ubytes(s) + (s->D16 ? 2 : 4), per_flow = 8 * s->ndim;
     int64_t b = V * (per_leaf * s->gc.NL + per_flow * s->gc.NF);
     if (s->alm && s->gc.NI == 0)  // pass 1: q r/w, p r, u r (+ p_S r); pass 2: q r, D r, p w, u r/w (+ p_S r/w)
         b = V * ((int64_t)s->gc.NL * (8 * s->ndim + 4 + 4 + 4 * s->ndim + (s->D16 ? 2 : 4) + 4 + 8) + 12);

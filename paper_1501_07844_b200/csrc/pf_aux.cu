@@ -12,24 +12,36 @@ __global__ void fill_kernel(float *p, int64_t n, float v) {
         p[i] = v;
 }
 
-// The labeling value of a stored u entry: the pseudo-flow state holds lambda = log2 u (ulog = 1, reading R18),
-// the explicit-flow ALM arm holds u itself (ulog = 0).
-__device__ __forceinline__ float u_value(float v, int ulog) { return ulog ? u_of_log2(v) : v; }
+// The stored label state at element idx: ufmt 0 = u itself in fp32 (explicit-flow ALM arm), 1 = lambda = log2 u
+// in fp32 (pseudo-flow, reading R18), 2 = lambda in binary16 (pf_config.u_half).  raw: lambda itself, else u.
+__device__ __forceinline__ float state_at(const void *u, int64_t idx, int ufmt) {
+    return ufmt == 2 ? __half2float(reinterpret_cast<const __half *>(u)[idx]) : reinterpret_cast<const float *>(u)[idx];
+}
+__device__ __forceinline__ float u_at(const void *u, int64_t idx, int ufmt) {
+    const float v = state_at(u, idx, ufmt);
+    return ufmt ? u_of_log2(v) : v;
+}
+
+__global__ void fill_half_kernel(__half *p, int64_t n, float v) {
+    const __half h = __float2half_rn(v);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = h;
+}
 
 // argmax over end labels, lowest label id wins ties ("thresholded"); compared on the same
 // u values pf_get_labeling exports.
-__global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__ out, int NL, int nx, int ny,
-                              int pitch, int64_t nz, int ulog) {
+__global__ void argmax_kernel(const void *__restrict__ u, uint8_t *__restrict__ out, int NL, int nx, int ny,
+                              int pitch, int64_t nz, int ufmt) {
     const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = i / ((int64_t)nx * ny);
         const int r = (int)(i - z * (int64_t)nx * ny);
         const int y = r / nx, x = r - y * nx;
-        const float *b = u + z * NL * P + (int64_t)y * pitch + x;
-        float best = u_value(b[0], ulog);
+        const int64_t b = z * NL * P + (int64_t)y * pitch + x;
+        float best = u_at(u, b, ufmt);
         int arg = 0;
         for (int l = 1; l < NL; ++l) {
-            const float v = u_value(b[l * P], ulog);
+            const float v = u_at(u, b + l * P, ufmt);
             if (v > best) { best = v; arg = l; }
         }
         out[i] = (uint8_t)arg;
@@ -38,17 +50,17 @@ __global__ void argmax_kernel(const float *__restrict__ u, uint8_t *__restrict__
 
 // Labeling of any node: u_v(x) = sum_B W_(v,B) u_B(x) over the end labels B (path weights P:199-209),
 // written densely as [z][y][x] (x fastest).
-__global__ void node_labeling_kernel(const float *__restrict__ u, float *__restrict__ out, NodeWeights w, int NL,
-                                     int nx, int ny, int pitch, int64_t nz, int ulog) {
+__global__ void node_labeling_kernel(const void *__restrict__ u, float *__restrict__ out, NodeWeights w, int NL,
+                                     int nx, int ny, int pitch, int64_t nz, int ufmt) {
     const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = i / ((int64_t)nx * ny);
         const int r = (int)(i - z * (int64_t)nx * ny);
         const int y = r / nx, x = r - y * nx;
-        const float *b = u + z * NL * P + (int64_t)y * pitch + x;
+        const int64_t b = z * NL * P + (int64_t)y * pitch + x;
         float acc = 0.f;
         for (int l = 0; l < NL; ++l)
-            if (w.W[l] != 0.f) acc = fmaf(w.W[l], u_value(b[l * P], ulog), acc);
+            if (w.W[l] != 0.f) acc = fmaf(w.W[l], u_at(u, b + l * P, ufmt), acc);
         out[i] = acc;
     }
 }
@@ -71,11 +83,11 @@ struct NodeVals {
     float v[kMaxNodes];
 };
 
-__device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, int64_t P, float *out) {
+__device__ __forceinline__ void labels_at(const EnergyArgs &a, int64_t ub, int64_t P, float *out) {
     // u_v for every position: end labels read, internal by bottom-up sums (Eq. 9);
     // Ishikawa chain: u_{N_i} = sum_{j >= i} u_{L_j}
     const int NV = a.NV, NI = a.NI;
-    for (int l = 0; l < a.NL; ++l) out[NI + l] = u_value(ub[l * P], a.ulog);
+    for (int l = 0; l < a.NL; ++l) out[NI + l] = u_at(a.u, ub + l * P, a.ufmt);
     if (a.model == 1) {
         double acc = 0.0;
         for (int f = NI - 1; f >= 0; --f) {
@@ -91,24 +103,37 @@ __device__ __forceinline__ void labels_at(const EnergyArgs &a, const float *ub, 
     }
 }
 
-// Export of the labeling (pf_get_labeling): internal [z][l][y][pitch] (log2 u or u) -> dense [l][z][y][x] u.
-__global__ void export_u_kernel(const float *__restrict__ u, float *__restrict__ out, int NL, int nx, int ny,
-                                int pitch, int64_t nz, int ulog) {
+// Export of the label state: internal [z][l][y][pitch] -> dense [l][z][y][x] fp32: the labeling u
+// (pf_get_labeling) or, raw = 1, the stored lambda itself (pf_get_state).
+__global__ void export_u_kernel(const void *__restrict__ u, float *__restrict__ out, int NL, int nx, int ny,
+                                int pitch, int64_t nz, int ufmt, int raw) {
     const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = i / ((int64_t)nx * ny);
         const int r = (int)(i - z * (int64_t)nx * ny);
         const int y = r / nx, x = r - y * nx;
-        const float *b = u + z * NL * P + (int64_t)y * pitch + x;
-        for (int l = 0; l < NL; ++l) out[l * V + i] = u_value(b[l * P], ulog);
+        const int64_t b = z * NL * P + (int64_t)y * pitch + x;
+        for (int l = 0; l < NL; ++l) out[l * V + i] = raw ? state_at(u, b + l * P, ufmt) : u_at(u, b + l * P, ufmt);
     }
 }
 
-// pf_set_state with a linear u: lambda = log2 u in place over n internal values (correctly rounded log2f;
-// u = 0 gives -inf, a label that is exactly dead)
-__global__ void log2_inplace_kernel(float *p, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = log2f(p[i]);
+// Import of a label state (pf_set_state): dense [l][z][y][x] fp32 on the device -> internal storage.  linear = 1:
+// the labeling u itself, lambda = log2 u (correctly rounded log2f; u = 0 gives -inf, a label that is exactly
+// dead); else lambda.  Stored as fp32 or (ufmt 2) rounded to nearest binary16.
+__global__ void import_u_kernel(const float *__restrict__ in, void *__restrict__ u, int NL, int nx, int ny, int pitch,
+                                int64_t nz, int ufmt, int linear) {
+    const int64_t V = (int64_t)nx * ny * nz, P = (int64_t)pitch * ny;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / ((int64_t)nx * ny);
+        const int r = (int)(i - z * (int64_t)nx * ny);
+        const int y = r / nx, x = r - y * nx;
+        const int64_t b = z * NL * P + (int64_t)y * pitch + x;
+        for (int l = 0; l < NL; ++l) {
+            const float v = linear ? log2f(in[l * V + i]) : in[l * V + i];
+            if (ufmt == 2) reinterpret_cast<__half *>(u)[b + l * P] = __float2half_rn(v);
+            else reinterpret_cast<float *>(u)[b + l * P] = v;
+        }
+    }
 }
 
 __global__ void f32_to_bf16_kernel(const float *__restrict__ src, uint16_t *__restrict__ dst, int64_t n) {
@@ -130,20 +155,20 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
         const int64_t zg = a.zg0 + z;
         // ---- primal: sum_L D_L u_L + sum_v S_v |nabla u_v|
         float uc[2 * kMaxNodes], un[2 * kMaxNodes];
-        labels_at(a, a.u + z * ups + pix, P, uc);
+        labels_at(a, z * ups + pix, P, uc);
         for (int l = 0; l < NL; ++l) e_acc += (double)load_D(a.D, z * ups + l * P + pix, a.d_bf16) * (double)uc[NI + l];
         double g2[2 * kMaxNodes], g1[2 * kMaxNodes];
         for (int v = 0; v < NV; ++v) { g2[v] = 0.0; g1[v] = 0.0; }
         if (x < a.nx - 1) {
-            labels_at(a, a.u + z * ups + pix + 1, P, un);
+            labels_at(a, z * ups + pix + 1, P, un);
             for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
         }
         if (y < a.ny - 1) {
-            labels_at(a, a.u + z * ups + pix + a.pitch, P, un);
+            labels_at(a, z * ups + pix + a.pitch, P, un);
             for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
         }
         if (a.ndim == 3 && zg < a.nzg - 1) {
-            labels_at(a, a.u + (z + 1) * ups + pix, P, un);
+            labels_at(a, (z + 1) * ups + pix, P, un);
             for (int v = 0; v < NV; ++v) { double g = (double)un[v] - uc[v]; g2[v] += g * g; g1[v] += fabs(g); }
         }
         for (int v = 0; v < NF; ++v) {  // nodes without a flow have zero capacity
@@ -206,20 +231,26 @@ cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz, int ulog,
+cudaError_t launch_argmax(const void *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz, int ufmt,
                           cudaStream_t st) {
-    argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz, ulog);
+    argmax_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz, ufmt);
     return cudaGetLastError();
 }
 
-cudaError_t launch_export_u(const float *u, float *out, int NL, int nx, int ny, int pitch, int64_t nz, int ulog,
+cudaError_t launch_export_u(const void *u, float *out, int NL, int nx, int ny, int pitch, int64_t nz, int ufmt, int raw,
                             cudaStream_t st) {
-    export_u_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz, ulog);
+    export_u_kernel<<<1184, 256, 0, st>>>(u, out, NL, nx, ny, pitch, nz, ufmt, raw);
     return cudaGetLastError();
 }
 
-cudaError_t launch_log2_inplace(float *p, int64_t n, cudaStream_t st) {
-    log2_inplace_kernel<<<1184, 256, 0, st>>>(p, n);
+cudaError_t launch_import_u(const float *in, void *u, int NL, int nx, int ny, int pitch, int64_t nz, int ufmt,
+                            int linear, cudaStream_t st) {
+    import_u_kernel<<<1184, 256, 0, st>>>(in, u, NL, nx, ny, pitch, nz, ufmt, linear);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_half(void *p, int64_t n, float v, cudaStream_t st) {
+    fill_half_kernel<<<1184, 256, 0, st>>>(reinterpret_cast<__half *>(p), n, v);
     return cudaGetLastError();
 }
 
@@ -228,9 +259,9 @@ cudaError_t launch_f32_to_bf16(const float *src, uint16_t *dst, int64_t n, cudaS
     return cudaGetLastError();
 }
 
-cudaError_t launch_node_labeling(const float *u, float *out, const NodeWeights &w, int NL, int nx, int ny, int pitch,
-                                 int64_t nz, int ulog, cudaStream_t st) {
-    node_labeling_kernel<<<1184, 256, 0, st>>>(u, out, w, NL, nx, ny, pitch, nz, ulog);
+cudaError_t launch_node_labeling(const void *u, float *out, const NodeWeights &w, int NL, int nx, int ny, int pitch,
+                                 int64_t nz, int ufmt, cudaStream_t st) {
+    node_labeling_kernel<<<1184, 256, 0, st>>>(u, out, w, NL, nx, ny, pitch, nz, ufmt);
     return cudaGetLastError();
 }
 

@@ -8,8 +8,8 @@
 namespace pf {
 
 struct EnergyArgs {
-    const float *u;   // current u, plane 0 (the plane above the slab must be current for the primal)
-    int ulog;         // 1: u holds log2 u (pseudo-flow state), 0: u itself (explicit-flow ALM)
+    const void *u;    // current label state, plane 0 (the plane above the slab must be current for the primal)
+    int ufmt;         // 0: u itself fp32 (explicit-flow ALM), 1: log2 u fp32, 2: log2 u binary16 (u_half)
     const float *q;   // current q, plane 0 (the plane below must be current for the dual)
     const void *D;    // fp32, or bf16 when d_bf16
     const float *S;
@@ -29,13 +29,15 @@ struct NodeWeights {
 };
 
 cudaError_t launch_fill(float *p, int64_t n, float v, cudaStream_t st);
-cudaError_t launch_node_labeling(const float *u, float *out, const NodeWeights &w, int NL, int nx, int ny, int pitch,
-                                 int64_t nz, int ulog, cudaStream_t st);
-cudaError_t launch_argmax(const float *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz, int ulog,
+cudaError_t launch_node_labeling(const void *u, float *out, const NodeWeights &w, int NL, int nx, int ny, int pitch,
+                                 int64_t nz, int ufmt, cudaStream_t st);
+cudaError_t launch_argmax(const void *u, uint8_t *out, int NL, int nx, int ny, int pitch, int64_t nz, int ufmt,
                           cudaStream_t st);
-cudaError_t launch_export_u(const float *u, float *out, int NL, int nx, int ny, int pitch, int64_t nz, int ulog,
+cudaError_t launch_export_u(const void *u, float *out, int NL, int nx, int ny, int pitch, int64_t nz, int ufmt, int raw,
                             cudaStream_t st);
-cudaError_t launch_log2_inplace(float *p, int64_t n, cudaStream_t st);
+cudaError_t launch_import_u(const float *in, void *u, int NL, int nx, int ny, int pitch, int64_t nz, int ufmt,
+                            int linear, cudaStream_t st);
+cudaError_t launch_fill_half(void *p, int64_t n, float v, cudaStream_t st);
 cudaError_t launch_f32_to_bf16(const float *src, uint16_t *dst, int64_t n, cudaStream_t st);
 cudaError_t launch_check_nonneg(const float *p, int64_t n, unsigned int *flag, cudaStream_t st);
 cudaError_t launch_energy(const EnergyArgs &a, double *partial, int nblocks, double *out, cudaStream_t st);

@@ -71,7 +71,7 @@ struct ClusterLayout {
 };
 
 // tm_q / tm_u / tm_D / tm_uo / tm_qo boxes have NL/2 channels here; q channel of (k, label) = k*NL + label.
-template <int NL, int TY, int DBF>
+template <int NL, int TY, int DBF, int UH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     pf_iter_cluster(const __grid_constant__ StagedArgs a) {
     using CL = ClusterLayout<NL, TY, DBF>;
@@ -251,7 +251,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                                                                                               ly * 40 + (lx < 0 ? 0 : lx)]);
                     else Dv = Db[v * UCS + uoff];
                     dl[v] = Dv + dq;                        // Potts: d_L = D_L + div q_L
-                    uold[v] = Ub[v * UCS + uoff];
+                    if constexpr (UH) uold[v] = __half2float(reinterpret_cast<const __half *>(Ub)[v * (UROWS * 40) +
+                                                                                                  ly * 40 + (lx < 0 ? 0 : lx)]);
+                    else uold[v] = Ub[v * UCS + uoff];
                 }
                 label_half<NLC>(dl, uold, rr, ut, a.shift, k2, mh, th, sh);
             }
@@ -276,10 +278,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                         atomicMin(a.err_voxel, vox);
                     }
                     float *uo = Uo + (p & 1) * L::UOSZ + ly * 32 + lx;
+                    __half *uoh = reinterpret_cast<__half *>(Uo + (p & 1) * L::UOSZ) + ly * 32 + lx;
 #pragma unroll
                     for (int v = 0; v < NLC; ++v) {
-                        const float ln = rr[v] + ch;
-                        uo[v * TY * 32] = ln;
+                        float ln = rr[v] + ch;
+                        if constexpr (UH) {   // stored as binary16: the residual sees the stored value
+                            ln = round_state_half(ln);
+                            uoh[v * TY * 32] = __float2half_rn(ln);
+                        } else {
+                            uo[v * TY * 32] = ln;
+                        }
                         if (a.check) resid = fmaxf(resid, fabsf(u_of_log2(ln) - u_of_log2(uold[v])));
                     }
                 }
@@ -338,6 +346,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     }
 }
 
-bool cluster_kernel_lookup(int NL, int DBF, StagedKernelInfo *info);
+bool cluster_kernel_lookup(int NL, int DBF, int UH, StagedKernelInfo *info);
 
 }  // namespace pf

@@ -155,6 +155,9 @@ pf_status cuda_fail(pf_solver *s, cudaError_t e, const char *what);
     } while (0)
 
 inline int64_t ups(const pf_solver *s) { return (int64_t)s->gc.NL * s->P; }
+// label state storage: 0 u fp32 (explicit-flow ALM), 1 lambda = log2 u fp32, 2 lambda binary16 (pf_config.u_half)
+inline int ufmt(const pf_solver *s) { return s->alm ? 0 : (s->cfg.u_half ? 2 : 1); }
+inline int64_t ubytes(const pf_solver *s) { return s->cfg.u_half ? 2 : 4; }
 // q always carries 3 components internally (q^z == 0 for 2-D volumes), so the kernels need no ndim branch
 inline int64_t qps(const pf_solver *s) { return (int64_t)3 * s->gc.NF * s->P; }
 
@@ -169,7 +172,8 @@ int phase1_grid(const pf_solver *s);
 pf_status ipc_wait_neighbours(pf_solver *s, uint32_t seq);
 bool stream_mem_ops();
 pf_status ipc_announce(pf_solver *s, uint32_t seq);
+// dtype: 0 fp32, 1 bf16, 2 fp16 (binary16)
 bool encode4d(CUtensorMap *m, const void *base, int64_t nx, int64_t ny, int64_t pitch, int64_t nch, int64_t nplanes,
-              int bx, int by, int bc, bool bf16 = false);
+              int bx, int by, int bc, int dtype = 0);
 
 }  // namespace pfi

@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cstring>
 
+#include <cuda_fp16.h>
+
 namespace pf {
 
 constexpr float kLog2e = 1.4426950408889634f;
@@ -53,6 +55,14 @@ __device__ __forceinline__ float load_D(const void *D, int64_t i, int bf16) {
 }
 
 // Streaming (evict-first) store: the new state is not re-read in this launch, keep it out of L2's way.
+__device__ __forceinline__ void st_stream_h(__half *p, __half v) {
+    asm volatile("st.global.cs.b16 [%0], %1;" ::"l"(p), "h"(__half_as_ushort(v)) : "memory");
+}
+
+// Stored label state (pf_config.u_half): lambda = log2 u rounded to nearest binary16 once per store; the
+// arithmetic stays fp32.  round_state gives the value the next iteration will read back.
+__device__ __forceinline__ float round_state_half(float lam) { return __half2float(__float2half_rn(lam)); }
+
 __device__ __forceinline__ void st_stream(float *p, float v) {
     asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }

@@ -62,8 +62,9 @@ pf_status pf_halo_regions(pf_solver *s, pf_halo *h) {
     memset(h, 0, sizeof(*h));
     const int NV = s->gc.NF;  // flow-carrying nodes
     const int64_t P = s->P, nzl = s->nzl;
-    float *u = s->u[s->cur], *q = s->q[s->cur];
-    h->bytes_u = ups(s) * (int64_t)sizeof(float);
+    char *u = reinterpret_cast<char *>(s->u[s->cur]);   // label state: fp32 or binary16 elements
+    float *q = s->q[s->cur];
+    h->bytes_u = ups(s) * ubytes(s);
     h->bytes_q = qps(s) * (int64_t)sizeof(float);
     h->bytes_qz = s->ndim == 3 ? (int64_t)NV * P * (int64_t)sizeof(float) : 0;
     if (s->z0 > 0) {  // neighbour below exists
@@ -72,7 +73,7 @@ pf_status pf_halo_regions(pf_solver *s, pf_halo *h) {
         if (s->ndim == 3) h->recv_down_qz = q - qps(s) + 2 * NV * P;
     }
     if (s->z1 < s->nz) {  // neighbour above exists
-        h->recv_up_u = u + nzl * ups(s);
+        h->recv_up_u = u + nzl * ups(s) * ubytes(s);
         h->recv_up_q = q + nzl * qps(s);
         if (s->ndim == 3) h->send_up_qz = q + (nzl - 1) * qps(s) + 2 * NV * P;
     }
@@ -87,7 +88,8 @@ pf_status pf_exchange_local(pf_solver *const *solvers, int32_t n) {
     }
     for (int i = 0; i + 1 < n; ++i) {
         pf_solver *lo = solvers[i], *hi = solvers[i + 1];
-        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->gc.NF != hi->gc.NF)
+        if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->gc.NF != hi->gc.NF ||
+            lo->cfg.u_half != hi->cfg.u_half)
             return fail(PF_ERR_INVALID, "exchange: solvers %d and %d are not consecutive slabs of one volume", i, i + 1);
     }
     // order: every receiver waits for every sender's pending work, copies on the receiver's stream,
@@ -152,6 +154,7 @@ pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n) {
         const pf_solver *lo = solvers[i], *hi = solvers[i + 1];
         if (lo->z1 != hi->z0 || lo->nx != hi->nx || lo->ny != hi->ny || lo->pitch != hi->pitch ||
             lo->gc.NF != hi->gc.NF || lo->gc.NL != hi->gc.NL || lo->cluster != hi->cluster || lo->cur != hi->cur ||
+            lo->cfg.u_half != hi->cfg.u_half ||
             lo->sinfo.tile_y != hi->sinfo.tile_y)
             return fail(PF_ERR_INVALID, "link: solvers %d and %d are not consecutive slabs of one volume in step", i,
                         i + 1);
@@ -185,7 +188,8 @@ pf_status pf_link_slabs(pf_solver *const *solvers, int32_t n) {
         for (int b = 0; b < 2; ++b) {
             if (s->nb_below) {   // below neighbour's buffers: its upper halo plane receives our plane 0
                 const pf_solver *t = s->nb_below;
-                ok = ok && encode4d(&s->tm_uo_nb[b], t->u_alloc[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl);
+                ok = ok && encode4d(&s->tm_uo_nb[b], t->u_alloc[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl,
+                                    t->cfg.u_half ? 2 : 0);
                 ok = ok && encode4d(&s->tm_qo_nb[b], t->q_alloc[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2,
                                     32, ty, cq);
             }
@@ -309,6 +313,7 @@ pf_status pf_ipc_export(pf_solver *s, pf_ipc_slab *out) {
     out->cluster = s->cluster ? 1 : 0;
     out->cur = s->cur;
     out->seq = s->ipc_seq;
+    out->u_half = s->cfg.u_half;
     return PF_OK;
 }
 
@@ -325,7 +330,8 @@ pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab 
         if (!t) continue;
         const bool adjacent = side == 0 ? t->z0 + t->nzl == s->z0 : t->z0 == s->z1;
         if (!adjacent || t->nx != s->nx || t->ny != s->ny || t->pitch != s->pitch || t->NF != NF || t->NL != NL ||
-            t->tile_y != ty || t->cluster != (s->cluster ? 1 : 0) || t->cur != s->cur || t->seq != s->ipc_seq)
+            t->tile_y != ty || t->cluster != (s->cluster ? 1 : 0) || t->cur != s->cur || t->seq != s->ipc_seq ||
+            t->u_half != s->cfg.u_half)
             return fail(PF_ERR_INVALID, "ipc_link: the %s blob is not this slab's neighbour in step",
                         side == 0 ? "below" : "above");
         void *ub[2] = {nullptr, nullptr}, *qb[2] = {nullptr, nullptr}, *ib = nullptr;
@@ -345,7 +351,8 @@ pf_status pf_ipc_link(pf_solver *s, const pf_ipc_slab *below, const pf_ipc_slab 
         bool ok = true;
         for (int b = 0; b < 2; ++b) {
             if (side == 0) {   // below: its upper halo plane receives our plane 0
-                ok = ok && encode4d(&s->tm_uo_nb[b], ub[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl);
+                ok = ok && encode4d(&s->tm_uo_nb[b], ub[b], t->nx, t->ny, t->pitch, NL, t->nzl + 2, 32, ty, cl,
+                                    t->u_half ? 2 : 0);
                 ok = ok && encode4d(&s->tm_qo_nb[b], qb[b], t->nx, t->ny, t->pitch, (int64_t)3 * NF, t->nzl + 2, 32,
                                     ty, cq);
             } else {           // above: its lower halo plane receives our last q^z

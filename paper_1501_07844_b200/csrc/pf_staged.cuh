@@ -176,8 +176,10 @@ __device__ __forceinline__ void stage_row_acquire(int lane, int since) {
     __syncwarp();
 }
 
-// DBF: D stored as bf16 (pf_config.d_bf16; the D stage then holds rows of 40 bf16)
-template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF>
+// DBF: D stored as bf16 (pf_config.d_bf16; the D stage then holds rows of 40 bf16).
+// UH: lambda = log2 u stored as binary16 (pf_config.u_half; the u stage then holds rows of 40 halves, the u
+// staging tile halves [l][row][32]).
+template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF, int UH>
 __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
     constexpr int NF = L::NF;
@@ -376,8 +378,15 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
 #pragma unroll
                     for (int l = 0; l < NLG; ++l) Dv[l] = Db[(l0 + l) * UCS + uoff];
                 }
+                if constexpr (UH) {
+                    const __half *Uh = reinterpret_cast<const __half *>(Ub);
+                    const int hoff = ly * 40 + (lx < 0 ? 0 : lx);
 #pragma unroll
-                for (int l = 0; l < NLG; ++l) uold[l] = Ub[(l0 + l) * UCS + uoff];
+                    for (int l = 0; l < NLG; ++l) uold[l] = __half2float(Uh[(l0 + l) * (UROWS * 40) + hoff]);
+                } else {
+#pragma unroll
+                    for (int l = 0; l < NLG; ++l) uold[l] = Ub[(l0 + l) * UCS + uoff];
+                }
             }
             float sum = 1.f;
             if constexpr (G == 1) {
@@ -412,6 +421,10 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                     ut[l] *= gh;
                 }
             }
+            if constexpr (UH) {   // the stored (binary16) state is what the next iteration reads: round once here
+#pragma unroll
+                for (int l = 0; l < NLG; ++l) un[l] = round_state_half(un[l]);
+            }
             if (lx >= 0) {
                 if (p < zc1 && is_main && valid) {
                     if (grp == 0 && label_sum_bad(sum)) {
@@ -419,9 +432,19 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                         atomicMin(a.err_voxel, vox);
                     }
                     if (OSTAGE) {
-                        float *uo = Uo + (p & 1) * L::UOSZ + l0 * TY * 32 + ly * 32 + lx;
+                        if constexpr (UH) {
+                            __half *uo = reinterpret_cast<__half *>(Uo + (p & 1) * L::UOSZ) + l0 * TY * 32 + ly * 32 + lx;
 #pragma unroll
-                        for (int l = 0; l < NLG; ++l) uo[l * TY * 32] = un[l];
+                            for (int l = 0; l < NLG; ++l) uo[l * TY * 32] = __float2half_rn(un[l]);
+                        } else {
+                            float *uo = Uo + (p & 1) * L::UOSZ + l0 * TY * 32 + ly * 32 + lx;
+#pragma unroll
+                            for (int l = 0; l < NLG; ++l) uo[l * TY * 32] = un[l];
+                        }
+                    } else if constexpr (UH) {
+                        __half *uo = reinterpret_cast<__half *>(a.u_out) + (int64_t)p * ups + l0 * P + pix;
+#pragma unroll
+                        for (int l = 0; l < NLG; ++l) st_stream_h(uo + l * (int)P, __float2half_rn(un[l]));
                     } else {
                         float *uo = a.u_out + (int64_t)p * ups + l0 * P + pix;
 #pragma unroll
@@ -511,6 +534,6 @@ struct StagedKernelInfo {
     int groups;      // label groups per row (G)
 };
 
-bool staged_kernel_lookup(int NI, int NL, int MODEL, int DBF, StagedKernelInfo *info);
+bool staged_kernel_lookup(int NI, int NL, int MODEL, int DBF, int UH, StagedKernelInfo *info);
 
 }  // namespace pf

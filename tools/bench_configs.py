@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--d-bf16", action="store_true", help="store D as bf16 (pf_config.d_bf16)")
     ap.add_argument("--alm", action="store_true", help="explicit-flow ALM comparison arm (Potts configs)")
+    ap.add_argument("--u-half", action="store_true", help="lambda = log2 u stored as binary16 (pf_config.u_half)")
+    ap.add_argument("--linf", action="store_true", help="anisotropic capacities: the l-inf box (dual of l1-TV)")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -50,7 +52,7 @@ def main():
             kw = {"s_shared": torch.from_numpy(inp.s_field).to(dev)}
         else:
             kw = {"s_scalars": inp.s_scalars}
-        extra = {"d_bf16": args.d_bf16}
+        extra = {"d_bf16": args.d_bf16, "u_half": args.u_half, "cap": pf.PF_CAP_LINF if args.linf else pf.PF_CAP_L2}
         c, tau = cfg.c, cfg.tau
         if args.alm:
             extra["method"] = pf.PF_METHOD_EXPLICIT_ALM
@@ -89,7 +91,8 @@ def main():
         e, f = s.energy()
         s.close()
         line = {"config": name, "method": "explicit-flow ALM" if args.alm else "pseudo-flow",
-                "d_dtype": "bf16" if args.d_bf16 else "f32",
+                "d_dtype": "bf16" if args.d_bf16 else "f32", "u_storage": "binary16 lambda" if args.u_half else "f32 lambda",
+                "capacity": "linf" if args.linf else "l2",
                 "dims": [cfg.nx, cfg.ny, cfg.nz], "end_labels": NL, "nodes": g.num_nodes - 1,
                 "iterations": n, "ms_per_solve": ms, "ms_per_iteration": it_ms,
                 "gvl_it_per_s": V * NL * n / (ms / 1e3) / 1e9,

@@ -4,6 +4,7 @@ follow the paper-exact fp64 oracle (u_floor = 0) on the HMF (C3) shapes where la
 Three fp32 storage/arithmetic variants of the label update (P:290-293 / Eq. 15), everything else fp32:
   flush  -- normalised u < FLT_MIN set to 0 and exp results flushed (round-1 kernel: ex2.approx.ftz + floor)
   subn   -- IEEE fp32 with subnormals kept (no FTZ anywhere)
+  log2T16 -- log2T with the stored lambda rounded to binary16 (pf_config.u_half)
   log2   -- u stored as lambda = log2 u in fp32; u~ = 2^(lambda + (m - d) log2(e)/c) for the sums/masses,
             lambda' = lambda + (m - d) log2(e)/c - log2(a)  (no underflow of the stored state)
 usage: PYTHONPATH=. python tools/fp32_underflow_study.py [C3 33 17 9 300 0] ...
@@ -74,13 +75,15 @@ def run32(inp, n, shift, mode):
                 ut = exp2_f32(t, False)
                 a = ut.sum(0, dtype=f32)
                 lam = (t - np.log2(a.astype(np.float64)).astype(f32)).astype(f32)
-            elif mode == "log2T":   # the kernel's form: max shift T, e = 2^(t-T) in (0,1], s = sum e in [1,K]
+            elif mode in ("log2T", "log2T16"):   # the kernel's form: max shift T, e = 2^(t-T) in (0,1], s = sum e in [1,K]
                 t = np.stack([lam[s_] + (m - d[v]) * k2 for s_, v in enumerate(leaves)]).astype(f32)
                 T = t.max(0)
                 r = (t - T).astype(f32)
                 e = exp2_f32(r, True)
                 s = e.sum(0, dtype=f32)
                 lam = (r - np.log2(s.astype(np.float64)).astype(f32)).astype(f32)
+                if mode == "log2T16":   # pf_config.u_half: the stored lambda rounded to binary16
+                    lam = lam.astype(np.float16).astype(f32)
                 ut = (e * exp2_f32(T, True)).astype(f32)
             else:
                 fl = mode == "flush"
