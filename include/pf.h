@@ -121,6 +121,14 @@ typedef struct {
                           * error in u <= 2^-11 u |ln u| <= 2^-11 / e = 1.8e-4 per store (R25 for the
                           * re-derived parity bar).  Needs the TMA-staged kernels (PF_ERR_UNSUPPORTED for the
                           * global-load fallback and the explicit-flow ALM).  0: fp32. */
+    int32_t tblock;      /* 2: temporal blocking -- TWO iterations per HBM pass: pf_iterate runs
+                          * pairs of iterations in one fused launch that keeps iteration t's flows, labels and
+                          * masses on chip for iteration t + 1 (an odd remainder runs as one ordinary iteration);
+                          * bitwise the same results as tblock = 0.  Supported for Potts models with 2..4 labels
+                          * on whole volumes with scalar or shared-field capacities and fp32 storage
+                          * (PF_ERR_UNSUPPORTED otherwise: the on-chip state of larger graphs does not fit the
+                          * 227 KB of shared memory per CTA).  0 (default): one iteration
+                          * per pass. */
 } pf_config;
 
 enum { PF_METHOD_PSEUDO_FLOW = 0, PF_METHOD_EXPLICIT_ALM = 1 };
@@ -314,6 +322,7 @@ typedef struct {
     int32_t flow_nodes;                      /* nodes whose spatial flow is stored */
     int32_t cluster;                         /* 1: labels split over a 2-CTA cluster (pf_iter_cluster) */
     int32_t phase1_ctas;                     /* grid of a pf_iterate_phase(1) launch (see pf_set_reserved_sms) */
+    int32_t tblock;                          /* iterations per HBM pass of pf_iterate (1 or 2, pf_config.tblock) */
 } pf_kernel_info;
 
 pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info);

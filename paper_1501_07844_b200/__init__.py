@@ -58,7 +58,7 @@ class pf_smoothness(ctypes.Structure):
 class pf_config(ctypes.Structure):
     _fields_ = [("c", ctypes.c_float), ("tau", ctypes.c_float), ("cap", ctypes.c_int32), ("shift", ctypes.c_int32),
                 ("check_every", ctypes.c_int32), ("d_bf16", ctypes.c_int32), ("ipc", ctypes.c_int32),
-                ("method", ctypes.c_int32), ("u_half", ctypes.c_int32)]
+                ("method", ctypes.c_int32), ("u_half", ctypes.c_int32), ("tblock", ctypes.c_int32)]
 
 
 class pf_ipc_slab(ctypes.Structure):
@@ -87,7 +87,7 @@ class pf_kernel_info(ctypes.Structure):
                 ("algorithmic_bytes_per_iteration", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("staged", ctypes.c_int32), ("work_items", ctypes.c_int32),
                 ("model", ctypes.c_int32), ("flow_nodes", ctypes.c_int32), ("cluster", ctypes.c_int32),
-                ("phase1_ctas", ctypes.c_int32)]
+                ("phase1_ctas", ctypes.c_int32), ("tblock", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p
@@ -182,7 +182,8 @@ def pf_last_error() -> str:
 def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, weight, D: Sequence, s_kind: int, s_scalars=None,
               s_fields: Optional[Sequence] = None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2,
               shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None,
-              d_bf16: bool = False, method: int = 0, ipc: bool = False, u_half: bool = False) -> int:
+              d_bf16: bool = False, method: int = 0, ipc: bool = False, u_half: bool = False,
+              tblock: int = 0) -> int:
     """pf_create.  dims = (nx, ny, nz) global.  D: one float32 volume per end label (node-id order)
     covering the slab plus the plane above it.  Returns the opaque solver handle."""
     nx, ny, nz = [int(v) for v in dims]
@@ -209,7 +210,7 @@ def pf_create(dims: Sequence[int], ndim: int, num_nodes: int, parent, child, wei
     sm = pf_smoothness(s_kind, sc.ctypes.data_as(_P(ctypes.c_float)) if sc is not None else None,
                        ctypes.cast(fp, _P(ctypes.c_void_p)) if fp is not None else None)
     cfg = pf_config(c, tau, cap, shift, check_every, 1 if d_bf16 else 0, 1 if ipc else 0, int(method),
-                    1 if u_half else 0)
+                    1 if u_half else 0, int(tblock))
     sl = pf_slab(int(slab[0]), int(slab[1])) if slab is not None else None
     out = ctypes.c_void_p()
     _check(_lib.pf_create(ctypes.byref(d), ctypes.byref(g), ctypes.cast(Dp, _P(ctypes.c_void_p)), ctypes.byref(sm),

@@ -589,6 +589,44 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
                                  (s->D16 ? 2 * 40 : 4 * 36) * (ty + 1) * cl);
     }
     choose_chunking(s);
+    if (cfg->tblock == 2) {   // two iterations per HBM pass (pf_tb2.cuh)
+        const bool whole = z0 == 0 && z1 == dims->nz;
+        const bool ok_graph = gc.model == 0 && gc.NI == 0 && gc.NL >= 2 && gc.NL <= 4;
+        const bool ok_s = S->kind == PF_S_SCALAR_PER_NODE || S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD;
+        if (alm || !s->staged || !whole || !ok_graph || !ok_s || cfg->d_bf16 || cfg->u_half || cfg->ipc ||
+            !tb2_kernel_lookup(gc.NL, cfg->cap, &s->tinfo))
+            return bail(fail(PF_ERR_UNSUPPORTED, "config: tblock = 2 needs a Potts model with 2..4 labels on a whole "
+                                                 "volume, scalar or shared capacities, fp32 storage"));
+        const int ty = s->tinfo.tile_y, K = gc.NL;
+        s->tb_smem = s->tinfo.smem_bytes;
+        e = cudaFuncSetAttribute(s->tinfo.func, cudaFuncAttributeMaxDynamicSharedMemorySize, s->tb_smem);
+        if (e != cudaSuccess) { cuda_fail(s, e, "cudaFuncSetAttribute (tb2)"); return bail(PF_ERR_CUDA); }
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, s->tinfo.func, s->tinfo.threads, s->tb_smem);
+        bool ok = occ > 0;
+        for (int i = 0; i < 2; ++i) {
+            ok = ok && encode4d(&s->tb_q[i], s->q_alloc[i], s->nx, s->ny, s->pitch, 3 * K, nzl + 2, 36, ty + 4, 3 * K);
+            ok = ok && encode4d(&s->tb_u[i], s->u_alloc[i], s->nx, s->ny, s->pitch, K, nzl + 2, 36, ty + 3, K);
+            ok = ok && encode4d(&s->tb_uo[i], s->u_alloc[i], s->nx, s->ny, s->pitch, K, nzl + 2, 28, ty, K);
+            ok = ok && encode4d(&s->tb_qo[i], s->q_alloc[i], s->nx, s->ny, s->pitch, 3 * K, nzl + 2, 28, ty, 3 * K);
+        }
+        ok = ok && encode4d(&s->tb_D, s->D_alloc, s->nx, s->ny, s->pitch, K, nzl + 1, 36, ty + 3, K);
+        if (s->s_ch) ok = ok && encode4d(&s->tb_S, s->S_alloc, s->nx, s->ny, s->pitch, 1, nzl, 36, ty + 2, 1);
+        else memset(&s->tb_S, 0, sizeof(s->tb_S));
+        if (!ok) return bail(fail(PF_ERR_CUDA, "tblock: cuTensorMapEncodeTiled failed"));
+        s->tb_tx = (unsigned)(4 * 36 * (3 * K * (ty + 4) + 2 * K * (ty + 3) + s->s_ch * (ty + 2)));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+        s->tb_tiles_x = (int)((s->nx + 27) / 28);
+        s->tb_tiles = s->tb_tiles_x * (int)((s->ny + ty - 1) / ty);
+        const int nch = best_chunks(s->tb_tiles, (int)nzl, (int64_t)sms * occ);
+        s->tb_zchunk = (int)((nzl + nch - 1) / nch);
+        s->tb_items = s->tb_tiles * (int)((nzl + s->tb_zchunk - 1) / s->tb_zchunk);
+        s->tb_grid = (int)std::min<int64_t>((int64_t)sms * occ, s->tb_items);
+        s->tb2 = true;
+    } else if (cfg->tblock != 0) {
+        return bail(fail(PF_ERR_INVALID, "config: tblock must be 0 or 2"));
+    }
     e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) { cuda_fail(s, e, "create"); return bail(PF_ERR_CUDA); }
     *out = s;
@@ -802,6 +840,47 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check, int reserve_sms)
     return PF_OK;
 }
 
+pf_status launch_tb2(pf_solver *s, int check) {
+    StagedArgs sa;
+    memset(&sa, 0, sizeof(sa));
+    sa.tm_q = s->tb_q[s->cur];
+    sa.tm_u = s->tb_u[s->cur];
+    sa.tm_D = s->tb_D;
+    sa.tm_S = s->tb_S;
+    sa.tm_uo = s->tb_uo[1 - s->cur];
+    sa.tm_qo = s->tb_qo[1 - s->cur];
+    sa.q_in = s->q[s->cur];
+    sa.nx = (int)s->nx;
+    sa.ny = (int)s->ny;
+    sa.pitch = (int)s->pitch;
+    sa.nzl = (int)s->nzl;
+    sa.zg0 = 0;
+    sa.nzg = (int)s->nz;
+    sa.zchunk = s->tb_zchunk;
+    sa.tiles_x = s->tb_tiles_x;
+    sa.tiles = s->tb_tiles;
+    sa.item_begin = 0;
+    sa.items = s->tb_items;
+    sa.s_ch = s->s_ch;
+    sa.cap = s->cfg.cap;
+    sa.shift = s->cfg.shift;
+    sa.check = check;
+    sa.tx_bytes = s->tb_tx;
+    sa.inv_c = 1.0f / s->cfg.c;
+    sa.ctau = s->cfg.c * s->cfg.tau;
+    sa.resid_bits = s->d_resid;
+    sa.err_voxel = s->d_err;
+    sa.g = s->gc.g;
+    sa.ticket = s->d_err + 1 + s->launch_parity;
+    sa.ticket_next = s->d_err + 2 - s->launch_parity;
+    void *args[] = {(void *)&sa};
+    CK(cudaLaunchKernel(s->tinfo.func, dim3(s->tb_grid), dim3(s->tinfo.threads), args, s->tb_smem, s->stream),
+       "launch pf_iter_tb2");
+    s->launch_parity ^= 1;
+    s->launches++;
+    return PF_OK;
+}
+
 int check_this_iteration(pf_solver *s) {
     const int64_t it = s->iters + 1;
     return (s->cfg.check_every > 0 && it % s->cfg.check_every == 0) ? 1 : 0;
@@ -829,6 +908,21 @@ pf_status read_residual(pf_solver *s, bool any_check, float *residual) {
 pf_status launch_iterations(pf_solver *s, int32_t n, bool *any_check) {
     pf_status st;
     for (int t = 0; t < n; ++t) {
+        if (s->tb2 && n - t >= 2) {   // two iterations in one pass; the residual of the pair's last check iteration
+            const int c1 = check_this_iteration(s);
+            s->iters += 1;
+            const int c2 = check_this_iteration(s);
+            s->iters -= 1;
+            if (c1 || c2) {
+                CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
+                *any_check = true;
+            }
+            if ((st = launch_tb2(s, c2 ? 2 : (c1 ? 1 : 0))) != PF_OK) return st;
+            s->cur = 1 - s->cur;
+            s->iters += 2;
+            ++t;
+            continue;
+        }
         const int check = check_this_iteration(s);
         if (check) {
             CK(cudaMemsetAsync(s->d_resid, 0, sizeof(unsigned int), s->stream), "reset residual");
@@ -846,12 +940,16 @@ pf_status launch_iterations(pf_solver *s, int32_t n, bool *any_check) {
     return PF_OK;
 }
 
-// Iterations per graph: even (ping-pong buffer and counter parity return to their start) and a multiple
-// of check_every (the residual resets / checks sit at the same positions in every replay).
+// Iterations per graph: a multiple of check_every (the residual resets / checks sit at the same positions in
+// every replay) whose launches return the ping-pong buffer and the ticket-counter parity to their start: an even
+// number of launches -- 2 iterations, or 4 with two iterations per launch (tblock).
 int graph_period(const pf_solver *s) {
     const int k = s->cfg.check_every;
+    const int m = s->tb2 ? 4 : 2;
     if (k <= 0) return 16;
-    return (k % 2) ? 2 * k : k;
+    int P = k;
+    while (P % m) P += k;
+    return P;
 }
 
 bool graph_aligned(const pf_solver *s) {
@@ -1166,6 +1264,7 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
                  (int64_t)s->gc.NL * (s->D16 ? 2 : 4) + 12);
     if (s->s_kind == PF_S_SHARED_FIELD || s->s_kind == PF_S_SCALED_FIELD) b += 4 * V;
     if (s->s_kind == PF_S_FIELD_PER_NODE) b += 4 * V * s->gc.NF;
+    if (s->tb2) b /= 2;   // one pass moves the state once for two iterations
     info->algorithmic_bytes_per_iteration = b;
     info->device_bytes = s->device_bytes;
     info->kernel_launches = s->launches;
@@ -1173,6 +1272,7 @@ pf_status pf_get_kernel_info(const pf_solver *s, pf_kernel_info *info) {
     info->flow_nodes = s->gc.NF;
     info->cluster = s->cluster ? 1 : 0;
     info->phase1_ctas = phase1_grid(s);
+    info->tblock = s->tb2 ? 2 : 1;
     return PF_OK;
 }
 

@@ -20,6 +20,7 @@
 #include "pf_cluster.cuh"
 #include "pf_kernels.cuh"
 #include "pf_staged.cuh"
+#include "pf_tb2.cuh"
 
 namespace pfi {
 
@@ -142,6 +143,12 @@ struct pf_solver {
     int reserved_sms = 0;   // SMs a phase-1 launch leaves free (pf_set_reserved_sms)
     int sms = 148;
     unsigned int tx_bytes = 0;
+    // two iterations per HBM pass (pf_config.tblock = 2, pf_tb2.cuh): its own tiles (28 wide), maps, chunking
+    bool tb2 = false;
+    StagedKernelInfo tinfo{};
+    CUtensorMap tb_q[2], tb_u[2], tb_D, tb_S, tb_uo[2], tb_qo[2];
+    int tb_smem = 0, tb_tiles_x = 0, tb_tiles = 0, tb_items = 0, tb_zchunk = 0, tb_grid = 0;
+    unsigned int tb_tx = 0;
 };
 
 namespace pfi {
@@ -166,6 +173,7 @@ pf_status check_numeric(pf_solver *s);
 int check_this_iteration(pf_solver *s);
 pf_status read_residual(pf_solver *s, bool any_check, float *residual);
 pf_status launch_items(pf_solver *s, int ib, int ie, int check, int reserve_sms = 0);
+pf_status launch_tb2(pf_solver *s, int check);   // iterations iters+1, iters+2 in one pass; check: 0, 1 or 2
 int phase1_grid(const pf_solver *s);
 // device-side ordering of IPC-linked slabs (pf_ipc_step, pf_reset): wait until both neighbours announced
 // step `seq` in this slab's inbox / announce `seq` into theirs

@@ -26,7 +26,8 @@ class Solver:
     def __init__(self, dims: Sequence[int], ndim: int, graph, D: Sequence, *, s_scalars=None, s_shared=None,
                  s_fields=None, s_scaled=None, c: float = 0.25, tau: float = 0.1, cap: int = PF_CAP_L2,
                  shift: int = PF_SHIFT_MIN, check_every: int = 10, slab: Optional[Sequence[int]] = None,
-                 d_bf16: bool = False, method: int = 0, ipc: bool = False, u_half: bool = False):
+                 d_bf16: bool = False, method: int = 0, ipc: bool = False, u_half: bool = False,
+                 tblock: int = 0):
         num_nodes, parent, child, weight = graph
         self.dims = tuple(int(v) for v in dims)
         self.ndim = ndim
@@ -43,7 +44,7 @@ class Solver:
         else:
             kind, fields = PF_S_FIELD_PER_NODE, list(s_fields)
         self.h = pf_create(self.dims, ndim, num_nodes, parent, child, weight, list(D), kind, s_scalars, fields, c, tau, cap,
-                           shift, check_every, slab, d_bf16, method, ipc, u_half)
+                           shift, check_every, slab, d_bf16, method, ipc, u_half, tblock)
 
     # ---------------------------------------------------------------- C-ABI calls
     @property

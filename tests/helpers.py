@@ -7,7 +7,7 @@ CAP = {"l2": 0, "linf": 1}
 
 
 def solver_from_inputs(inp, shift=0, cap=None, check_every=10, slab=None, c=None, tau=None, device_inputs=False,
-                       d_bf16=False, method=0, u_half=False):
+                       d_bf16=False, method=0, u_half=False, tblock=0):
     import paper_1501_07844_b200 as pf
 
     cfg, g = inp.cfg, inp.graph
@@ -38,7 +38,7 @@ def solver_from_inputs(inp, shift=0, cap=None, check_every=10, slab=None, c=None
     cap = CAP[cfg.cap] if cap is None else cap
     return pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.child, g.weight), D,
                      c=cfg.c if c is None else c, tau=cfg.tau if tau is None else tau, cap=cap, shift=shift,
-                     check_every=check_every, slab=None if slab is None else (z0, z1), d_bf16=d_bf16, u_half=u_half,
+                     check_every=check_every, slab=None if slab is None else (z0, z1), d_bf16=d_bf16, u_half=u_half, tblock=tblock,
                      method=method, **kw)
 
 

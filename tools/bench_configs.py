@@ -23,6 +23,9 @@ import phantoms as P  # noqa: E402
 def cfg_of(name):
     if name == "C5slab":
         return P.config("C5").resized(768, 768, 96, name="C5slab")
+    if name in ("T2", "T3", "T4"):   # f3 demonstration volumes: C2's recipe (256^3, edge S) with K = 2..4 labels
+        K = int(name[1])
+        return P.Config(name, 3, 256, 256, 256, "potts", K, 4 * K, 0.15, "sq", "edge", 0.05, 300, seed=2020)
     return P.config(name)
 
 
@@ -35,6 +38,7 @@ def main():
     ap.add_argument("--alm", action="store_true", help="explicit-flow ALM comparison arm (Potts configs)")
     ap.add_argument("--u-half", action="store_true", help="lambda = log2 u stored as binary16 (pf_config.u_half)")
     ap.add_argument("--linf", action="store_true", help="anisotropic capacities: the l-inf box (dual of l1-TV)")
+    ap.add_argument("--tblock", type=int, default=0, help="2: two iterations per HBM pass (pf_config.tblock)")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -52,7 +56,8 @@ def main():
             kw = {"s_shared": torch.from_numpy(inp.s_field).to(dev)}
         else:
             kw = {"s_scalars": inp.s_scalars}
-        extra = {"d_bf16": args.d_bf16, "u_half": args.u_half, "cap": pf.PF_CAP_LINF if args.linf else pf.PF_CAP_L2}
+        extra = {"d_bf16": args.d_bf16, "u_half": args.u_half, "cap": pf.PF_CAP_LINF if args.linf else pf.PF_CAP_L2,
+                 "tblock": args.tblock}
         c, tau = cfg.c, cfg.tau
         if args.alm:
             extra["method"] = pf.PF_METHOD_EXPLICIT_ALM
@@ -92,7 +97,7 @@ def main():
         s.close()
         line = {"config": name, "method": "explicit-flow ALM" if args.alm else "pseudo-flow",
                 "d_dtype": "bf16" if args.d_bf16 else "f32", "u_storage": "binary16 lambda" if args.u_half else "f32 lambda",
-                "capacity": "linf" if args.linf else "l2",
+                "capacity": "linf" if args.linf else "l2", "tblock": info["tblock"],
                 "dims": [cfg.nx, cfg.ny, cfg.nz], "end_labels": NL, "nodes": g.num_nodes - 1,
                 "iterations": n, "ms_per_solve": ms, "ms_per_iteration": it_ms,
                 "gvl_it_per_s": V * NL * n / (ms / 1e3) / 1e9,
