@@ -69,8 +69,9 @@ __device__ __forceinline__ void tb_flow(float cx, float cy, float cz, const floa
     }
 }
 
+// two CTAs per SM for K = 2 (~80 KB of shared memory, <= 93 registers)
 template <int K, int TY, int CAP>
-__global__ void __launch_bounds__(32 * (TY + 3), 1) pf_iter_tb2(const __grid_constant__ StagedArgs a) {
+__global__ void __launch_bounds__(32 * (TY + 3), K == 2 ? 2 : 1) pf_iter_tb2(const __grid_constant__ StagedArgs a) {
     using L = TB2Layout<K, TY>;
     constexpr int W = L::W, BW = L::BW, MS = L::MS;
     constexpr int QCS = L::QR * BW, UCS = L::UR * BW;
@@ -270,7 +271,9 @@ __global__ void __launch_bounds__(32 * (TY + 3), 1) pf_iter_tb2(const __grid_con
                     }
                 }
             }
-            __syncthreads();   // M^{t+1}(p-1) complete
+            // (no barrier: B_{t+1}(p-2) reads the M^{t+1} ring slot of plane p-2, complete since the previous step,
+            // and the point's own M^{t+1}(p-1); the exchange buffer is rewritten only after the next step's first
+            // barrier)
             // ---------------- B_{t+1}(p-2) on R_B1: q^{t+2}(p-2)
             if (doB1 && inB1) {
                 float qo3[3][K];

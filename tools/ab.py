@@ -16,6 +16,7 @@ ap.add_argument("--configs", nargs="+", default=["C2", "C5slab"])
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--alm", action="store_true", help="time the explicit-flow ALM arm (bench_configs.py --alm)")
+ap.add_argument("--extra", default="", help="extra bench_configs.py arguments, e.g. '--tblock 2'")
 args = ap.parse_args()
 res = {}
 for r in range(args.rounds):
@@ -28,7 +29,8 @@ for r in range(args.rounds):
                 k, _, v = kv.partition("=")
                 env[k] = v
             pr = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_configs.py"), c, "--steps",
-                                 str(args.steps)] + (["--alm"] if args.alm else []), env=env, capture_output=True, text=True)
+                                 str(args.steps)] + (["--alm"] if args.alm else []) + args.extra.split(), env=env, capture_output=True,
+                                text=True)
             out = pr.stdout
             if pr.returncode != 0:
                 print(json.dumps({"round": r, "config": c, "lib": lib, "failed": pr.returncode,
