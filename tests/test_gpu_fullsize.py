@@ -34,7 +34,7 @@ def test_fullsize_sampled_parity(name):
     cfg = _cfg(name)
     inp = P.generate(cfg)
     s = solver_from_inputs(inp)
-    n = 6
+    n = 10   # SURVEY 8.4.5 fallback set: full size at N = 10 (C5 as its per-GPU slab C5slab)
     s.iterate(n)
     u, _ = s.labeling()
     q = s.flows()
