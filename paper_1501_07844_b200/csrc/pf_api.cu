@@ -409,8 +409,16 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     {
         const char *env = getenv("PF_ITER_KERNEL");
         const bool want_global = env && strcmp(env, "global") == 0;
+        // the graph's edge mask: a kernel specialised for exactly these edges is used when one is compiled in
+        // (PF_DENSE_GRAPH=1, experiments: always the dense weight rows)
+        uint64_t mask = 0;
+        for (int i = 0; i < gc.NI && i < kMaxInternal; ++i)
+            for (int j = 0; j < gc.NV && j < kMaxNodes; ++j)
+                if (gc.g.w[i][j] != 0.f) mask |= 1ull << (i * 16 + j);
+        if (gc.model != 0 || (getenv("PF_DENSE_GRAPH") && strcmp(getenv("PF_DENSE_GRAPH"), "1") == 0)) mask = kDenseMask;
         s->staged = !alm && !want_global &&
-                    staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, cfg->u_half ? 1 : 0, &s->sinfo) &&
+                    staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, cfg->u_half ? 1 : 0, mask,
+                                         &s->sinfo) &&
                     encode_fn() != nullptr;
         // Potts with many labels: the 2-CTA cluster split (scalar / shared capacities; PF_CLUSTER=0 disables)
         const char *cenv = getenv("PF_CLUSTER");

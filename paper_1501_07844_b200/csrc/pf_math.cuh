@@ -198,23 +198,31 @@ __device__ __forceinline__ float resid_log2(const float *lnew, const float *lold
 // infinite or NaN -- e.g. every label of the voxel at lambda = -inf, or a non-finite excess
 __device__ __forceinline__ bool label_sum_bad(float s) { return !(s > 0.f) || !(s <= FLT_MAX); }
 
+// Edge mask of a compiled graph (pf_graph.cu): bit i * kMaxNodes + j set iff w[i][j] != 0 (internal position i ->
+// position j).  Kernels specialised for a mask emit only the graph's edges (the flat per-level schedule of row
+// a10); ~0 = dense rows, any graph.  Skipped terms are fmaf(0, x, y) = y up to the sign of a zero.
+constexpr uint64_t kDenseMask = ~0ull;
+__host__ __device__ constexpr bool edge_on(uint64_t mask, int i, int j) { return (mask >> (i * 16 + j)) & 1ull; }
+
 // Top-down excess pushes along O \ {S}: d_j += w_ij d_i for internal i (positions < NI).
-template <int NI, int NV>
+template <int NI, int NV, uint64_t MASK = kDenseMask>
 __device__ __forceinline__ void push_down(float (&d)[NV], const float (&w)[kMaxInternal][kMaxNodes]) {
 #pragma unroll
     for (int i = 0; i < NI; ++i)
 #pragma unroll
-        for (int j = i + 1; j < NV; ++j) d[j] = fmaf(w[i][j], d[i], d[j]);
+        for (int j = i + 1; j < NV; ++j)
+            if (MASK == kDenseMask || edge_on(MASK, i, j)) d[j] = fmaf(w[i][j], d[i], d[j]);
 }
 
 // Bottom-up masses along O^-1 \ {S}: M_i = sum_j w_ij M_j for internal i.
-template <int NI, int NV>
+template <int NI, int NV, uint64_t MASK = kDenseMask>
 __device__ __forceinline__ void push_up(float (&M)[NV], const float (&w)[kMaxInternal][kMaxNodes]) {
 #pragma unroll
     for (int i = NI - 1; i >= 0; --i) {
         float acc = 0.f;
 #pragma unroll
-        for (int j = i + 1; j < NV; ++j) acc = fmaf(w[i][j], M[j], acc);
+        for (int j = i + 1; j < NV; ++j)
+            if (MASK == kDenseMask || edge_on(MASK, i, j)) acc = fmaf(w[i][j], M[j], acc);
         M[i] = acc;
     }
 }
@@ -231,7 +239,7 @@ struct Model {
 // End-label excesses from the flow divergences dq and data terms Dv into dlab[NI + l].
 //   MODEL 0: d_v = div q_v; d_L += D_L; top-down pushes
 //   MODEL 1: d_0 = D_0; d_i = (d_{i-1} + div q_i) + D_i (prefix)
-template <int MODEL, int NI, int NL>
+template <int MODEL, int NI, int NL, uint64_t MASK = kDenseMask>
 __device__ __forceinline__ void label_excess(const float (&dq)[Model<MODEL, NI, NL>::NF], const float (&Dv)[NL],
                                              float (&dlab)[NI + NL], const float (&w)[kMaxInternal][kMaxNodes]) {
     if constexpr (MODEL == 0) {
@@ -239,7 +247,7 @@ __device__ __forceinline__ void label_excess(const float (&dq)[Model<MODEL, NI, 
         for (int v = 0; v < NI + NL; ++v) dlab[v] = dq[v];
 #pragma unroll
         for (int l = 0; l < NL; ++l) dlab[NI + l] = Dv[l] + dlab[NI + l];
-        push_down<NI, NI + NL>(dlab, w);
+        push_down<NI, NI + NL, MASK>(dlab, w);
     } else {
         float run = 0.f;
         dlab[NI] = Dv[0];
@@ -254,13 +262,13 @@ __device__ __forceinline__ void label_excess(const float (&dq)[Model<MODEL, NI, 
 // Unnormalised masses M of the flow-carrying nodes from the end-label masses ut.
 //   MODEL 0: M_L = u~_L; bottom-up pushes
 //   MODEL 1: M_N = u~_N; M_i = u~_i + M_{i+1} (suffix)
-template <int MODEL, int NI, int NL>
+template <int MODEL, int NI, int NL, uint64_t MASK = kDenseMask>
 __device__ __forceinline__ void node_masses(const float (&ut)[NL], float (&M)[Model<MODEL, NI, NL>::NF],
                                             const float (&w)[kMaxInternal][kMaxNodes]) {
     if constexpr (MODEL == 0) {
 #pragma unroll
         for (int l = 0; l < NL; ++l) M[NI + l] = ut[l];
-        push_up<NI, NI + NL>(M, w);
+        push_up<NI, NI + NL, MASK>(M, w);
     } else {
         M[NI - 1] = ut[NL - 1];
 #pragma unroll

@@ -179,7 +179,7 @@ __device__ __forceinline__ void stage_row_acquire(int lane, int since) {
 // DBF: D stored as bf16 (pf_config.d_bf16; the D stage then holds rows of 40 bf16).
 // UH: lambda = log2 u stored as binary16 (pf_config.u_half; the u stage then holds rows of 40 halves, the u
 // staging tile halves [l][row][32]).
-template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF, int UH>
+template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF, int UH, uint64_t MASK>
 __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
     using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
     constexpr int NF = L::NF;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
             float sum = 1.f;
             if constexpr (G == 1) {
                 if (lx >= 0) {
-                    label_excess<MODEL, NI, NL>(dq, Dv, dlab, a.g.w);
+                    label_excess<MODEL, NI, NL, MASK>(dq, Dv, dlab, a.g.w);
                     sum = label_update<NI, NL>(dlab, uold, ut, un, a.shift, k2);
                 }
             } else {
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
                     if (a.check) resid = resid_log2<NLG>(un, uold, resid);
                 }
                 if constexpr (G == 1) {
-                    node_masses<MODEL, NI, NL>(ut, Mv, a.g.w);
+                    node_masses<MODEL, NI, NL, MASK>(ut, Mv, a.g.w);
                 } else {
 #pragma unroll
                     for (int l = 0; l < NLG; ++l) Mv[l] = ut[l];
@@ -534,6 +534,7 @@ struct StagedKernelInfo {
     int groups;      // label groups per row (G)
 };
 
-bool staged_kernel_lookup(int NI, int NL, int MODEL, int DBF, int UH, StagedKernelInfo *info);
+// mask: the graph's edge mask (edge_on); a kernel specialised for exactly that mask is preferred, else dense rows
+bool staged_kernel_lookup(int NI, int NL, int MODEL, int DBF, int UH, uint64_t mask, StagedKernelInfo *info);
 
 }  // namespace pf
