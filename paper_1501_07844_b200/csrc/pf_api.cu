@@ -596,6 +596,12 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
                                  (cfg->u_half ? 2 * 40 : 4 * 36) * (ty + 1) * cl +
                                  (s->D16 ? 2 * 40 : 4 * 36) * (ty + 1) * cl);
     }
+    {   // plain projection where no square can under- or overflow (pf_math.cuh flow_step3; PF_SCALED_PROJ=1 off)
+        bool fast = s->s_ch == 0 && cfg->shift == PF_SHIFT_MIN && cfg->cap == PF_CAP_L2 && gc.NF > 0;
+        for (int p = 0; p < gc.NF && fast; ++p) fast = s->gc.g.s[p] >= 0x1p-60f && std::isfinite(s->gc.g.s[p]);
+        if (getenv("PF_SCALED_PROJ") && strcmp(getenv("PF_SCALED_PROJ"), "1") == 0) fast = false;
+        s->fastproj = fast ? 1 : 0;
+    }
     choose_chunking(s);
     if (cfg->tblock == 2) {   // two iterations per HBM pass (pf_tb2.cuh)
         const bool whole = z0 == 0 && z1 == dims->nz;
@@ -779,6 +785,7 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check, int reserve_sms)
         sa.s_ch = s->s_ch;
         sa.cap = s->cfg.cap;
         sa.shift = s->cfg.shift;
+        sa.fastproj = s->fastproj;
         sa.tx_bytes = s->tx_bytes;
         sa.inv_c = 1.0f / s->cfg.c;
         sa.ctau = s->cfg.c * s->cfg.tau;

@@ -141,6 +141,7 @@ struct pf_solver {
     int nb = 0, bplane[2] = {0, 0}, zlo = 0, zhi = 0, items_b = 0;
     int phase_pending = 0;  // 1 after pf_iterate_phase(0) until its phase 1
     int reserved_sms = 0;   // SMs a phase-1 launch leaves free (pf_set_reserved_sms)
+    int fastproj = 0;       // plain projection is exact for this solver (flow_step3 SCALED = false)
     int sms = 148;
     unsigned int tx_bytes = 0;
     // two iterations per HBM pass (pf_config.tblock = 2, pf_tb2.cuh): its own tiles (28 wide), maps, chunking

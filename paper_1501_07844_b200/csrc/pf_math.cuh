@@ -280,13 +280,21 @@ __device__ __forceinline__ void node_masses(const float (&ut)[NL], float (&M)[Mo
 //   q^ = q - c tau nabla M;  q' = q^ if |q^| <= S else q^ S/|q^|  (CAP 0, l2)  |  clamp(q^, -S, S) (CAP 1).
 // cx, cy, cz: c tau per axis, 0 where nabla_k M is 0 (last index along k) -- the staged kernel folds the
 // boundary into the coefficient (q - 0 * g == q for the finite g it passes there).
-template <int CAP>
+// SCALED = false (StagedArgs.fastproj): the plain formula, for launches where no square can under- or overflow --
+// SHIFT_MIN (masses u~ <= 1, so |q^| stays near S) with scalar capacities all >= 2^-60; there every decision and,
+// since the rescale is by an exact power of two (and MUFU.RSQ of a 4^k-scaled argument is the 2^-k-scaled
+// result), every value equals the scaled form's.
+template <int CAP, bool SCALED = true>
 __device__ __forceinline__ void flow_step3(float cx, float cy, float cz, float gx, float gy, float gz, float sv,
                                            float &hx, float &hy, float &hz) {
     hx = fmaf(-cx, gx, hx);
     hy = fmaf(-cy, gy, hy);
     hz = fmaf(-cz, gz, hz);
-    if (CAP == 0) {
+    if (CAP == 0 && !SCALED) {
+        const float n2 = fmaf(hx, hx, fmaf(hy, hy, hz * hz));
+        const float f = n2 > sv * sv ? sv * rsqrt_approx(n2) : 1.f;
+        hx *= f; hy *= f; hz *= f;
+    } else if (CAP == 0) {
         // Norm on a power-of-two rescaled copy (exact scaling), so tiny flows next to tiny capacities
         // (S(x) down to 1e-38 in the configs' edge-weighted S) neither under-flow their squares nor
         // need a slow path; for normal ranges the result is bitwise that of the unscaled formula.

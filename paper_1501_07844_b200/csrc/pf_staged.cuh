@@ -64,6 +64,7 @@ struct StagedArgs {
     int nb, bplane0, bplane1, zlo, zhi;
     int s_ch;     // 0: scalar capacities, 1: shared field (x g.s[f]), NF: field per flow node
     int cap, shift, check;
+    int fastproj;       // 1: flow_step3's plain projection is exact for this launch (see pf_math.cuh)
     unsigned int tx_bytes;
     float inv_c, ctau;
     unsigned int *resid_bits;
@@ -143,7 +144,8 @@ __device__ __forceinline__ void flow_out_staged(const StagedArgs &a, const float
         const float gy = Rz[f * rps + roff + rs] - mc;
         const float gz = Mn[v] - mc;
         float hx = qc[0][v], hy = qc[1][v], hz = qc[2][v];
-        flow_step3<CAP>(cx, cy, cz, gx, gy, gz, sv, hx, hy, hz);
+        if (a.fastproj) flow_step3<CAP, false>(cx, cy, cz, gx, gy, gz, sv, hx, hy, hz);
+        else flow_step3<CAP, true>(cx, cy, cz, gx, gy, gz, sv, hx, hy, hz);
         if (OSTAGE) {
             qo[v * Pf] = hx;
             qo[v * Pf + Pk] = hy;

@@ -407,3 +407,23 @@ def test_ishikawa_chain_with_flowing_labels_uses_dag_kernel():
                   s_scalars=np.full(g.num_nodes, 0.05, np.float32))
     assert s.kernel_info()["model"] == 0
     s.close()
+
+
+def test_plain_projection_and_edge_mask_bitwise(monkeypatch, kernel_variant):
+    """The per-launch specialisations of the scalar-capacity SHIFT_MIN configs -- the plain projection
+    (StagedArgs.fastproj) and the edge-mask kernels of C3 / C4 -- give the general code's bits."""
+    if kernel_variant != "staged":
+        pytest.skip("specialisations of the TMA-staged kernel")
+    for name, dims in (("C3", (45, 38, 31)), ("C4", (41, 38, 29)), ("C1", (64, 64, 1))):
+        inp = P.generate(P.config(name).resized(*dims))
+        out = []
+        for env in ({}, {"PF_SCALED_PROJ": "1", "PF_DENSE_GRAPH": "1"}):
+            for k in ("PF_SCALED_PROJ", "PF_DENSE_GRAPH"):
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            s = solver_from_inputs(inp)
+            s.iterate(120)
+            out.append((s.labeling()[0], s.flows()))
+            s.close()
+        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1]), name
