@@ -433,7 +433,8 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         if (s->staged) {
             const int s_ch = (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD)
                                  ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? gc.NF : 0);
-            s->staged_smem = s->sinfo.smem_bytes + 16 * ((s_ch * s->sinfo.tile_y * 32 + 31) / 32 * 32);  // 4 S slots
+            s->staged_smem = s->sinfo.smem_bytes +
+                             4 * s->sinfo.s_slots * ((s_ch * s->sinfo.tile_y * 32 + 31) / 32 * 32);   // S ring slots
             int maxsm = 0;
             cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->device);
             cudaFuncAttributes fa{};

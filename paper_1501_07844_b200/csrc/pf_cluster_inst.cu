@@ -22,6 +22,7 @@ bool cluster_kernel_lookup(int NL, int DBF, int UH, StagedKernelInfo *info) {
         info->tile_y = 8;                                                                               \
         info->ostage = 1;                                                                               \
         info->groups = 1;                                                                               \
+        info->s_slots = 4;                                                                              \
         return true;                                                                                    \
     }
 #define PF_CLUSTER_CASE3(NLV) PF_CLUSTER_CASE(NLV, 0, 0) PF_CLUSTER_CASE(NLV, 1, 0) PF_CLUSTER_CASE(NLV, 0, 1)

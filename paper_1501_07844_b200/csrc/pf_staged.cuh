@@ -90,9 +90,12 @@ __device__ __forceinline__ void tile_origin(const StagedArgs &a, int t, int ty_r
     y0 = ty * ty_rows;
 }
 
-template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G>
+// NSTG: input stages in flight (2: one plane of look-ahead; 3: two, where shared memory allows -- short tiles).
+// SR: S ring slots covering the planes p - 1 .. p + NSTG.
+template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int NSTG_ = 2>
 struct StagedLayout {
     static_assert(OSTAGE >= 0 && OSTAGE <= 2, "OSTAGE: 0 direct, 1 tile stores, 2 tile u + per-warp q rows");
+    static constexpr int NSTG = NSTG_, SR = NSTG_ == 2 ? 4 : 8;
     static constexpr int NV = NI + NL;
     static constexpr int NF = Model<MODEL, NI, NL>::NF;   // flow-carrying nodes
     static constexpr int QW = 40, UW = 36, SW = 32;
@@ -107,10 +110,10 @@ struct StagedLayout {
     static constexpr int kThreads = 32 * G * (TY + 2);
     // runtime part: the S staging ring holds s_ch channels (0, 1 or NF)
     __host__ __device__ static constexpr int ssz(int s_ch) { return round32(s_ch * TY * SW); }
-    __host__ __device__ static constexpr int off_U() { return 2 * QSZ; }
-    __host__ __device__ static constexpr int off_D() { return 2 * QSZ + 2 * USZ; }
-    __host__ __device__ static constexpr int off_S() { return 2 * QSZ + 4 * USZ; }
-    __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + 4 * ssz(s_ch); }
+    __host__ __device__ static constexpr int off_U() { return NSTG * QSZ; }
+    __host__ __device__ static constexpr int off_D() { return NSTG * (QSZ + USZ); }
+    __host__ __device__ static constexpr int off_S() { return NSTG * (QSZ + 2 * USZ); }
+    __host__ __device__ static constexpr int off_R(int s_ch) { return off_S() + SR * ssz(s_ch); }
     __host__ __device__ static constexpr int off_Uo(int s_ch) { return off_R(s_ch) + round32(3 * RING); }
     __host__ __device__ static constexpr int off_Qo(int s_ch) { return off_Uo(s_ch) + 2 * UOSZ; }
     __host__ __device__ static constexpr int off_X(int s_ch) { return off_Qo(s_ch) + QOB * QOSZ; }
@@ -181,9 +184,10 @@ __device__ __forceinline__ void stage_row_acquire(int lane, int since) {
 // DBF: D stored as bf16 (pf_config.d_bf16; the D stage then holds rows of 40 bf16).
 // UH: lambda = log2 u stored as binary16 (pf_config.u_half; the u stage then holds rows of 40 halves, the u
 // staging tile halves [l][row][32]).
-template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF, int UH, uint64_t MASK>
+template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int DBF, int UH, uint64_t MASK, int NSTG_ = 2>
 __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __grid_constant__ StagedArgs a) {
-    using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G>;
+    using L = StagedLayout<NI, NL, TY, OSTAGE, MODEL, G, NSTG_>;
+    constexpr int NSTG = L::NSTG, SR = L::SR;
     constexpr int NF = L::NF;
     static_assert(G == 1 || (G == 2 && MODEL == 0 && NI == 0 && NL % 2 == 0), "label split: Potts, two halves");
     constexpr int NLG = NL / G;   // end labels of this thread's group
@@ -224,8 +228,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
     float *qo_row = Qo + (ly * G + grp) * 3 * NFG * 32;
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int i = 0; i < NSTG; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
         prefetch_tmap(&a.tm_q);
         prefetch_tmap(&a.tm_u);
@@ -243,7 +246,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
         tma_load_4d(Qs + stage * L::QSZ, &a.tm_q, &bars[stage], x0 - 4, y0 - 1, 0, plane + 1);
         tma_load_4d(Us + stage * L::USZ, &a.tm_u, &bars[stage], x0, y0, 0, plane + 1);
         tma_load_4d(Ds + stage * L::USZ, &a.tm_D, &bars[stage], x0, y0, 0, plane);
-        if (a.s_ch) tma_load_4d(Ss + (plane & 3) * SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
+        if (a.s_ch) tma_load_4d(Ss + (plane & (SR - 1)) * SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
     };
     const uint64_t pol_out = OSTAGE ? policy_evict_first() : 0;
 
@@ -284,8 +287,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
         if (tid == 0) {
             s_item = grab();  // next item; read by all threads after this item's plane barriers
             fence_proxy_async();
-            issue(zc0, kbase & 1, x0, y0);
-            if (zc0 + 1 <= pend) issue(zc0 + 1, (kbase + 1) & 1, x0, y0);
+            for (int i = 0; i < NSTG && zc0 + i <= pend; ++i) issue(zc0 + i, (kbase + i) % NSTG, x0, y0);
         }
         // q of the plane below the chunk (its z-component enters div of the first plane).  Two register
         // sets alternate between "current plane" and "plane awaiting its flow step" (no copies).
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
         // flow step + projection of plane z (stage B); Mn = M(z+1) at the voxel (unused when !has_z)
         auto stage_b = [&](const int z, const float (&Mn)[NFG], bool has_z, const float (&qc)[3][NFG]) {
             const float *Rz = R + (z % 3) * RING;
-            const float *Sz = Ss + (z & 3) * SSZ + ly * SW + lx;
+            const float *Sz = Ss + (z & (SR - 1)) * SSZ + ly * SW + lx;
             if (OSTAGE == 2) {
                 if (row_out) {
                     stage_row_acquire(lane, since_q);
@@ -348,8 +350,8 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
 
         auto plane_step = [&](const int p, float (&qc)[3][NFG], float (&qn)[3][NFG]) {
             const int k = kbase + (p - zc0);
-            const int st = k & 1;
-            mbar_wait(&bars[st], (k >> 1) & 1);
+            const int st = k % NSTG;
+            mbar_wait(&bars[st], (k / NSTG) & 1);
             const float *Qb = Qs + st * L::QSZ;
             const float *Ub = Us + st * L::USZ;
             const float *Db = Ds + st * L::USZ;
@@ -469,9 +471,9 @@ __global__ void __launch_bounds__(32 * G *(TY + 2), 1) pf_iter_staged(const __gr
             }
             __syncthreads();  // ring slot p complete; stage st fully consumed; staged u complete
             if (tid == 0) {
-                if (p + 2 <= pend) {
+                if (p + NSTG <= pend) {   // the slot plane p released: NSTG - 1 planes of look-ahead
                     fence_proxy_async();
-                    issue(p + 2, st, x0, y0);
+                    issue(p + NSTG, st, x0, y0);
                 }
                 if (OSTAGE) {
                     if (p < zc1) {
@@ -534,6 +536,7 @@ struct StagedKernelInfo {
     int tile_y;
     int ostage;      // 1: outputs staged in smem and written by TMA stores
     int groups;      // label groups per row (G)
+    int s_slots;     // S ring slots (StagedLayout::SR)
 };
 
 // mask: the graph's edge mask (edge_on); a kernel specialised for exactly that mask is preferred, else dense rows

@@ -22,6 +22,7 @@ bool tb2_kernel_lookup(int K, int CAP, StagedKernelInfo *info) {
         info->tile_y = 8;                                                                               \
         info->ostage = 1;                                                                               \
         info->groups = 1;                                                                               \
+        info->s_slots = 0;                                                                              \
         return true;                                                                                    \
     }
     PF_TB2_CASE(2, 0)
