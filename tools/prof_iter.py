@@ -23,4 +23,7 @@ s = pf.Solver((cfg.nx, cfg.ny, cfg.nz), cfg.ndim, (g.num_nodes, g.parent, g.chil
               tau=cfg.tau, check_every=10, **kw)
 s.iterate(n, residual=True)
 print(name, s.kernel_info())
+if len(sys.argv) > 3:   # kernel info as JSON (tools/profile_round.sh: algorithmic bytes for the traffic entry)
+    import json
+    json.dump(s.kernel_info(), open(sys.argv[3], "w"))
 s.close()
