@@ -9,8 +9,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build_obj")
-LIB = os.path.join(HERE, "libpf.so")
+# experiments only (tools/ab.py A/B builds): PF_BUILD_DEFS="-DNAME=VALUE ..." compiles a variant into
+# PF_BUILD_LIB (another in-tree library name, loaded with PF_LIB=<name>) with its own object directory
+DEFS = os.environ.get("PF_BUILD_DEFS", "").split()
+LIB = os.path.join(HERE, os.environ.get("PF_BUILD_LIB", "libpf.so"))
+BUILD = os.path.join(HERE, "build_obj" + ("" if LIB.endswith("/libpf.so") else "_" + os.path.basename(LIB)[:-3]))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -32,7 +35,7 @@ def _compile(src: str) -> str:
         return obj
     log = obj + ".ptxas.txt"
     with open(log, "w") as fh:
-        subprocess.check_call([NVCC] + FLAGS + ["-c", src, "-o", obj], stdout=fh, stderr=subprocess.STDOUT)
+        subprocess.check_call([NVCC] + FLAGS + DEFS + ["-c", src, "-o", obj], stdout=fh, stderr=subprocess.STDOUT)
     return obj
 
 

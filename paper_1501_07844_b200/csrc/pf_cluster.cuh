@@ -16,7 +16,21 @@
 #pragma once
 #include "pf_staged.cuh"
 
+// Early refill of the input stage (experiments): every warp but warp 0 signals "stage read" on named barrier
+// kStageBar right after its shared-memory reads of the plane (bar.arrive, no wait); warp 0 waits for them
+// (bar.sync) -- 1: after its label_half, 2: after the exchange wait -- and thread 0 then issues the loads of plane
+// p + 2 instead of at the plane barrier.
+#ifndef PF_EARLY_ISSUE
+#define PF_EARLY_ISSUE 2
+#endif
+
 namespace pf {
+
+constexpr int kStageBar = 14;
+
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -131,7 +145,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
     }
     __syncthreads();
 
-    auto issue = [&](int plane, int stage, int x0, int y0) {
+    // inputs of plane step `seq` (plane `plane` of the tile at (x0, y0)) into stage seq & 1, S slot seq & 3
+    auto issue = [&](int plane, int seq, int x0, int y0) {
+        const int stage = seq & 1;
         mbar_arrive_expect_tx(&bars[stage], a.tx_bytes);
 #pragma unroll
         for (int k = 0; k < 3; ++k)
@@ -139,33 +155,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                         plane + 1);
         tma_load_4d(Us + stage * L::USZ, &a.tm_u, &bars[stage], x0, y0, lb, plane + 1);
         tma_load_4d(Ds + stage * L::USZ, &a.tm_D, &bars[stage], x0, y0, lb, plane);
-        if (a.s_ch) tma_load_4d(Ss + (plane & 3) * SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
+        if (a.s_ch) tma_load_4d(Ss + (seq & 3) * SSZ, &a.tm_S, &bars[stage], x0, y0, 0, plane);
     };
     const uint64_t pol_out = policy_evict_first();
 
     float resid = 0.f;
     int kbase = 0;
-    __shared__ int s_item;
-    // one ticket per cluster: rank 0 grabs it and publishes it to both CTAs before a cluster barrier
+    // One ticket per cluster: rank 0 grabs it and publishes it to both CTAs before a cluster barrier.  The
+    // (n+1)-th item of the cluster is taken at the start of its n-th, so the refills of the n-th item's last two
+    // plane steps can already load the (n+1)-th item's first two planes (no pipeline bubble between items; the
+    // plane steps carry a sequence number k across items: stage k & 1, S slot k & 3).
+    __shared__ int s_item[2];
     if (blockIdx.x == 0 && tid == 0) *a.ticket_next = 0ull;   // the next launch's counter (see pf_staged.cuh)
-    auto grab_publish = [&]() {
+    auto grab_publish = [&](int slot) {
         if (rank == 0 && tid == 0) {
             const unsigned long long t = atomicAdd(a.ticket, 1ull);
             const int it = t < (unsigned long long)(a.items - a.item_begin) ? a.item_begin + (int)t : a.items;
-            s_item = it;
-            st_cluster_s32(map_to_rank(&s_item, 1), it);
+            s_item[slot] = it;
+            st_cluster_s32(map_to_rank(&s_item[slot], 1), it);
         }
     };
-    grab_publish();
+    grab_publish(0);
     cluster_sync_all();
-    for (int item = s_item; item < a.items; item = s_item) {
-        const int chunk = item / a.tiles, tile = item - chunk * a.tiles;
-        int x0, y0;
-        tile_origin(a, tile, TY, x0, y0);
-        const int zc0 = chunk < a.nb ? (chunk == 0 ? a.bplane0 : a.bplane1) : a.zlo + (chunk - a.nb) * a.zchunk;
-        const int zc1 = chunk < a.nb ? zc0 + 1 : min(zc0 + a.zchunk, a.zhi);
-        const bool has_above = (a.zg0 + zc1) < a.nzg;
-        const int pend = has_above ? zc1 : zc1 - 1;
+    int nit = 0, prev_steps = 0;
+    for (int item = s_item[0]; item < a.items; item = s_item[(++nit) & 1]) {
+        const ItemGeom cg = item_geom(a, item, TY);
+        const int x0 = cg.x0, y0 = cg.y0, zc0 = cg.zc0, zc1 = cg.zc1, pend = cg.pend;
+        const bool has_above = cg.has_above;
         const int x = x0 + (lx < 0 ? 0 : lx), y = y0 + ly;
         const bool valid = (lx >= 0) && x < a.nx && y < a.ny;
         const int pix = valid ? y * a.pitch + x : 0;
@@ -173,13 +189,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
         const int uoff = ly * UW + (lx < 0 ? 0 : lx);
         const int roff = ly * RS + (lx < 0 ? 0 : lx);
 
-        // both CTAs have read s_item and finished the previous item's readers of the ring / stage buffers
+        // next item (its slot was last read two items ago); after the barrier both CTAs see it, and both have
+        // finished the previous item's readers of the ring / staging buffers
+        grab_publish((nit + 1) & 1);
         cluster_sync_all();
-        grab_publish();   // next item, read after this item's cluster barriers
-        if (tid == 0) {
+        const int nxt = s_item[(nit + 1) & 1];
+        const ItemGeom ng = item_geom(a, nxt < a.items ? nxt : a.item_begin, TY);
+        const int nsteps_next = nxt < a.items ? ng.steps() : 0;
+        if (tid == 0) {   // the item's first planes the previous item's last steps did not prefetch
             fence_proxy_async();
-            issue(zc0, kbase & 1, x0, y0);
-            if (zc0 + 1 <= pend) issue(zc0 + 1, (kbase + 1) & 1, x0, y0);
+            const int n0 = min(prev_steps >= 2 ? 0 : 2 - prev_steps, cg.steps());
+            for (int i = 0; i < n0; ++i) issue(zc0 + i, kbase + i, x0, y0);
         }
         float qA[3][NLC], qB[3][NLC];
 #pragma unroll
@@ -193,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
         auto stage_b = [&](const int z, const float (&Mn)[NLC], bool has_z, const float (&qc)[3][NLC]) {
             if (!(is_main && valid)) return;
             const float *Rz = R + (z % 3) * RING;
-            const float *Sz = Ss + (z & 3) * SSZ + ly * SW + lx;
+            const float *Sz = Ss + ((kbase + z - zc0) & 3) * SSZ + ly * SW + lx;
             const float cx = x < a.nx - 1 ? a.ctau : 0.f, cy = y < a.ny - 1 ? a.ctau : 0.f;
             const float cz = (has_z && a.zg0 + z < a.nzg - 1) ? a.ctau : 0.f;
             const float sb = a.s_ch == 1 ? Sz[0] : 1.f;
@@ -257,6 +277,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                 }
                 label_half<NLC>(dl, uold, rr, ut, a.shift, k2, mh, th, sh);
             }
+            if (PF_EARLY_ISSUE && warp != 0) named_arrive(kStageBar, 32 * (TY + 2));
+            // refill of stage st with step k + 2: this item's plane p + 2, else the next item's first planes
+            auto refill = [&]() {
+                fence_proxy_async();
+                if (p + 2 <= pend) issue(p + 2, k + 2, x0, y0);
+                else if (p + 1 - pend < nsteps_next) issue(ng.zc0 + (p + 1 - pend), k + 2, ng.x0, ng.y0);
+            };
+            auto early_issue = [&]() {
+                if (warp == 0) {
+                    named_bar(kStageBar, 32 * (TY + 2));
+                    if (tid == 0) refill();
+                }
+            };
+            if (PF_EARLY_ISSUE == 1) early_issue();
             // ---- ONE exchange of (m_h, T_h, s_h) with the partner CTA (label_update's split form, pf_math.cuh)
             const int xb = k & 1;   // exchange buffer / mbarrier of this plane; phase = (k >> 1) & 1
             if (tid == 0) mbar_arrive_expect_tx(&bars[2 + xb], kXBytes);   // arm (bytes may already be in)
@@ -264,6 +298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
                 st_async_f32x4(x_remote + xb * kXBuf, mh, th, sh, barx_remote + xb * 8u);
             }
             mbar_wait(&bars[2 + xb], (k >> 1) & 1);
+            if (PF_EARLY_ISSUE == 2) early_issue();
             float sum = 1.f;
             if (lx >= 0) {
                 const float4 xo = reinterpret_cast<const float4 *>(X2)[xb * CL::XPTS + xpt];
@@ -298,10 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
             if (tid == 0) bulk_wait_read_all();
             __syncthreads();   // ring slot p complete; stage st consumed; staged u complete
             if (tid == 0) {
-                if (p + 2 <= pend) {
-                    fence_proxy_async();
-                    issue(p + 2, st, x0, y0);
-                }
+                if (!PF_EARLY_ISSUE) refill();
                 if (p < zc1) {
                     tma_store_4d(&a.tm_uo, Uo + (p & 1) * L::UOSZ, x0, y0, lb, p + 1, pol_out);
                     if (a.link_below && p == 0)
@@ -335,7 +367,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (TY + 2), 1)
             bulk_commit();
             bulk_wait_read_all();
         }
-        kbase += pend - zc0 + 1;
+        kbase += cg.steps();
+        prev_steps = cg.steps();
     }
     if (lane == 0) bulk_wait_all();
     cluster_sync_all();   // no CTA leaves while its partner may still write into its shared memory

@@ -90,6 +90,25 @@ __device__ __forceinline__ void tile_origin(const StagedArgs &a, int t, int ty_r
     y0 = ty * ty_rows;
 }
 
+// Geometry of one work item: tile origin, the chunk's planes [zc0, zc1) and the last plane step pend (zc1 when a
+// plane above exists: its stage A gives the masses M(zc1) the flow step of plane zc1 - 1 needs).
+struct ItemGeom {
+    int x0, y0, zc0, zc1, pend;
+    bool has_above;
+    __device__ __forceinline__ int steps() const { return pend - zc0 + 1; }
+};
+
+__device__ __forceinline__ ItemGeom item_geom(const StagedArgs &a, int item, int ty_rows) {
+    ItemGeom g;
+    const int chunk = item / a.tiles, tile = item - chunk * a.tiles;
+    tile_origin(a, tile, ty_rows, g.x0, g.y0);
+    g.zc0 = chunk < a.nb ? (chunk == 0 ? a.bplane0 : a.bplane1) : a.zlo + (chunk - a.nb) * a.zchunk;
+    g.zc1 = chunk < a.nb ? g.zc0 + 1 : min(g.zc0 + a.zchunk, a.zhi);
+    g.has_above = (a.zg0 + g.zc1) < a.nzg;
+    g.pend = g.has_above ? g.zc1 : g.zc1 - 1;
+    return g;
+}
+
 // NSTG: input stages in flight (2: one plane of look-ahead; 3: two, where shared memory allows -- short tiles).
 // SR: S ring slots covering the planes p - 1 .. p + NSTG.
 template <int NI, int NL, int TY, int OSTAGE, int MODEL, int G, int NSTG_ = 2>
