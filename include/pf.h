@@ -50,7 +50,7 @@ typedef enum {
     PF_ERR_GRAPH = 2,   /* label graph violates the DAGMF assumptions (all violations listed) */
     PF_ERR_OOM = 3,     /* device allocation failed */
     PF_ERR_CUDA = 4,    /* CUDA runtime error (message carries cudaGetErrorString) */
-    PF_ERR_UNSUPPORTED = 5, /* graph shape outside the compiled kernel set */
+    PF_ERR_UNSUPPORTED = 5, /* graph beyond 31 non-source nodes / 16 end labels, or an unsupported combination */
     PF_ERR_NUMERIC = 6, /* a(x) <= 0 or not finite detected at a check (message names the voxel) */
     PF_ERR_STATE = 7    /* solver poisoned by an earlier error, or calls out of order (split iterations,
                            linked slabs, IPC protocol) */
@@ -145,7 +145,13 @@ typedef struct {
  * S -> N_1 -> ... -> N_N, end labels L_0..L_N (increasing node ids) with S -> L_0 and N_i -> L_i, all
  * weights 1 -- whose end labels have identically zero capacity (scalar 0, or factor 0 of a
  * PF_S_SCALED_FIELD) is solved by the dedicated Ishikawa kernels: flows are stored for the N level
- * nodes only (prefix excesses, suffix masses), N <= 15.  Any other graph runs Algorithm 2. */
+ * nodes only (prefix excesses, suffix masses), N <= 15.  Any other graph runs Algorithm 2.
+ *
+ * Graph size: up to 31 non-source nodes and 16 end labels (else PF_ERR_UNSUPPORTED).  Graphs
+ * with <= 4 internal and <= 16 non-source nodes (Potts up to 16 labels, the configs' HMF tree and DAG) run on
+ * the fused one-pass kernels; larger ones on the generic two-pass kernels (pf_generic.cu: same arithmetic,
+ * masses through an HBM scratch buffer), which take whole volumes with the fp32 label state only
+ * (PF_ERR_UNSUPPORTED for a slab, ipc, u_half or tblock). */
 
 /* Create a solver for the (slab of the) volume and initialise the state:
  * u_L = 1/|L|, q = 0 (reading R8).

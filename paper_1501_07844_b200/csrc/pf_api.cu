@@ -77,7 +77,7 @@ void free_all(pf_solver *s) {
         }
     }
     void *ptrs[] = {s->u_alloc[0], s->u_alloc[1], s->q_alloc[0], s->q_alloc[1], s->D_alloc, s->S_alloc, s->D16,
-                    s->p_alloc, s->pS_alloc, s->uint_alloc,
+                    s->p_alloc, s->pS_alloc, s->uint_alloc, s->M_alloc, s->d_wide,
                     s->d_resid, s->d_err, s->d_flag, s->d_energy};
     for (void *p : ptrs)
         if (p) cudaFreeAsync(p, s->stream);
@@ -86,6 +86,7 @@ void free_all(pf_solver *s) {
     s->D_alloc = s->S_alloc = nullptr;
     s->D16 = nullptr;
     s->p_alloc = s->pS_alloc = s->uint_alloc = nullptr;
+    s->M_alloc = s->d_wide = nullptr;
     s->d_resid = nullptr;
     s->d_err = nullptr;
     s->d_flag = nullptr;
@@ -368,10 +369,14 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         for (int l = 0; l < gc.NL && zero; ++l) zero = S->scalars[gc.node_of_pos[gc.NI + l]] == 0.f;
         gc.model = zero ? 1 : 0;
     }
-    if (gc.model == 0 && (gc.NI > kMaxInternal || gc.NV > kMaxNodes))
-        return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes exceeds the compiled kernel set "
-                                        "(<= %d internal, <= %d non-source nodes)", gc.NI, gc.NL, kMaxInternal,
-                    kMaxNodes);
+    // beyond the compiled kernel set: the generic two-pass path (pf_generic.cu), whole volumes, fp32 state
+    // (PF_GENERIC=1, tests: any model-0 graph on the generic kernels -- bitwise those of the dense compiled kernels)
+    const char *genv = getenv("PF_GENERIC");
+    gc.generic = gc.model == 0 && (gc.NI > kMaxInternal || gc.NV > kMaxNodes || (genv && strcmp(genv, "1") == 0));
+    if (gc.generic && (slab || cfg->ipc || cfg->u_half || cfg->tblock == 2))
+        return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes run on the generic kernels (beyond the "
+                                        "compiled set of <= %d internal, <= %d non-source nodes): whole volumes, "
+                                        "fp32 label state, no ipc / tblock", gc.NI, gc.NL, kMaxInternal, kMaxNodes);
     gc.NF = gc.model == 1 ? gc.NI : gc.NV;
     if (cfg->method != PF_METHOD_PSEUDO_FLOW && cfg->method != PF_METHOD_EXPLICIT_ALM)
         return fail(PF_ERR_INVALID, "config: bad method");
@@ -402,7 +407,12 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     s->gc = gc;
     s->cfg = *cfg;
     s->s_kind = S->kind;
-    if (!iter_kernel_lookup(gc.NI, gc.NL, gc.model, &s->kinfo)) {
+    if (gc.generic) {
+        s->kinfo.func = generic_kernel_func();
+        s->kinfo.threads = 256;
+        s->kinfo.smem_bytes = 0;
+        s->kinfo.tile_y = 8;
+    } else if (!iter_kernel_lookup(gc.NI, gc.NL, gc.model, &s->kinfo)) {
         delete s;
         return fail(PF_ERR_UNSUPPORTED, "no compiled kernel for %d internal / %d end nodes", gc.NI, gc.NL);
     }
@@ -416,7 +426,7 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
             for (int j = 0; j < gc.NV && j < kMaxNodes; ++j)
                 if (gc.g.w[i][j] != 0.f) mask |= 1ull << (i * 16 + j);
         if (gc.model != 0 || (getenv("PF_DENSE_GRAPH") && strcmp(getenv("PF_DENSE_GRAPH"), "1") == 0)) mask = kDenseMask;
-        s->staged = !alm && !want_global &&
+        s->staged = !alm && !want_global && !gc.generic &&
                     staged_kernel_lookup(gc.NI, gc.NL, gc.model, cfg->d_bf16 ? 1 : 0, cfg->u_half ? 1 : 0, mask,
                                          &s->sinfo) &&
                     encode_fn() != nullptr;
@@ -496,6 +506,11 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
                            ? 1 : (S->kind == PF_S_FIELD_PER_NODE ? NF : 0);
     if (nS > 0 && (st = alloc(s, (void **)&s->S_alloc, (size_t)(nzl * nS * P) * sizeof(float), "S")) != PF_OK)
         return bail(st);
+    if (gc.generic) {   // masses scratch of the two-pass generic iteration, and the graph for the energy kernel
+        if ((st = alloc(s, (void **)&s->M_alloc, (size_t)(nzl * gc.NV * P) * sizeof(float), "masses (generic)")) != PF_OK)
+            return bail(st);
+        if ((st = alloc(s, (void **)&s->d_wide, sizeof(GraphWide), "graph (generic)")) != PF_OK) return bail(st);
+    }
     if ((st = alloc(s, (void **)&s->d_resid, 64, "resid")) != PF_OK) return bail(st);
     if ((st = alloc(s, (void **)&s->d_err, 64, "err")) != PF_OK) return bail(st);
     e = cudaMemsetAsync(s->d_err, 0, 64, s->stream);
@@ -527,8 +542,10 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
     }
     if (S->kind == PF_S_SHARED_FIELD || S->kind == PF_S_SCALED_FIELD) {
         if (!S->fields[0]) return bail(fail(PF_ERR_INVALID, "smoothness: fields[0] is NULL"));
-        for (int p = 0; p < NF; ++p)  // per-node factor of the shared field
-            s->gc.g.s[p] = S->kind == PF_S_SHARED_FIELD ? 1.f : S->scalars[gc.node_of_pos[p]];
+        for (int p = 0; p < NF; ++p) {  // per-node factor of the shared field
+            s->gc.gw.s[p] = S->kind == PF_S_SHARED_FIELD ? 1.f : S->scalars[gc.node_of_pos[p]];
+            if (p < kMaxNodes) s->gc.g.s[p] = s->gc.gw.s[p];
+        }
         e = copy_volume(true, s->S_alloc, 1, (float *)S->fields[0], s->nx, s->ny, s->pitch, nzl, s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
     } else if (S->kind == PF_S_FIELD_PER_NODE) {
@@ -540,7 +557,10 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
             if (e != cudaSuccess) { cuda_fail(s, e, "upload S"); return bail(PF_ERR_CUDA); }
         }
     } else {
-        for (int p = 0; p < NF; ++p) s->gc.g.s[p] = S->scalars[gc.node_of_pos[p]];
+        for (int p = 0; p < NF; ++p) {
+            s->gc.gw.s[p] = S->scalars[gc.node_of_pos[p]];
+            if (p < kMaxNodes) s->gc.g.s[p] = s->gc.gw.s[p];
+        }
     }
     if (nS > 0) {
         cudaMemsetAsync(s->d_flag, 0, 4, s->stream);
@@ -551,6 +571,12 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         e = cudaStreamSynchronize(s->stream);
         if (e != cudaSuccess) { cuda_fail(s, e, "validate S"); return bail(PF_ERR_CUDA); }
         if (flag) return bail(fail(PF_ERR_INVALID, "smoothness: S must be >= 0 and finite everywhere"));
+    }
+    if (gc.generic) {
+        e = cudaMemcpyAsync(s->d_wide, &s->gc.gw, sizeof(GraphWide), cudaMemcpyHostToDevice, s->stream);
+        if (e != cudaSuccess) { cuda_fail(s, e, "upload graph"); return bail(PF_ERR_CUDA); }
+        e = cudaStreamSynchronize(s->stream);   // the source is host memory of the solver
+        if (e != cudaSuccess) { cuda_fail(s, e, "upload graph"); return bail(PF_ERR_CUDA); }
     }
     if ((st = init_state(s)) != PF_OK) return bail(st);
     // kernel configuration
@@ -822,6 +848,9 @@ pf_status launch_items(pf_solver *s, int ib, int ie, int check, int reserve_sms)
         CK(cudaLaunchKernel(s->sinfo.func, dim3(grid), dim3(s->sinfo.threads), args, s->staged_smem, s->stream),
            s->cluster ? "launch pf_iter_cluster" : "launch pf_iter_staged");
         s->launch_parity ^= 1;
+    } else if (s->gc.generic) {
+        CK(launch_generic_iteration(s, check), "launch pf_generic_masses / pf_generic_flows");
+        s->launches++;   // two kernels per iteration
     } else {
         IterArgs a;
         memset(&a, 0, sizeof(a));
@@ -994,6 +1023,7 @@ pf_status capture_graph(pf_solver *s) {
         s->stream = real;
         ok = cudaStreamEndCapture(cap, &g) == cudaSuccess && st == PF_OK;
     }
+    s->graph_launches = s->launches - l0;   // kernels per replay (the generic path: two per iteration; tblock: 1/2)
     s->cur = cur0;
     s->launch_parity = par0;
     s->iters = it0;
@@ -1035,7 +1065,7 @@ pf_status pf_iterate(pf_solver *s, int32_t n, float *residual) {
         if (!s->graph || s->cur != s->graph_cur || s->launch_parity != s->graph_parity) break;
         CK(cudaGraphLaunch(s->graph, s->stream), "graph launch");
         s->iters += P;
-        s->launches += (int64_t)P * (s->cfg.check_every > 0 ? 1 : 1);
+        s->launches += s->graph_launches;
         any_check = any_check || s->cfg.check_every > 0;
         n -= P;
     }
@@ -1238,6 +1268,7 @@ pf_status pf_get_energy(pf_solver *s, double *primal, double *dual) {
     a.s_kind = s->s_kind == PF_S_SCALED_FIELD ? 1 : s->s_kind;
     a.cap = s->cfg.cap;
     a.g = s->gc.g;
+    a.gw = reinterpret_cast<const GraphWide *>(s->d_wide);   // generic graphs: weights and capacity scalars of every position
     CK(launch_energy(a, s->d_energy + 2, kEnergyBlocks, s->d_energy, s->stream), "energy kernel");
     s->launches += 2;
     double h[2];

@@ -98,7 +98,7 @@ __device__ __forceinline__ void labels_at(const EnergyArgs &a, int64_t ub, int64
     }
     for (int i = NI - 1; i >= 0; --i) {
         double acc = 0.0;
-        for (int j = i + 1; j < NV; ++j) acc += (double)a.g.w[i][j] * out[j];
+        for (int j = i + 1; j < NV; ++j) acc += (double)(a.gw ? a.gw->w[i][j] : a.g.w[i][j]) * out[j];
         out[i] = (float)acc;
     }
 }
@@ -173,8 +173,9 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
         }
         for (int v = 0; v < NF; ++v) {  // nodes without a flow have zero capacity
             float sv;
-            if (a.s_kind == 0) sv = a.g.s[v];
-            else if (a.s_kind == 1) sv = a.S[z * P + pix] * a.g.s[v];
+            const float sn = a.gw ? a.gw->s[v] : a.g.s[v];
+            if (a.s_kind == 0) sv = sn;
+            else if (a.s_kind == 1) sv = a.S[z * P + pix] * sn;
             else sv = a.S[(z * NF + v) * P + pix];
             e_acc += (double)sv * (a.cap == 0 ? sqrt(g2[v]) : g1[v]);
         }
@@ -200,7 +201,7 @@ __global__ void energy_kernel(const EnergyArgs a, double *partial) {
             }
         } else {
             for (int ii = 0; ii < NI; ++ii)
-                for (int j = ii + 1; j < NV; ++j) d[j] += (double)a.g.w[ii][j] * d[ii];
+                for (int j = ii + 1; j < NV; ++j) d[j] += (double)(a.gw ? a.gw->w[ii][j] : a.g.w[ii][j]) * d[ii];
         }
         double mn = d[NI];
         for (int l = 1; l < NL; ++l) mn = fmin(mn, d[NI + l]);

@@ -20,6 +20,7 @@ struct EnergyArgs {
     int model;   // 0: DAG (dense weights), 1: Ishikawa chain
     int s_kind, cap;
     GraphConst g;
+    const GraphWide *gw;   // non-null: the graph is beyond the compiled set (GraphConst unused), device memory
 };
 
 constexpr int kEnergyBlocks = 592;

@@ -93,9 +93,11 @@ pf_status compile_graph(const pf_graph *gr, Compiled *out) {
                     (last || has_edge(lev[i], lev[i + 1]));
         }
     }
-    if (!chain && (NI > kMaxInternal || NI + NL > kMaxNodes))
-        return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes exceeds the compiled kernel set "
-                                        "(<= %d internal, <= %d non-source nodes)", NI, NL, kMaxInternal, kMaxNodes);
+    // graphs beyond the compiled kernel set (<= kMaxInternal internal, <= kMaxNodes non-source nodes) run on the
+    // generic path (pf_generic.cu) up to kWideNodes non-source nodes and 16 end labels
+    if (NI + NL > kWideNodes || NL > 16)
+        return fail(PF_ERR_UNSUPPORTED, "graph: %d internal + %d end nodes exceeds the supported size "
+                                        "(<= %d non-source nodes, <= 16 end labels)", NI, NL, kWideNodes);
     if (chain && NL > kMaxNodes)
         return fail(PF_ERR_UNSUPPORTED, "graph: Ishikawa chain with %d labels exceeds %d", NL, kMaxNodes);
     out->chain = chain;
@@ -117,10 +119,15 @@ pf_status compile_graph(const pf_graph *gr, Compiled *out) {
         out->node_of_pos.push_back(v);
     }
     memset(&out->g, 0, sizeof(out->g));
-    for (int v = 1; v < n && NI <= kMaxInternal; ++v) {  // dense weights (unused by the chain kernels)
+    memset(&out->gw, 0, sizeof(out->gw));
+    for (int v = 1; v < n; ++v) {  // dense weights (unused by the chain kernels)
         if (kids[v].empty()) continue;
         const int i = out->pos_of_node[v];
-        for (auto &c : kids[v]) out->g.w[i][out->pos_of_node[c.first]] += c.second;
+        for (auto &c : kids[v]) {
+            const int j = out->pos_of_node[c.first];
+            out->gw.w[i][j] += c.second;
+            if (NI <= kMaxInternal && NI + NL <= kMaxNodes) out->g.w[i][j] += c.second;
+        }
     }
     out->w_src.assign(out->NV, 0.f);
     for (auto &c : kids[0]) out->w_src[out->pos_of_node[c.first]] += c.second;

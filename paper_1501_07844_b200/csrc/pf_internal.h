@@ -61,7 +61,9 @@ struct Compiled {
     int NF = 0;          // flow-carrying nodes (positions 0..NF-1)
     std::vector<int> pos_of_node;  // node id -> position, S -> -1
     std::vector<int> node_of_pos;
-    GraphConst g;
+    GraphConst g;    // dense weights of the compiled kernels (NI <= kMaxInternal, NV <= kMaxNodes)
+    GraphWide gw;    // dense weights of every model-0 graph up to kWideNodes (the generic path, energies)
+    bool generic = false;   // beyond the compiled kernel set: pf_generic.cu
     std::vector<std::vector<float>> W;  // W[pos][leaf slot] path weights
     std::vector<float> w_src;           // weight of the edge S -> position (0: none)
 };
@@ -93,6 +95,8 @@ struct pf_solver {
     bool alm = false;                                 // PF_METHOD_EXPLICIT_ALM (pf_alm.cu)
     float *p_alloc = nullptr, *pS_alloc = nullptr;    // ALM sink flows [z][l][y][pitch], source flow [z][y][pitch]
     float *uint_alloc = nullptr;                      // ALM on a DAG: u of the internal nodes [z][NI][y][pitch]
+    float *M_alloc = nullptr;                         // generic path (pf_generic.cu): masses [z][v][y][pitch]
+    float *d_wide = nullptr;                          // GraphWide on the device (energy kernel, generic graphs)
     const void *Dptr() const { return D16 ? (const void *)D16 : (const void *)D_alloc; }
     float *u[2] = {nullptr, nullptr}, *q[2] = {nullptr, nullptr};
     int cur = 0;
@@ -118,6 +122,7 @@ struct pf_solver {
     cudaGraphExec_t graph = nullptr;
     int graph_iters = 0, graph_cur = 0, graph_parity = 0;
     bool graph_failed = false;
+    int64_t graph_launches = 0;     // kernel launches one replay of the captured graph stands for
     unsigned int *d_flag = nullptr;
     double *d_energy = nullptr;  // partials + result
     IterKernelInfo kinfo{};
@@ -186,3 +191,9 @@ bool encode4d(CUtensorMap *m, const void *base, int64_t nx, int64_t ny, int64_t 
               int bx, int by, int bc, int dtype = 0);
 
 }  // namespace pfi
+
+namespace pf {
+// generic path (pf_generic.cu): graphs beyond the compiled kernel set, two kernels per iteration
+cudaError_t launch_generic_iteration(const pf_solver *s, int check);
+const void *generic_kernel_func();
+}  // namespace pf

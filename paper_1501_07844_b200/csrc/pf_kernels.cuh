@@ -213,6 +213,14 @@ __global__ void __launch_bounds__(32 * TY + 64) pf_iter_kernel(const IterArgs a)
 }
 
 // Launch table entry (pf_iter_table.cu); returns false if (NI, NL) is not compiled in.
+// Generic path (pf_generic.cu): any DAG up to kWideNodes non-source nodes (<= 16 end labels) -- the graphs beyond
+// the compiled kernel set (> kMaxInternal internal or > kMaxNodes nodes).  Dense weights over all positions.
+constexpr int kWideNodes = 31;
+struct GraphWide {
+    float w[kWideNodes][32];   // w[i][j]: weight of edge (position i -> position j), i internal; 0 = no edge
+    float s[32];               // capacity scalar per position
+};
+
 struct IterKernelInfo {
     const void *func;
     int threads;

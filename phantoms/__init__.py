@@ -150,6 +150,39 @@ def ishikawa_graph(N: int) -> Graph:
     return Graph(2 * N + 2, e, names)
 
 
+def wide_dag(ni: int, nl: int, seed: int) -> Graph:
+    """A seeded random label DAG with `ni` internal nodes (ids 1..ni) and `nl` end labels (ids ni+1..ni+nl), for
+    the graphs beyond the compiled kernel set (up to 31 non-source nodes, 16 end labels).  A random
+    tree below S (internal node i hangs under S or an earlier internal node, weight 1; every internal node gets at
+    least one end label), then about a quarter of the end labels and of the non-top internal nodes get a second,
+    earlier parent with weights 0.5 / 0.5 -- so W_(S,L) = 1 stays exact for every end label (reading R9)."""
+    rng = SplitMix64(seed)
+    top = max(1, ni // 4)
+    par = {}
+    for i in range(1, ni + 1):
+        par[i] = [(0, 1.0)] if i <= top else [(rng.randint(1, i - 1), 1.0)]
+    has_child = {p for i in par for p, _ in par[i] if p != 0}
+    bare = [i for i in range(1, ni + 1) if i not in has_child]
+    assert len(bare) <= nl, "too few end labels for the internal tree"
+    for k in range(nl):
+        leaf = ni + 1 + k
+        par[leaf] = [(bare[k], 1.0)] if k < len(bare) else [(rng.randint(0, ni), 1.0)]
+    def second_parent(v, lo, hi):
+        p0 = par[v][0][0]
+        p1 = rng.randint(lo, hi)
+        if p1 != p0:
+            par[v] = [(p0, 0.5), (p1, 0.5)]
+    for k in range(nl):
+        if rng.uniform() < 0.25:
+            second_parent(ni + 1 + k, 1, ni)
+    for i in range(top + 1, ni + 1):
+        if rng.uniform() < 0.25:
+            second_parent(i, 1, i - 1)
+    edges = sorted((p, v, w) for v in par for p, w in par[v])
+    names = ["S"] + [f"N{i}" for i in range(1, ni + 1)] + [f"L{k}" for k in range(nl)]
+    return Graph(ni + nl + 1, edges, names)
+
+
 # --------------------------------------------------------------------------
 # Configs (BASELINE.json configs[0..4]; unspecified details = SURVEY §8.4.1)
 # --------------------------------------------------------------------------
@@ -172,6 +205,7 @@ class Config:
     tau: float = 0.1
     cap: str = "l2"
     seed: int = 0
+    wide_ni: int = 0     # kind "wide": internal nodes of wide_dag(wide_ni, classes, seed)
 
     @property
     def K(self) -> int:
@@ -190,6 +224,8 @@ class Config:
             return dag_graph()
         if self.kind == "ishikawa":
             return ishikawa_graph(self.classes - 1)
+        if self.kind == "wide":
+            return wide_dag(self.wide_ni, self.classes, self.seed)
         raise ValueError(self.kind)
 
     def mu(self) -> np.ndarray:
