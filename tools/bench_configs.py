@@ -23,6 +23,12 @@ import phantoms as P  # noqa: E402
 def cfg_of(name):
     if name == "C5slab":
         return P.config("C5").resized(768, 768, 96, name="C5slab")
+    if name in ("W8", "W8s", "W16s"):   # diagnostics, C5's recipe: K = 8 (one-CTA staged kernel) on 768^2 / 256^2
+        # planes, K = 16 (cluster kernel) on 256^2 planes -- the same voxel count as C5slab
+        K = 16 if name == "W16s" else 8
+        nx, nz = (768, 96) if name == "W8" else (256, 864)
+        return P.Config(name, 3, nx, nx, nz, "potts", K, 60 if K == 16 else 28, 0.15, "abs", "edge", 0.05, 200,
+                        seed=1005)
     if name in ("T2", "T3", "T4"):   # f3 demonstration volumes: C2's recipe (256^3, edge S) with K = 2..4 labels
         K = int(name[1])
         return P.Config(name, 3, 256, 256, 256, "potts", K, 4 * K, 0.15, "sq", "edge", 0.05, 300, seed=2020)

@@ -13,7 +13,10 @@ import phantoms as P  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-cfg = P.config("C5").resized(768, 768, 96, name="C5slab") if name == "C5slab" else P.config(name)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from bench_configs import cfg_of  # noqa: E402
+
+cfg = cfg_of(name)
 inp = P.generate(cfg)
 g = inp.graph
 D = [np.ascontiguousarray(inp.D[l]) for l in range(inp.D.shape[0])]
