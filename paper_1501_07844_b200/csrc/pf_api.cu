@@ -221,11 +221,16 @@ void choose_chunking(pf_solver *s) {
         s->tiles_x = gx;
         // tile order (pf_staged.cuh tile_origin): full rows.  Narrower strips (to bring a tile's y-neighbour
         // closer in the ticket order) measured slower on 768-wide planes: C5slab strips of 12 / 8 / 6 / 4 tiles
-        // 7.15 / 7.21 / 7.32 / 8.77 ms vs 7.10 (full rows of 24), C4 strips of 5: 2.09 vs 1.73 ms (tools/ab.py)
+        // 7.15 / 7.21 / 7.32 / 8.77 ms vs 7.10 (full rows of 24), C4 strips of 5: 2.09 vs 1.73 ms (tools/ab.py).
+        // Row groups (PF_STRIP = -h: h tile rows, column-major inside, the y-neighbour one ticket away and the
+        // x-neighbour h) also measured slower: C5slab h = 2 / 4 / 8 7.06 / 7.17 / 8.69 vs 7.03 ms, DRAM reads
+        // 21.2 / 21.7 / 26.5 vs 21.4 GB per iteration (profiles/r2/cluster_rowgroups.txt): the x-neighbour,
+        // whose 256-byte blocks a q row shares, has to stay the adjacent ticket.
         s->strip = gx;
         if (const char *sp = getenv("PF_STRIP")) {   // experiments (tools/ab.py): force the strip width
             const int want = atoi(sp);
             if (want > 0) s->strip = std::min(want, gx);
+            if (want < 0) s->strip = want;   // row groups of -want tile rows, column-major inside a group
         }
         s->tiles = (int)tiles;
         s->items_b = (int)(tiles * s->nb);
@@ -238,6 +243,10 @@ void choose_chunking(pf_solver *s) {
         s->grid = dim3(gx, gy, (nzl + s->zchunk - 1) / s->zchunk);
     }
 }
+
+#ifndef PF_L2PROMO_DEFAULT
+#define PF_L2PROMO_DEFAULT 3
+#endif
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
@@ -267,11 +276,21 @@ bool encode4d(CUtensorMap *m, const void *base, int64_t nx, int64_t ny, int64_t 
                              (cuuint64_t)(pitch * ny * nch * es_b)};
     cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bc, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
+    // L2 promotion of the TMA requests: PF_L2PROMO = 0 (none) / 1 (64 B) / 2 (128 B) / 3 (256 B) overrides the
+    // default (experiments, tools/ab.py)
+    static const int promo = [] {
+        const char *e = getenv("PF_L2PROMO");
+        return e && e[0] >= '0' && e[0] <= '3' ? e[0] - '0' : PF_L2PROMO_DEFAULT;
+    }();
+    const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                      : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                      : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     return fn(m, dtype == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : dtype == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
               4, (void *)base, dims,
               strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_SWIZZLE_NONE, pr,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -345,6 +364,8 @@ pf_status pf_create(const pf_dims *dims, const pf_graph *graph, const float *con
         z1 = slab->z_end;
         if (z0 < 0 || z1 > dims->nz || z1 <= z0) return fail(PF_ERR_INVALID, "slab: need 0 <= z_begin < z_end <= nz");
     }
+    if (const char *fg = getenv("PF_L2FETCH"))   // experiments: device-wide L2 fetch granularity hint (32 / 64 / 128)
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
     Compiled gc;
     pf_status st = compile_graph(graph, &gc);
     if (st != PF_OK) return st;

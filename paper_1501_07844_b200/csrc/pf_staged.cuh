@@ -77,10 +77,20 @@ struct StagedArgs {
 __host__ __device__ constexpr int round32(int n) { return (n + 31) / 32 * 32; }
 
 // Tile origin of the t-th tile of a z-chunk.  Tiles are taken in column strips of `strip` tiles (the last
-// strip may be narrower), row-major inside a strip.  The default is one strip of full rows (narrower strips,
-// which bring a tile's y-neighbour closer in the ticket order, measured slower: pf_api.cu choose_chunking).
+// strip may be narrower), row-major inside a strip; strip < 0: row groups of -strip tile rows, column-major inside
+// a group.  The default is one strip of full rows (narrower strips and row groups, which bring a tile's
+// y-neighbour closer in the ticket order, measured slower: pf_api.cu choose_chunking).
 __device__ __forceinline__ void tile_origin(const StagedArgs &a, int t, int ty_rows, int &x0, int &y0) {
     const int tiles_y = a.tiles / a.tiles_x;
+    if (a.strip < 0) {   // row groups of h tile rows, column-major inside a group: a tile's y-neighbour inside the
+        const int h = -a.strip;                     // group is the next ticket, its x-neighbour h tickets away
+        const int gblk = h * a.tiles_x, gidx = t / gblk;
+        const int hh = min(h, tiles_y - gidx * h);
+        const int r = t - gidx * gblk, cx = r / hh;
+        x0 = cx * 32;
+        y0 = (gidx * h + (r - cx * hh)) * ty_rows;
+        return;
+    }
     const int sblk = a.strip * tiles_y;           // tiles per full strip
     const int sidx = t / sblk;
     const int w = min(a.strip, a.tiles_x - sidx * a.strip);

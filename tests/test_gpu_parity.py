@@ -213,6 +213,34 @@ def test_many_label_potts_cluster_kernel(K, dims, shift, monkeypatch):
     s.close()
 
 
+def test_tile_order_does_not_change_results(monkeypatch):
+    """The order in which the ticket queue hands out the tiles (full rows, column strips, row groups:
+    pf_staged.cuh tile_origin, PF_STRIP at pf_create) is a schedule, not arithmetic: results are bitwise equal,
+    for the cluster kernel (K = 16), the one-CTA staged kernel (C4) and a 2-D volume, on ragged sizes with a
+    partial last strip / group."""
+    import dataclasses
+    cases = [(dataclasses.replace(P.config("C5"), classes=16).resized(100, 75, 21), 14),
+             (P.config("C4").resized(97, 70, 23), 14), (P.config("C1").resized(130, 50, 1), 14)]
+    for cfg, n in cases:
+        inp = P.generate(cfg)
+        ref = None
+        for order in ("", "2", "3", "-1", "-2", "-4", "-7"):
+            if order:
+                monkeypatch.setenv("PF_STRIP", order)
+            else:
+                monkeypatch.delenv("PF_STRIP", raising=False)
+            s = solver_from_inputs(inp)
+            r = s.iterate(n, residual=True)
+            got = (s.labeling()[0], s.flows(), r)
+            s.close()
+            if ref is None:
+                ref = got
+            else:
+                assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]) and got[2] == ref[2], \
+                    (cfg.name, order)
+    monkeypatch.delenv("PF_STRIP", raising=False)
+
+
 def test_cuda_graph_replay_equals_plain_launches(monkeypatch):
     """pf_iterate replays whole check periods as a CUDA graph; the result is bitwise that of plain launches
     (including the fused residual and odd check cadences), also after reset and mixed call sizes."""
